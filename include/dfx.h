@@ -1,0 +1,184 @@
+/*
+ * dfx.h -- C ABI of the B200 data-flow fixpoint engine (libdfx.so).
+ *
+ * Drop-in boundary for the hot path of the OMPDart host/device data-flow
+ * analysis (reference package `dartomp` 0.1.0, pure Python).  Each entry point
+ * below replaces one reference interface; the Python shim in
+ * `paper_2406_13881_b200/` (ctypes) keeps the reference signatures:
+ *
+ *   dfx_replay_batch   <- dartomp.dataflow.analyze_function
+ *                         (pkg/src/dartomp/dataflow.py:737-740), batched over
+ *                         functions (pipeline.plan_transform calls it once per
+ *                         function, pipeline.py:85-96).
+ *   dfx_summaries      <- dartomp.interproc.summarize_all
+ *                         (pkg/src/dartomp/interproc.py:90-144).
+ *   dfx_mfp_csr        <- the north-star CSR fixpoint (kernel a) plus the
+ *                         per-edge transfer-requirement kernel (kernel b); the
+ *                         gen/kill core of dataflow.py:299-378 with the AND meet
+ *                         of dataflow.py:130-134 on an explicit CSR graph.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Host-pointer entry
+ * points copy in and out themselves; `_dev` variants take device pointers
+ * that the caller owns.  All calls return 0 on success and a negative status
+ * otherwise; dfx_last_error() returns the message for the calling thread.
+ * A handle is bound to one CUDA device and is not thread-safe.
+ */
+#ifndef DFX_H
+#define DFX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFX_ABI_VERSION 1
+
+#define DFX_OK 0
+#define DFX_E_ARG (-1)
+#define DFX_E_CUDA (-2)
+#define DFX_E_NOSPC (-3)     /* output capacity too small; required size reported */
+#define DFX_E_LIMIT (-4)     /* program exceeds an engine limit */
+
+typedef struct dfx_handle dfx_handle;
+
+int dfx_abi_version(void);
+const char *dfx_last_error(void);
+int dfx_open(int device, dfx_handle **out);
+int dfx_close(dfx_handle *h);
+
+/* ------------------------------------------------------------------------ */
+/* E1: exact schedule replay of `_Analyzer` (dataflow.py:194-734)            */
+/* ------------------------------------------------------------------------ */
+
+/* opcodes: low 8 bits of op word 0; flags above (see lower.py) */
+enum {
+  DFX_OP_END = 0, DFX_OP_HR = 1, DFX_OP_HW = 2, DFX_OP_DR = 3, DFX_OP_DW = 4,
+  DFX_OP_BR_BEGIN = 5, DFX_OP_ARM_FORK = 6, DFX_OP_ARM_CLOSE = 7,
+  DFX_OP_ARM_PASSIVE = 8, DFX_OP_BR_END = 9, DFX_OP_LOOP_BEGIN = 10,
+  DFX_OP_LOOP_END = 11, DFX_OP_ERR = 12
+};
+#define DFX_F_AFTER_REGION (1 << 8)
+#define DFX_F_OVR (1 << 9)
+#define DFX_F_FP (1 << 10)
+#define DFX_F_CAPTURE (1 << 11)
+#define DFX_F_MAY_SKIP (1 << 12)
+
+/* per-variable flags (low 16 bits) | name rank << 16 */
+#define DFX_V_SCALAR 1
+#define DFX_V_ALLOW_STALE 2
+#define DFX_V_DECL_LATE 4
+#define DFX_V_NONLOCAL 8
+
+/* anchor codes in hoist tables */
+#define DFX_AC_NODE_MASK ((1 << 20) - 1)
+#define DFX_AC_ERR (1 << 20)
+#define DFX_AC_QUAL (1 << 21)
+#define DFX_AC_CLEAN (1 << 22)
+
+/* arm anchor kinds */
+enum { DFX_ARM_BEFORE = 0, DFX_ARM_AFTER = 1, DFX_ARM_ERR_ARM = 2, DFX_ARM_ERR_LOOP = 3 };
+
+/* plan positions (dataflow.py:47-52) */
+enum { DFX_POS_BEFORE = 0, DFX_POS_AFTER = 1, DFX_POS_BODY_END = 2, DFX_POS_KERNEL = 3 };
+
+/* event kinds */
+enum {
+  DFX_EV_UPDATE_FROM = 1, DFX_EV_UPDATE_TO = 2, DFX_EV_FIRSTPRIVATE = 3,
+  DFX_EV_SUPPRESS = 4,
+  DFX_EV_ERR_DATAMAP = 16,     /* PreconditionError, dataflow.py:459-463 */
+  DFX_EV_ERR_BRACES_LOOP = 17, /* PreconditionError, dataflow.py:291-294 */
+  DFX_EV_ERR_BRACES_ARM = 18,  /* PreconditionError, dataflow.py:554-557 */
+  DFX_EV_ERR_DECL = 19,        /* DeclPlacementError, dataflow.py:250-255 */
+  DFX_EV_ERR_ENGINE = 20       /* engine resource limit hit (slots) */
+};
+
+/* per-variable output bits */
+#define DFX_OUT_PRESENCE 1
+#define DFX_OUT_TO 2
+#define DFX_OUT_FROM 4
+#define DFX_OUT_H 8
+#define DFX_OUT_D 16
+
+typedef struct {
+  int32_t op_off, n_ops;       /* into ops (units of 4 int32) */
+  int32_t var_off, n_vars;     /* into var_flags / var_out */
+  int32_t stmt_off, n_stmts;   /* into stmt_span (units of 2 int32) */
+  int32_t site_off, arm_off;   /* into sites (int32) / arms (units of 2) */
+  int32_t region_begin_start;  /* -1: function has no kernels */
+  int32_t n_slots, max_loop_depth, max_br_depth, max_arms;
+  int32_t reserved[3];
+} dfx_fn_desc;
+
+typedef struct {
+  int32_t n_funcs;
+  const dfx_fn_desc *fns;
+  const int32_t *ops;
+  const int32_t *var_flags;
+  const int32_t *stmt_span;
+  const int32_t *sites;
+  const int32_t *arms;
+  int64_t n_ops, n_vars, n_stmts, n_sites, n_arms; /* array lengths, in units */
+} dfx_replay_in;
+
+typedef struct {
+  uint64_t key;     /* visit order: seq << 24 | name_rank << 8 | arm */
+  int32_t fn;
+  int32_t var;      /* function-local variable index */
+  int32_t node;     /* function-local statement id (anchor / error site) */
+  uint8_t kind;
+  uint8_t pos;
+  uint16_t pad;
+} dfx_event;
+
+typedef struct {
+  dfx_event *events;   /* capacity event_cap */
+  int64_t event_cap;
+  int64_t n_events;    /* out: events produced (may exceed cap -> DFX_E_NOSPC) */
+  uint8_t *var_out;    /* [n_vars] DFX_OUT_* bits */
+  float kernel_ms;     /* out: device time of the replay kernel */
+} dfx_replay_out;
+
+/* Host buffers in, host buffers out (H2D + kernel + D2H). */
+int dfx_replay_batch(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
+
+/* ------------------------------------------------------------------------ */
+/* Kernels (a)+(b): CSR fixpoint and per-edge transfer requirements          */
+/* ------------------------------------------------------------------------ */
+
+/* Node-major bitplanes: plane[node * words + w], bit b of word w = var 32w+b.
+ * Node kinds: 0 host, 1 kernel.  Transfer functions per node:
+ *   host:   H' = H | GEN_H ;           D' = D & ~KILL_D
+ *   kernel: H' = H & ~KILL_H ;         D' = D | GEN_D | (FPC & ~H_in)
+ * expressed uniformly as two planes per node: (A, B) = (GEN_H, KILL_D) for
+ * host nodes and (GEN_D | FPC-bit-holder, KILL_H) for kernel nodes; see
+ * DESIGN.md §E2 for the encoding and csrc/mfp.cu for the kernels. */
+typedef struct {
+  int64_t n_nodes;
+  int32_t words;               /* V / 32 (multiple of 4) */
+  const int32_t *row_ptr;      /* [n+1] predecessor CSR */
+  const int32_t *col;          /* [nnz]  predecessor ids */
+  const uint8_t *node_kind;    /* [n] */
+  const uint32_t *gen;         /* [n*words] */
+  const uint32_t *kill;        /* [n*words] */
+  const uint32_t *use;         /* [n*words] host: HR bits, kernel: DR bits */
+  const uint32_t *fpc;         /* [n*words] kernel nodes: FPC-eligible DR bits */
+} dfx_csr_in;
+
+typedef struct {
+  uint32_t *out_h;             /* [n*words] fixpoint OUT planes (optional) */
+  uint32_t *out_d;
+  /* per-edge requirement records (kernel b) */
+  int64_t rec_cap;
+  int64_t n_rec;               /* out */
+  int32_t *rec_dst, *rec_src, *rec_word; uint8_t *rec_kind; uint32_t *rec_mask;
+  int32_t rounds;              /* out: rounds to fixpoint (both phases) */
+  float kernel_ms;             /* out: device time of the solve */
+} dfx_csr_out;
+
+int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_csr_out *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFX_H */

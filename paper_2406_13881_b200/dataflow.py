@@ -1,0 +1,322 @@
+"""Drop-in `analyze_function` backed by the E1 replay engine.
+
+`analyze_function(src, cfg, accesses, table, allow_stale)` keeps the reference
+signature and return type (`dartomp/dataflow.py:737-740`): a
+`dartomp.dataflow.FunctionPlan` whose anchors are the very `AstNode` objects
+of the caller's AST, so `dartomp.rewriter.apply_plans` and
+`dartomp.report.plan_lines` consume it unchanged.  `analyze_functions` is the
+batched form (one engine launch for many functions; SURVEY §8 b).
+
+Pipeline per batch: host lowering (`lower.py`) -> pack into flat arrays ->
+`dfx_replay_batch` (CUDA, `csrc/replay.cu`) -> events sorted by visit key ->
+`_finish` restated on name sets (`dataflow.py:678-711`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._host import import_dartomp
+from .lower import FnProgram, lower_function
+
+import_dartomp()
+from dartomp.access import Storage  # noqa: E402
+from dartomp.dataflow import (AFTER, BEFORE, BODY_END, KERNEL,  # noqa: E402
+                              DirectivePlan, FunctionPlan, PlanKind,
+                              TargetDataRegion)
+from dartomp.diagnostics import DeclPlacementError, PreconditionError  # noqa: E402
+
+_POS = {_abi.POS_BEFORE: BEFORE, _abi.POS_AFTER: AFTER,
+        _abi.POS_BODY_END: BODY_END, _abi.POS_KERNEL: KERNEL}
+
+
+@dataclass
+class PackedBatch:
+    fns: np.ndarray        # FN_DESC_DTYPE
+    ops: np.ndarray
+    var_flags: np.ndarray
+    stmt_span: np.ndarray
+    sites: np.ndarray
+    arms: np.ndarray
+
+    @property
+    def n_vars(self) -> int:
+        return int(self.var_flags.shape[0])
+
+    def replay_in(self) -> _abi.ReplayIn:
+        r = _abi.ReplayIn()
+        r.n_funcs = int(self.fns.shape[0])
+        r.fns = _abi.ptr(self.fns)
+        r.ops = _abi.ptr(self.ops)
+        r.var_flags = _abi.ptr(self.var_flags)
+        r.stmt_span = _abi.ptr(self.stmt_span)
+        r.sites = _abi.ptr(self.sites)
+        r.arms = _abi.ptr(self.arms)
+        r.n_ops = int(self.ops.shape[0])
+        r.n_vars = int(self.var_flags.shape[0])
+        r.n_stmts = int(self.stmt_span.shape[0])
+        r.n_sites = int(self.sites.shape[0])
+        r.n_arms = int(self.arms.shape[0])
+        return r
+
+
+def pack(progs: list[FnProgram]) -> PackedBatch:
+    """Concatenate lowered programs into the flat arrays of `dfx_replay_in`."""
+    n = len(progs)
+    fns = np.zeros(n, dtype=_abi.FN_DESC_DTYPE)
+    op_off = var_off = stmt_off = site_off = arm_off = 0
+    for i, p in enumerate(progs):
+        d = fns[i]
+        d["op_off"], d["n_ops"] = op_off, p.ops.shape[0]
+        d["var_off"], d["n_vars"] = var_off, p.var_flags.shape[0]
+        d["stmt_off"], d["n_stmts"] = stmt_off, p.stmt_span.shape[0]
+        d["site_off"], d["arm_off"] = site_off, arm_off
+        d["region_begin_start"] = p.region_begin_start
+        d["n_slots"] = p.n_slots
+        d["max_loop_depth"] = p.max_loop_depth
+        d["max_br_depth"] = p.max_br_depth
+        d["max_arms"] = p.max_arms
+        op_off += p.ops.shape[0]
+        var_off += p.var_flags.shape[0]
+        stmt_off += p.stmt_span.shape[0]
+        site_off += p.sites.shape[0]
+        arm_off += p.arms.shape[0] // 2
+
+    def cat(arrs, shape_tail, dtype=np.int32):
+        arrs = [a.reshape((-1,) + shape_tail) for a in arrs]
+        if not arrs:
+            return np.zeros((0,) + shape_tail, dtype=dtype)
+        return np.ascontiguousarray(np.concatenate(arrs).astype(dtype, copy=False))
+
+    return PackedBatch(
+        fns=fns,
+        ops=cat([p.ops for p in progs], (4,)),
+        var_flags=cat([p.var_flags for p in progs], ()),
+        stmt_span=cat([p.stmt_span for p in progs], (2,)),
+        sites=cat([p.sites for p in progs], ()),
+        arms=cat([p.arms for p in progs], ()),
+    )
+
+
+@dataclass
+class RawResult:
+    events: np.ndarray     # EVENT_DTYPE, all functions
+    var_out: np.ndarray    # uint8 per packed variable
+    kernel_ms: float
+
+
+def run_replay(batch: PackedBatch, runner=None, event_cap: int | None = None) -> RawResult:
+    """Execute a packed batch.  `runner(in, out) -> rc` defaults to the CUDA
+    engine's `dfx_replay_batch`; tests pass the CPU oracle's entry point."""
+    if runner is None:
+        eng = _abi.engine()
+
+        def runner(rin, rout):
+            return eng.check(eng.lib.dfx_replay_batch(eng.h, C.byref(rin), C.byref(rout)),
+                             "dfx_replay_batch")
+    cap = event_cap if event_cap is not None else max(1024, 4 * int(batch.ops.shape[0]))
+    while True:
+        events = np.zeros(cap, dtype=_abi.EVENT_DTYPE)
+        var_out = np.zeros(max(1, batch.n_vars), dtype=np.uint8)
+        rin = batch.replay_in()
+        rout = _abi.ReplayOut()
+        rout.events = _abi.ptr(events)
+        rout.event_cap = cap
+        rout.var_out = _abi.ptr(var_out)
+        rc = runner(rin, rout)
+        if rc == _abi.DFX_E_NOSPC or rout.n_events > cap:
+            cap = int(rout.n_events) + 16
+            continue
+        if rc != 0:
+            raise _abi.EngineError("replay failed with status %d" % rc)
+        return RawResult(events=events[:rout.n_events].copy(),
+                         var_out=var_out[:batch.n_vars].copy(),
+                         kernel_ms=float(rout.kernel_ms))
+
+
+# ---- decoding --------------------------------------------------------------
+
+def _raise_error(prog: FnProgram, src, ev) -> None:
+    kind = int(ev["kind"])
+    if kind == _abi.EV_ERR_DATAMAP:
+        stmt = prog.stmts[int(ev["node"])]
+        raise PreconditionError(
+            "input already contains a '%s' directive; analysis expects "
+            "unmapped offload regions" % stmt.omp.kind.value,
+            path=src.path, line=src.line_of(stmt.span.start))
+    if kind == _abi.EV_ERR_BRACES_LOOP:
+        node = prog.stmts[int(ev["node"])]
+        raise PreconditionError.at(
+            src, node.span.start,
+            "braces are required around this loop body to place an "
+            "update directive")
+    if kind == _abi.EV_ERR_BRACES_ARM:
+        node = prog.stmts[int(ev["node"])]
+        raise PreconditionError.at(
+            src, node.span.start,
+            "braces are required around this branch arm to place an "
+            "update directive")
+    if kind == _abi.EV_ERR_DECL:
+        var = prog.vars[int(ev["var"])]
+        begin = prog.region[1]
+        begin_line = src.line_of(begin.span.start)
+        decl_line = src.line_of(var.decl.span.start)
+        raise DeclPlacementError(
+            "'%s' needs a device mapping but is declared at line %d, "
+            "after the data region opening at line %d; move the "
+            "declaration above the region" % (var.name, decl_line, begin_line),
+            path=src.path, line=decl_line)
+    raise _abi.EngineError("replay engine resource limit hit in %s (event kind %d)"
+                           % (prog.fn.name, kind))
+
+
+def decode(prog: FnProgram, src, accesses, events: np.ndarray,
+           var_out: np.ndarray) -> FunctionPlan:
+    """Events of one function (any order) + per-variable bits -> FunctionPlan."""
+    if events.shape[0]:
+        events = events[np.argsort(events["key"], kind="stable")]
+        errs = events[events["kind"] >= _abi.EV_ERR_DATAMAP]
+        if errs.shape[0]:
+            _raise_error(prog, src, errs[0])
+    updates: list = []
+    firstprivates: list = []
+    suppressed: list[str] = []
+    keys: set = set()
+    for ev in events:
+        kind = int(ev["kind"])
+        var = prog.vars[int(ev["var"])]
+        if kind == _abi.EV_SUPPRESS:
+            if var.name not in suppressed:
+                suppressed.append(var.name)
+            continue
+        anchor = prog.stmts[int(ev["node"])]
+        pos = _POS[int(ev["pos"])]
+        pk = {_abi.EV_UPDATE_FROM: PlanKind.UPDATE_FROM,
+              _abi.EV_UPDATE_TO: PlanKind.UPDATE_TO,
+              _abi.EV_FIRSTPRIVATE: PlanKind.FIRSTPRIVATE}[kind]
+        key = (pk, var.name, id(anchor), pos)           # `dataflow.py:264`
+        if key in keys:
+            continue
+        keys.add(key)
+        bucket = firstprivates if pk is PlanKind.FIRSTPRIVATE else updates
+        bucket.append(DirectivePlan(pk, (var.name,), anchor, pos))
+    # sets (`dataflow.py:214-216`) and `_escape_liveness` (`:671-676`)
+    presence, to_comp, from_comp = set(), set(), set()
+    for i, var in enumerate(prog.vars):
+        o = int(var_out[i])
+        if o & _abi.OUT_PRESENCE:
+            presence.add(var)
+            if (o & _abi.OUT_D) and not (o & _abi.OUT_H) \
+                    and var.storage is not Storage.LOCAL:
+                from_comp.add(var)
+        if o & _abi.OUT_TO:
+            to_comp.add(var)
+        if o & _abi.OUT_FROM:
+            from_comp.add(var)
+    return _finish(prog, src, accesses, presence, to_comp, from_comp,
+                   updates, firstprivates, suppressed)
+
+
+def _finish(prog, src, accesses, presence, to_comp, from_comp, updates,
+            firstprivates, suppressed) -> FunctionPlan:
+    """`_Analyzer._finish` (`dataflow.py:678-711`)."""
+    fn = prog.fn
+    if not prog.kernel_stmts:
+        return FunctionPlan(fn, None, [], [], suppressed)
+    block, begin, end = prog.region
+    to_names = {v.name for v in to_comp}
+    from_names = {v.name for v in from_comp}
+    tofrom = sorted(to_names & from_names)
+    to_only = sorted(to_names - from_names)
+    from_only = sorted(from_names - to_names)
+    alloc = sorted({v.name for v in presence} - to_names - from_names)
+    kernel_clauses = list(firstprivates)
+    single = (len(prog.kernel_stmts) == 1
+              and begin is prog.kernel_stmts[0]
+              and end is prog.kernel_stmts[0]
+              and not updates)
+    region = None
+    if single:
+        k = prog.kernel_stmts[0]
+        for kind, names in ((PlanKind.MAP_TO, to_only),
+                            (PlanKind.MAP_TOFROM, tofrom),
+                            (PlanKind.MAP_FROM, from_only),
+                            (PlanKind.MAP_ALLOC, alloc)):
+            if names:
+                kernel_clauses.append(DirectivePlan(kind, tuple(names), k, KERNEL))
+    elif presence or updates:
+        _check_region_scoping(src, accesses, begin, end)
+        region = TargetDataRegion(block=block, begin=begin, end=end,
+                                  map_to=tuple(to_only), map_from=tuple(from_only),
+                                  map_tofrom=tuple(tofrom), map_alloc=tuple(alloc))
+    return FunctionPlan(fn, region, kernel_clauses, updates, suppressed)
+
+
+def _check_region_scoping(src, accesses, begin, end) -> None:
+    """`_Analyzer._check_region_scoping` (`dataflow.py:713-734`)."""
+    lo = begin.span.start
+    hi = end.span.end
+    inside = {}
+    for acc in accesses:
+        d = acc.var.decl
+        if d is None or not (lo <= d.span.start < hi):
+            continue
+        if acc.ast.span.start >= hi and acc.ast is not d:
+            inside.setdefault(acc.var, acc)
+    for var, acc in sorted(inside.items(), key=lambda kv: kv[0].name):
+        raise DeclPlacementError.at(
+            src, var.decl.span.start,
+            "'%s' is declared at line %d inside the new data region "
+            "(lines %d..%d) but used at line %d after it; move the "
+            "declaration above the region" % (
+                var.name, src.line_of(var.decl.span.start),
+                src.line_of(lo), src.line_of(hi - 1),
+                src.line_of(acc.ast.span.start)))
+
+
+# ---- public API --------------------------------------------------------------
+
+class _Deferred:
+    """Per-function result: a FunctionPlan or the exception the reference raises."""
+
+    def __init__(self, plan=None, error=None):
+        self.plan = plan
+        self.error = error
+
+    def get(self):
+        if self.error is not None:
+            raise self.error
+        return self.plan
+
+
+def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
+                      runner=None) -> list[_Deferred]:
+    """Batched `analyze_function`: `items` is a list of
+    `(src, cfg, accesses, table)`; one engine launch for all of them.
+    Returns one deferred result per item (`.get()` returns the
+    `FunctionPlan` or raises the reference's exception)."""
+    progs = [lower_function(src, cfg, accs, table, allow_stale)
+             for src, cfg, accs, table in items]
+    batch = pack(progs)
+    raw = run_replay(batch, runner=runner)
+    order = np.argsort(raw.events["fn"], kind="stable")
+    evs = raw.events[order]
+    bounds = np.searchsorted(evs["fn"], np.arange(len(progs) + 1))
+    out = []
+    for i, (p, (src, cfg, accs, table)) in enumerate(zip(progs, items)):
+        d = batch.fns[i]
+        vo = raw.var_out[int(d["var_off"]):int(d["var_off"]) + int(d["n_vars"])]
+        try:
+            out.append(_Deferred(plan=decode(p, src, accs, evs[bounds[i]:bounds[i + 1]], vo)))
+        except Exception as e:  # the reference's ToolError subclasses
+            out.append(_Deferred(error=e))
+    return out
+
+
+def analyze_function(src, cfg, accesses, table,
+                     allow_stale: frozenset[str] = frozenset()) -> FunctionPlan:
+    """Drop-in for `dartomp.dataflow.analyze_function` (`dataflow.py:737`)."""
+    return analyze_functions([(src, cfg, accesses, table)], allow_stale)[0].get()

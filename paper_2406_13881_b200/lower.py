@@ -1,0 +1,628 @@
+"""Host lowering: compile one function into an E1 replay program.
+
+The reference analysis (`dartomp/dataflow.py:194-734`, `_Analyzer`) is a
+syntax-directed abstract interpreter: it walks the AST in execution order,
+forks and re-joins per-variable (host-valid, device-valid) state at branches,
+and runs every loop body twice (dry round, weaken, planning round).  The
+traversal order, the branch/loop structure and every per-access decision that
+does not depend on run-time state are *static*; only the validity flags and
+the two provenance maps (`device_producer`, `last_host_write`) are dynamic.
+
+This module performs that static part once, on the host, and emits a compact
+structured bytecode (one op per access, plus branch/loop control ops).  The
+dynamic part -- per-variable state, slot aliasing (D4), the 2^depth loop
+replay (F4), reconcile joins (D1), firstprivate (D2), the zero-trip skip merge
+(D3), and the in-kernel Algorithm-1 hoisting against the dynamic `loc_lim`
+(`bounds.py:134-193`) -- is executed by the replay engine (CUDA kernel in
+`csrc/replay.cu`; CPU restatement in `oracle/replay_oracle.c`), one lane per
+variable, which is exact because the analysis separates per variable
+(SURVEY F3).
+
+Opcode set (each op is four int32 words: ``op|flags<<8, a, b, c``):
+
+=============  =========================================================
+HR  var stmt site|anchor   host_read   (`dataflow.py:299-324`)
+HW  var stmt               host_write  (`dataflow.py:326-330`)
+DR  var stmt site|anchor   device_read (`dataflow.py:332-368`)
+DW  var stmt               device_write (`dataflow.py:370-378`)
+BR_BEGIN                   push branch frame, saved = cur
+ARM_FORK                   cur = copy(saved); F_CAPTURE: arms += [cur]
+ARM_CLOSE                  arms += [cur]  (switch: arm = slot at group end)
+ARM_PASSIVE                arms += [copy(saved)] (absent else / default)
+BR_END   armtab n          `_merge_arms` (`dataflow.py:525-564`); cur = arm0
+LOOP_BEGIN loopstmt        `_loop_rounds` (`dataflow.py:566-590`) entry
+LOOP_END  bodypc           dry->plan round switch, skip merge
+ERR  kind node             statically-known error at this visit
+=============  =========================================================
+"""
+from __future__ import annotations
+
+import bisect
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._host import import_dartomp
+
+import_dartomp()
+from dartomp.access import (AccessKind, Space, Storage,  # noqa: E402
+                            enclosing_statement, kernel_rw_sets, reads, writes)
+from dartomp.bounds import (enclosing_for_loops, find_indexing_var,  # noqa: E402
+                            subscript_index_vars)
+from dartomp.dataflow import compute_region_extent  # noqa: E402
+from dartomp.nodes import NodeKind  # noqa: E402
+from dartomp.omp import DATA_MAPPING_KINDS  # noqa: E402
+
+# ---- opcodes (must match include/dfx.h) ----------------------------------
+OP_END = 0
+OP_HR = 1
+OP_HW = 2
+OP_DR = 3
+OP_DW = 4
+OP_BR_BEGIN = 5
+OP_ARM_FORK = 6
+OP_ARM_CLOSE = 7
+OP_ARM_PASSIVE = 8
+OP_BR_END = 9
+OP_LOOP_BEGIN = 10
+OP_LOOP_END = 11
+OP_ERR = 12
+
+F_AFTER_REGION = 1 << 8   # HR: statement lies after the data region
+F_OVR = 1 << 9            # HR/DR: anchor override (BODY_END, c = loop stmt)
+F_FP = 1 << 10            # DR: firstprivate-eligible (scalar, not kernel-written, kernel stmt)
+F_CAPTURE = 1 << 11       # ARM_FORK: the forked slot itself is the arm (if-arms, D4)
+F_MAY_SKIP = 1 << 12      # LOOP_BEGIN: for/while (zero-trip skip merge, D3)
+
+# ---- per-variable flags ----------------------------------------------------
+V_SCALAR = 1
+V_ALLOW_STALE = 2
+V_DECL_LATE = 4           # check_decl_placement would raise (`dataflow.py:242-255`)
+V_NONLOCAL = 8            # storage is not LOCAL (`_escape_liveness`, `dataflow.py:671-676`)
+
+# ---- anchor codes (hoist tables and arm anchors) ---------------------------
+AC_NODE_MASK = (1 << 20) - 1
+AC_ERR = 1 << 20          # the node is the one `_normalize_anchor` failed at
+AC_QUAL = 1 << 21         # loop's induction variable indexes the subscript
+AC_CLEAN = 1 << 22        # no write to the variable in [loop.start, read)
+
+# arm anchor kinds
+ARM_BEFORE = 0
+ARM_AFTER = 1
+ARM_ERR_ARM = 2           # "braces are required around this branch arm"
+ARM_ERR_LOOP = 3          # `_normalize_anchor` failed ("... loop body ...")
+
+# static error kinds (OP_ERR) and event kinds (must match include/dfx.h)
+ERR_DATAMAP = 1
+
+POS_BEFORE = 0
+POS_AFTER = 1
+POS_BODY_END = 2
+POS_KERNEL = 3
+
+MAX_STMTS = 0xFFFE        # provenance ids are uint16 with 0xFFFF = none
+
+
+class LoweringError(Exception):
+    pass
+
+
+def _clause_names(info, clause: str) -> set[str]:
+    """Names listed in one clause kind (restates `dataflow.py:145-155`)."""
+    names: set[str] = set()
+    for cl in info.clauses:
+        if cl.name != clause:
+            continue
+        for arg in cl.args:
+            if ":" in arg:
+                arg = arg.split(":", 1)[1]
+            if arg.strip():
+                names.add(arg.strip())
+    return names
+
+
+_JUMPS = (NodeKind.RETURN_STMT, NodeKind.BREAK_STMT, NodeKind.CONTINUE_STMT)
+
+
+@dataclass
+class FnProgram:
+    """One function's lowered replay program plus what the host needs to
+    turn engine events back into a `FunctionPlan`."""
+
+    fn: object
+    ops: np.ndarray                      # [n_ops, 4] int32
+    var_flags: np.ndarray                # [n_vars] int32 (flags | name_rank << 16)
+    stmt_span: np.ndarray                # [n_stmts, 2] int32 (start, end)
+    sites: np.ndarray                    # flat int32 hoist tables
+    arms: np.ndarray                     # flat int32 (kind, node) pairs
+    region_begin_start: int              # -1 when the function has no kernels
+    n_slots: int
+    max_loop_depth: int
+    max_br_depth: int
+    max_arms: int
+    vars: list = field(default_factory=list)
+    stmts: list = field(default_factory=list)
+    kernel_stmts: list = field(default_factory=list)
+    region: tuple | None = None          # (block, begin, end)
+
+    @property
+    def n_vars(self) -> int:
+        return len(self.vars)
+
+
+class _Lowerer:
+    """Static half of `_Analyzer` (`dataflow.py:194-734`)."""
+
+    def __init__(self, src, cfg, accesses, table, allow_stale=frozenset()):
+        self.src = src
+        self.cfg = cfg
+        self.fn = cfg.function
+        self.accesses = accesses
+        self.table = table
+        self.allow_stale = allow_stale
+        # `dataflow.py:204-212`
+        self.kernel_node_ids = {n.id for n in cfg.kernel_nodes()}
+        self.kernel_stmts = [cfg.node(i).ast for i in sorted(self.kernel_node_ids)]
+        self.kernel_stmts.sort(key=lambda n: n.span.start)
+        self.stmt_groups: dict = {}
+        for acc in accesses:
+            if acc.space is Space.DEVICE and acc.cfg_node in self.kernel_node_ids:
+                continue
+            stmt = enclosing_statement(acc.ast)
+            self.stmt_groups.setdefault(stmt, []).append(acc)
+        self.region_block = self.region_begin = self.region_end = None
+        if self.kernel_stmts:
+            self.region_block, self.region_begin, self.region_end = \
+                compute_region_extent(self.fn, self.kernel_stmts)
+        # write positions per variable, for the static `writes_between`
+        # (`bounds.py:160-165`) queries of Algorithm-1 finalisation
+        self._write_pos: dict[int, list[int]] = {}
+        for acc in accesses:
+            if writes(acc.kind):
+                self._write_pos.setdefault(id(acc.var), []).append(acc.ast.span.start)
+        for v in self._write_pos.values():
+            v.sort()
+        self.ops: list[tuple[int, int, int, int]] = []
+        self.sites: list[int] = []
+        self.arms: list[int] = []
+        self.var_index: dict[int, int] = {}
+        self.vars: list = []
+        self.stmt_index: dict[int, int] = {}
+        self.stmts: list = []
+        self._site_cache: dict = {}
+        self._norm_cache: dict = {}
+        # structural bounds for engine resources
+        self.loop_depth = 0
+        self.max_loop_depth = 0
+        self.br_depth = 0
+        self.max_br_depth = 0
+        self.max_arms = 0
+        self.live = 1       # slot references held (cur)
+        self.max_live = 1
+
+    # ---- interning ------------------------------------------------------
+    def sid(self, node) -> int:
+        k = id(node)
+        i = self.stmt_index.get(k)
+        if i is None:
+            i = len(self.stmts)
+            if i >= MAX_STMTS:
+                raise LoweringError("function has more than %d statements" % MAX_STMTS)
+            self.stmt_index[k] = i
+            self.stmts.append(node)
+        return i
+
+    def vid(self, var) -> int:
+        k = id(var)
+        i = self.var_index.get(k)
+        if i is None:
+            i = len(self.vars)
+            self.var_index[k] = i
+            self.vars.append(var)
+        return i
+
+    def emit(self, op: int, a: int = 0, b: int = 0, c: int = 0) -> int:
+        self.ops.append((op, a, b, c))
+        return len(self.ops) - 1
+
+    # ---- region geometry (`dataflow.py:231-240`) ------------------------
+    def in_region(self, stmt) -> bool:
+        if self.region_begin is None:
+            return False
+        return (stmt.span.start >= self.region_begin.span.start
+                and stmt.span.end <= self.region_end.span.end)
+
+    def after_region(self, stmt) -> bool:
+        if self.region_end is None:
+            return False
+        return stmt.span.start > self.region_end.span.end
+
+    # ---- anchors ---------------------------------------------------------
+    def norm_code(self, anchor) -> int:
+        """`_normalize_anchor` (`dataflow.py:278-295`) as a static code."""
+        k = id(anchor)
+        if k in self._norm_cache:
+            return self._norm_cache[k]
+        node = anchor
+        code = None
+        while node.parent is not None:
+            p = node.parent
+            if p.kind in (NodeKind.COMPOUND_STMT, NodeKind.FUNCTION_DEF):
+                code = self.sid(node)
+                break
+            if p.kind in (NodeKind.IF_STMT, NodeKind.OMP_DIRECTIVE, NodeKind.SWITCH_STMT):
+                node = p
+                continue
+            if p.kind is NodeKind.FOR_STMT and node is not p.body:
+                node = p
+                continue
+            code = self.sid(node) | AC_ERR
+            break
+        if code is None:
+            code = self.sid(node)
+        self._norm_cache[k] = code
+        return code
+
+    def writes_between(self, var, begin: int, end: int) -> bool:
+        pos = self._write_pos.get(id(var))
+        if not pos:
+            return False
+        i = bisect.bisect_left(pos, begin)
+        return i < len(pos) and pos[i] < end
+
+    def site(self, access_stmt, subscript, var) -> int:
+        """Static Algorithm-1 table for one (read site, variable).
+
+        `_hoist` = `find_update_insert_loc` (`bounds.py:134-157`) +
+        `finalize_update_anchor` (`bounds.py:168-193`) + `_normalize_anchor`;
+        only `loc_lim` is dynamic, so per enclosing for-level we store the
+        loop start, whether its induction variable indexes the subscript, and
+        whether the variable is written in [loop.start, read) -- the engine
+        picks the level from `loc_lim` at run time.
+        """
+        key = (id(access_stmt), id(subscript), id(var))
+        off = self._site_cache.get(key)
+        if off is not None:
+            return off
+        off = len(self.sites)
+        acc_code = self.norm_code(access_stmt)
+        if subscript is None:
+            self.sites.extend([0, acc_code])
+        else:
+            loops = enclosing_for_loops(access_stmt, stop_at=self.fn)
+            idx_vars = subscript_index_vars(subscript)
+            read_pos = access_stmt.span.start
+            self.sites.extend([len(loops), acc_code])
+            for f in loops:
+                code = self.norm_code(f)
+                v = find_indexing_var(f)
+                if v is not None and v in idx_vars:
+                    code |= AC_QUAL
+                if not self.writes_between(var, f.span.start, read_pos):
+                    code |= AC_CLEAN
+                self.sites.extend([f.span.start, code])
+        self._site_cache[key] = off
+        return off
+
+    def device_read_subscript(self, var, kernel_stmt):
+        """`_device_read_subscript` (`dataflow.py:380-390`)."""
+        node = self.cfg.node_of_ast.get(kernel_stmt)
+        if node is None:
+            return None
+        for acc in self.accesses:
+            if (acc.cfg_node == node.id and acc.space is Space.DEVICE
+                    and acc.var is var and reads(acc.kind)
+                    and acc.subscript is not None):
+                return acc.subscript
+        return None
+
+    # ---- access ops ------------------------------------------------------
+    def op_hr(self, var, stmt, subscript, override):
+        flags = OP_HR
+        if self.after_region(stmt):
+            flags |= F_AFTER_REGION
+        if override is not None:
+            flags |= F_OVR
+            c = self.sid(override)
+        else:
+            c = self.site(stmt, subscript, var)
+        self.emit(flags, self.vid(var), self.sid(stmt), c)
+
+    def op_dr(self, var, stmt, kernel_writes, override):
+        flags = OP_DR
+        if (var.is_scalar and var not in kernel_writes
+                and stmt.kind is NodeKind.OMP_DIRECTIVE):
+            flags |= F_FP
+        if override is not None:
+            flags |= F_OVR
+            c = self.sid(override)
+        else:
+            c = self.site(stmt, self.device_read_subscript(var, stmt), var)
+        self.emit(flags, self.vid(var), self.sid(stmt), c)
+
+    def op_hw(self, var, stmt):
+        self.emit(OP_HW, self.vid(var), self.sid(stmt), 0)
+
+    def op_dw(self, var, stmt):
+        self.emit(OP_DW, self.vid(var), self.sid(stmt), 0)
+
+    # ---- traversal (mirrors `dataflow.py:394-667`) -------------------------
+    def run(self) -> None:
+        body = self.fn.body
+        if body is not None:
+            self.exec_block(body)
+        self.emit(OP_END)
+
+    def exec_block(self, block) -> None:
+        for stmt in block.children:
+            self.exec_stmt(stmt)
+
+    def group(self, stmt):
+        return self.stmt_groups.get(stmt, [])
+
+    def accs_in(self, stmt, sub):
+        return [a for a in self.group(stmt)
+                if sub.span.start <= a.ast.span.start < sub.span.end]
+
+    def process_accesses(self, stmt, accs, override=None) -> None:
+        inside = self.in_region(stmt)
+        for acc in accs:
+            if acc.kind is AccessKind.UNKNOWN:
+                continue
+            space = acc.space
+            if space is Space.DEVICE and not inside:
+                space = Space.HOST
+            if space is Space.HOST:
+                if reads(acc.kind):
+                    self.op_hr(acc.var, stmt, acc.subscript, override)
+                if writes(acc.kind):
+                    self.op_hw(acc.var, stmt)
+            else:
+                if reads(acc.kind):
+                    self.op_dr(acc.var, stmt, frozenset(), override)
+                if writes(acc.kind):
+                    self.op_dw(acc.var, stmt)
+
+    def exec_stmt(self, stmt) -> None:
+        kind = stmt.kind
+        if kind is NodeKind.COMPOUND_STMT:
+            self.exec_block(stmt)
+        elif kind is NodeKind.OMP_DIRECTIVE:
+            self.exec_omp(stmt)
+        elif kind is NodeKind.IF_STMT:
+            self.exec_if(stmt)
+        elif kind is NodeKind.FOR_STMT:
+            self.exec_for(stmt)
+        elif kind is NodeKind.WHILE_STMT:
+            self.exec_while(stmt)
+        elif kind is NodeKind.DO_STMT:
+            self.exec_do(stmt)
+        elif kind is NodeKind.SWITCH_STMT:
+            self.exec_switch(stmt)
+        else:
+            self.process_accesses(stmt, self.group(stmt))
+
+    def exec_omp(self, stmt) -> None:
+        info = stmt.omp
+        if info.kind in DATA_MAPPING_KINDS:
+            self.emit(OP_ERR, ERR_DATAMAP, self.sid(stmt), 0)
+            return
+        node = self.cfg.node_of_ast.get(stmt)
+        if node is None or node.sub_cfg is None:
+            if stmt.children:
+                self.exec_stmt(stmt.children[0])
+            return
+        entry_reads, kernel_writes = kernel_rw_sets(self.accesses, node.id, stmt)
+        kw = set(kernel_writes)
+        captured = _clause_names(info, "firstprivate")
+        private = _clause_names(info, "private") | _clause_names(info, "linear")
+        for f in stmt.find_all(NodeKind.FOR_STMT):
+            v = find_indexing_var(f)
+            if v is not None:
+                private.add(v)
+        for var in sorted(entry_reads, key=lambda v: v.name):
+            if var.name in private:
+                continue
+            if var.name in captured:
+                self.op_hr(var, stmt, None, None)
+                continue
+            self.op_dr(var, stmt, kw, None)
+        for var in sorted(kernel_writes, key=lambda v: v.name):
+            if var.name in private or var.name in captured:
+                continue
+            self.op_dw(var, stmt)
+        extra = list(self.group(stmt))
+        if extra:
+            self.process_accesses(stmt, extra)
+
+    # -- branches --
+    def _br_begin(self):
+        self.emit(OP_BR_BEGIN)
+        self.br_depth += 1
+        self.max_br_depth = max(self.max_br_depth, self.br_depth)
+        self.live += 1                      # saved
+
+    def _hold(self, n=1):
+        self.live += n
+        self.max_live = max(self.max_live, self.live + 1)
+
+    def _br_end(self, anchors) -> None:
+        off = len(self.arms)
+        for a in anchors:
+            self.arms.extend(a)
+        self.emit(OP_BR_END, off // 2, len(anchors), 0)
+        self.br_depth -= 1
+        self.max_arms = max(self.max_arms, len(anchors))
+        self.live -= 1 + len(anchors)       # saved + arms released, cur kept
+
+    def arm_anchor(self, arm, branch_stmt):
+        """`_arm_anchor` (`dataflow.py:512-523`) with the `None` case already
+        resolved to `(BEFORE, normalize(branch))` (`dataflow.py:551-552`)."""
+        if arm is None:
+            return self._none_anchor(branch_stmt)
+        if arm.kind is NodeKind.COMPOUND_STMT:
+            if not arm.children:
+                return self._none_anchor(branch_stmt)
+            last = arm.children[-1]
+            if last.kind in _JUMPS:
+                return (ARM_BEFORE, self.sid(last))
+            return (ARM_AFTER, self.sid(last))
+        if arm.kind in _JUMPS:
+            return self._none_anchor(branch_stmt)
+        return (ARM_ERR_ARM, self.sid(arm))
+
+    def _none_anchor(self, branch_stmt):
+        code = self.norm_code(branch_stmt)
+        if code & AC_ERR:
+            return (ARM_ERR_LOOP, code & AC_NODE_MASK)
+        return (ARM_BEFORE, code)
+
+    def group_anchor(self, group, branch_stmt):
+        """`_group_anchor` (`dataflow.py:661-667`)."""
+        if not group:
+            return self._none_anchor(branch_stmt)
+        last = group[-1]
+        if last.kind in _JUMPS:
+            return (ARM_BEFORE, self.sid(last))
+        return (ARM_AFTER, self.sid(last))
+
+    def exec_if(self, stmt) -> None:
+        self.process_accesses(stmt, self.group(stmt))
+        self._br_begin()
+        self.emit(OP_ARM_FORK | F_CAPTURE)
+        self._hold(2)                       # arm0 + new cur
+        self.exec_stmt(stmt.then_branch)
+        anchors = [self.arm_anchor(stmt.then_branch, stmt)]
+        if stmt.else_branch is not None:
+            self.emit(OP_ARM_FORK | F_CAPTURE)
+            self._hold(2)
+            self.exec_stmt(stmt.else_branch)
+            anchors.append(self.arm_anchor(stmt.else_branch, stmt))
+            self.live -= 1
+        else:
+            self.emit(OP_ARM_PASSIVE)
+            self._hold(1)
+            anchors.append(self._none_anchor(stmt))
+        self.live -= 1
+        self._br_end(anchors)
+
+    def exec_switch(self, stmt) -> None:
+        self.process_accesses(stmt, self.group(stmt))
+        body = stmt.body
+        if body is None or body.kind is not NodeKind.COMPOUND_STMT:
+            if body is not None:
+                self.exec_stmt(body)
+            return
+        groups: list[list] = []
+        has_default = False
+        for child in body.children:
+            if child.kind is NodeKind.CASE_LABEL:
+                groups.append([])
+                if child.value is None:
+                    has_default = True
+                continue
+            if not groups:
+                groups.append([])
+            groups[-1].append(child)
+        if not groups and has_default:     # unreachable: has_default implies a group
+            return
+        self._br_begin()
+        anchors = []
+        for group in groups:
+            self.emit(OP_ARM_FORK)
+            self._hold(1)
+            for s in group:
+                self.exec_stmt(s)
+            self.emit(OP_ARM_CLOSE)
+            self._hold(1)
+            self.live -= 1                  # cur reference transferred to arm
+            anchors.append(self.group_anchor(group, stmt))
+        if not has_default:
+            self.emit(OP_ARM_PASSIVE)
+            self._hold(1)
+            anchors.append(self._none_anchor(stmt))
+        self._br_end(anchors)
+
+    # -- loops --
+    def _loop(self, stmt, may_skip: bool, body_fn) -> None:
+        flags = OP_LOOP_BEGIN | (F_MAY_SKIP if may_skip else 0)
+        begin = self.emit(flags, self.sid(stmt), 0, 0)
+        self.loop_depth += 1
+        self.max_loop_depth = max(self.max_loop_depth, self.loop_depth)
+        self._hold(2)                       # entry/weakened + a stale round-0 cur
+        body_fn()
+        self.emit(OP_LOOP_END, begin + 1, 0, 0)
+        self.live -= 2
+        self.loop_depth -= 1
+
+    def exec_for(self, stmt) -> None:
+        self.exec_stmt(stmt.for_init)
+        cond_accs = self.accs_in(stmt, stmt.for_cond)
+        inc_accs = self.accs_in(stmt, stmt.for_inc)
+        self.process_accesses(stmt, cond_accs)
+
+        def body():
+            self.exec_stmt(stmt.body)
+            self.process_accesses(stmt, inc_accs)
+            self.process_accesses(stmt, cond_accs, override=stmt)
+        self._loop(stmt, True, body)
+
+    def exec_while(self, stmt) -> None:
+        cond_accs = self.accs_in(stmt, stmt.cond)
+        self.process_accesses(stmt, cond_accs)
+
+        def body():
+            self.exec_stmt(stmt.body)
+            self.process_accesses(stmt, cond_accs, override=stmt)
+        self._loop(stmt, True, body)
+
+    def exec_do(self, stmt) -> None:
+        cond_accs = self.accs_in(stmt, stmt.cond)
+
+        def body():
+            self.exec_stmt(stmt.body)
+            self.process_accesses(stmt, cond_accs, override=stmt)
+        self._loop(stmt, False, body)
+
+    # ---- packing ---------------------------------------------------------
+    def finish(self) -> FnProgram:
+        # name ranks: the reference sorts by name in `_merge_arms`
+        order = sorted(range(len(self.vars)), key=lambda i: (self.vars[i].name, i))
+        rank = [0] * len(self.vars)
+        for r, i in enumerate(order):
+            rank[i] = r
+        flags = []
+        for i, v in enumerate(self.vars):
+            f = 0
+            if v.is_scalar:
+                f |= V_SCALAR
+            if v.name in self.allow_stale:
+                f |= V_ALLOW_STALE
+            if (v.storage is Storage.LOCAL and v.decl is not None
+                    and self.region_begin is not None
+                    and v.decl.span.start >= self.region_begin.span.start):
+                f |= V_DECL_LATE
+            if v.storage is not Storage.LOCAL:
+                f |= V_NONLOCAL
+            flags.append(f | (rank[i] << 16))
+        span = np.array([[s.span.start, s.span.end] for s in self.stmts],
+                        dtype=np.int32).reshape(-1, 2)
+        ops = np.array(self.ops, dtype=np.int32).reshape(-1, 4)
+        n_slots = self.max_live + 2 * self.max_loop_depth + 2
+        return FnProgram(
+            fn=self.fn, ops=ops, var_flags=np.array(flags, dtype=np.int32),
+            stmt_span=span, sites=np.array(self.sites, dtype=np.int32),
+            arms=np.array(self.arms, dtype=np.int32),
+            region_begin_start=(self.region_begin.span.start
+                                if self.region_begin is not None else -1),
+            n_slots=n_slots, max_loop_depth=self.max_loop_depth,
+            max_br_depth=self.max_br_depth, max_arms=self.max_arms,
+            vars=self.vars, stmts=self.stmts, kernel_stmts=self.kernel_stmts,
+            region=((self.region_block, self.region_begin, self.region_end)
+                    if self.region_begin is not None else None))
+
+
+def lower_function(src, cfg, accesses, table, allow_stale=frozenset()) -> FnProgram:
+    lw = _Lowerer(src, cfg, accesses, table, allow_stale)
+    lw.run()
+    return lw.finish()

@@ -142,42 +142,6 @@ typedef struct {
 /* Host buffers in, host buffers out (H2D + kernel + D2H). */
 int dfx_replay_batch(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
 
-/* ------------------------------------------------------------------------ */
-/* Kernels (a)+(b): CSR fixpoint and per-edge transfer requirements          */
-/* ------------------------------------------------------------------------ */
-
-/* Node-major bitplanes: plane[node * words + w], bit b of word w = var 32w+b.
- * Node kinds: 0 host, 1 kernel.  Transfer functions per node:
- *   host:   H' = H | GEN_H ;           D' = D & ~KILL_D
- *   kernel: H' = H & ~KILL_H ;         D' = D | GEN_D | (FPC & ~H_in)
- * expressed uniformly as two planes per node: (A, B) = (GEN_H, KILL_D) for
- * host nodes and (GEN_D | FPC-bit-holder, KILL_H) for kernel nodes; see
- * DESIGN.md §E2 for the encoding and csrc/mfp.cu for the kernels. */
-typedef struct {
-  int64_t n_nodes;
-  int32_t words;               /* V / 32 (multiple of 4) */
-  const int32_t *row_ptr;      /* [n+1] predecessor CSR */
-  const int32_t *col;          /* [nnz]  predecessor ids */
-  const uint8_t *node_kind;    /* [n] */
-  const uint32_t *gen;         /* [n*words] */
-  const uint32_t *kill;        /* [n*words] */
-  const uint32_t *use;         /* [n*words] host: HR bits, kernel: DR bits */
-  const uint32_t *fpc;         /* [n*words] kernel nodes: FPC-eligible DR bits */
-} dfx_csr_in;
-
-typedef struct {
-  uint32_t *out_h;             /* [n*words] fixpoint OUT planes (optional) */
-  uint32_t *out_d;
-  /* per-edge requirement records (kernel b) */
-  int64_t rec_cap;
-  int64_t n_rec;               /* out */
-  int32_t *rec_dst, *rec_src, *rec_word; uint8_t *rec_kind; uint32_t *rec_mask;
-  int32_t rounds;              /* out: rounds to fixpoint (both phases) */
-  float kernel_ms;             /* out: device time of the solve */
-} dfx_csr_out;
-
-int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_csr_out *out);
-
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,444 @@
+// replay.cu -- E1: exact schedule replay of the reference analysis on sm_100a.
+//
+// Semantics: dartomp/dataflow.py:194-734 (`_Analyzer`), compiled to a
+// structured bytecode by paper_2406_13881_b200/lower.py.  Work decomposition:
+// one warp per (function, 32-variable chunk); lane = variable.  This is exact
+// because the analysis separates per variable: each lane carries
+// its own validity bits and provenance for every live state slot, while the
+// control state (current slot, branch/loop frames, slot reference counts,
+// record flag, visit counter) is uniform across the warp and kept in shared
+// memory, updated by lane 0.  Lanes diverge only inside the per-access ops
+// that touch their variable.
+//
+// Per lane state:  H, D  bitmask over slots (uint64 registers)
+//                  provenance (device_producer | last_host_write << 16) per
+//                  slot in shared memory, [slot][lane] (conflict-free)
+// Outputs: order-keyed events (plans, suppressions, errors) appended with one
+// global atomic per event, and per-variable result bits.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dfx.h"
+#include "dfx_internal.h"
+
+namespace dfx {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kMaxSlots = 64;
+constexpr int kMaxBr = 48;
+constexpr int kMaxArmStk = 192;
+constexpr int kMaxLoop = 24;
+constexpr uint32_t kNone = 0xFFFFu;
+
+struct BrFrame { int16_t saved, arm_base, narms, pad; };
+struct LoopFrame { int32_t stmt, body_pc, loop_start; int16_t slot; int8_t round, may_skip, rec_saved, pad[3]; };
+
+struct WarpCtl {
+  uint8_t ref[kMaxSlots];
+  BrFrame br[kMaxBr];
+  uint8_t armstk[kMaxArmStk];
+  LoopFrame lp[kMaxLoop];
+  int cur, nbr, narm, nlp, record, fault;
+  int bc0, bc1;          // broadcast scratch
+};
+
+__device__ __forceinline__ int st_start(const int32_t* span, int s) { return __ldg(span + 2 * s); }
+__device__ __forceinline__ int st_end(const int32_t* span, int s) { return __ldg(span + 2 * s + 1); }
+
+__device__ __forceinline__ int alloc_slot(WarpCtl& c, int nslots) {
+  for (int i = 0; i < nslots; i++)
+    if (c.ref[i] == 0) { c.ref[i] = 1; return i; }
+  c.fault = 1;
+  return 0;
+}
+
+__device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, int64_t cap,
+                                     uint64_t key, int fn, int var, int node, int kind, int pos) {
+  unsigned long long i = atomicAdd(count, 1ull);
+  if ((int64_t)i < cap) {
+    dfx_event e;
+    e.key = key; e.fn = fn; e.var = var; e.node = node;
+    e.kind = (uint8_t)kind; e.pos = (uint8_t)pos; e.pad = 0;
+    ev[i] = e;
+  }
+}
+
+// `_State.merge_conj` provenance rule (dataflow.py:135-142)
+__device__ __forceinline__ uint32_t pick(const int32_t* span, uint32_t mine, uint32_t other) {
+  if (other == kNone) return mine;
+  if (mine == kNone || st_end(span, other) > st_end(span, mine)) return other;
+  return mine;
+}
+
+// Algorithm 1 + finalize + normalize on the static site table
+// (bounds.py:134-193, dataflow.py:270-295)
+__device__ __forceinline__ int hoist(const int32_t* t, int loc_lim) {
+  int n = __ldg(t), acc = __ldg(t + 1);
+  int k = 0;
+  while (k < n && __ldg(t + 2 + 2 * k) < loc_lim) k++;
+  int c = k;
+  while (c < n && !(__ldg(t + 3 + 2 * c) & DFX_AC_QUAL)) c++;
+  if (c == n) return acc;
+  for (int j = c; j < n; j++) {
+    int code = __ldg(t + 3 + 2 * j);
+    if (code & DFX_AC_CLEAN) return code & (DFX_AC_NODE_MASK | DFX_AC_ERR);
+  }
+  return acc;
+}
+
+struct Lane {
+  uint64_t H, D;
+  uint32_t skipH, skipD;
+  int presence, to_comp, from_comp;
+  int halted;
+};
+
+__device__ __forceinline__ int getb(uint64_t m, int s) { return (int)((m >> s) & 1ull); }
+__device__ __forceinline__ uint64_t setb(uint64_t m, int s, int v) {
+  return v ? (m | (1ull << s)) : (m & ~(1ull << s));
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
+              const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
+              const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
+              const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
+              int n_items, int slots_per_warp, dfx_event* __restrict__ events,
+              int64_t event_cap, unsigned long long* __restrict__ event_count,
+              uint8_t* __restrict__ var_out) {
+  __shared__ WarpCtl ctl_all[kWarpsPerBlock];
+  extern __shared__ uint32_t prov_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kWarpsPerBlock + warp;
+  if (item >= n_items) return;
+  WarpCtl& c = ctl_all[warp];
+  uint32_t* prov = prov_all + warp * slots_per_warp * 32;
+
+  const int fi = __ldg(item_fn + item);
+  const dfx_fn_desc d = fns[fi];
+  const int var = __ldg(item_chunk + item) * 32 + lane;
+  const bool active = var < d.n_vars;
+  const int myvar = active ? var : -1;
+  int vflags = 0, rank = 0;
+  if (active) {
+    int w = __ldg(var_flags + d.var_off + var);
+    vflags = w & 0xFFFF;
+    rank = (int)((uint32_t)w >> 16);
+  }
+  const int4* fops = reinterpret_cast<const int4*>(ops) + d.op_off;
+  const int32_t* span = stmt_span + 2 * (int64_t)d.stmt_off;
+  const int32_t* fsites = sites + d.site_off;
+  const int32_t* farms = arms + 2 * (int64_t)d.arm_off;
+  const int nslots = d.n_slots < slots_per_warp ? d.n_slots : slots_per_warp;
+  const int rbs = d.region_begin_start;
+
+  if (lane == 0) {
+    for (int i = 0; i < kMaxSlots; i++) c.ref[i] = 0;
+    c.nbr = c.narm = c.nlp = 0;
+    c.record = 1;
+    c.fault = 0;
+    c.cur = alloc_slot(c, nslots);
+  }
+  for (int s = 0; s < slots_per_warp; s++) prov[s * 32 + lane] = 0xFFFFFFFFu;
+  __syncwarp();
+
+  Lane L;
+  L.H = ~0ull; L.D = 0ull;
+  L.skipH = L.skipD = 0u;
+  L.presence = L.to_comp = L.from_comp = 0;
+  L.halted = !active;
+  int cur = c.cur;
+  int record = 1;
+  uint64_t seq = 0;
+  int pc = 0;
+
+  // plan-log window bookkeeping for the zero-trip skip merge (dataflow.py:573-589)
+  auto log_plan = [&](int kind, int pos, int node) {
+    for (int l = 0; l < c.nlp; l++) {
+      const LoopFrame& f = c.lp[l];
+      if (f.round != 1) continue;
+      int pre = (pos == DFX_POS_BEFORE && st_start(span, node) <= f.loop_start) ||
+                (pos == DFX_POS_AFTER && st_end(span, node) <= f.loop_start);
+      if (!pre) continue;
+      if (kind == DFX_EV_UPDATE_FROM) L.skipH |= 1u << l; else L.skipD |= 1u << l;
+    }
+  };
+  auto copy_slot = [&](int dst, int src) {
+    L.H = setb(L.H, dst, getb(L.H, src));
+    L.D = setb(L.D, dst, getb(L.D, src));
+    prov[dst * 32 + lane] = prov[src * 32 + lane];
+  };
+  auto merge_conj = [&](int a, int b) {
+    L.H = setb(L.H, a, getb(L.H, a) & getb(L.H, b));
+    L.D = setb(L.D, a, getb(L.D, a) & getb(L.D, b));
+    uint32_t pa = prov[a * 32 + lane], pb = prov[b * 32 + lane];
+    uint32_t dp = pick(span, pa & 0xFFFFu, pb & 0xFFFFu);
+    uint32_t lw = pick(span, pa >> 16, pb >> 16);
+    prov[a * 32 + lane] = dp | (lw << 16);
+  };
+
+  for (;;) {
+    const int4 op = __ldg(fops + pc);
+    const int code = op.x & 0xFF, fl = op.x;
+    seq++;
+    const uint64_t key = seq << 24;
+    if (code == DFX_OP_END) break;
+    switch (code) {
+      case DFX_OP_HR: {   // host_read, dataflow.py:299-324
+        if (op.y != myvar || L.halted || getb(L.H, cur)) break;
+        if (vflags & DFX_V_ALLOW_STALE) {
+          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_SUPPRESS, 0);
+          L.H = setb(L.H, cur, 1); break;
+        }
+        if (fl & DFX_F_AFTER_REGION) {
+          L.presence = 1; L.from_comp = 1; L.H = setb(L.H, cur, 1); break;
+        }
+        uint32_t dp = prov[cur * 32 + lane] & 0xFFFFu;
+        int lim = dp == kNone ? 0 : st_end(span, dp);
+        int pos, node;
+        if (fl & DFX_F_OVR) { pos = DFX_POS_BODY_END; node = op.w; }
+        else {
+          int a = hoist(fsites + op.w, lim);
+          if (a & DFX_AC_ERR) {
+            emit(events, event_count, event_cap, key, fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
+            L.halted = 1; break;
+          }
+          pos = DFX_POS_BEFORE; node = a;
+        }
+        log_plan(DFX_EV_UPDATE_FROM, pos, node);
+        if (record) emit(events, event_count, event_cap, key, fi, var, node, DFX_EV_UPDATE_FROM, pos);
+        L.H = setb(L.H, cur, 1);
+        break;
+      }
+      case DFX_OP_HW: {   // host_write, dataflow.py:326-330
+        if (op.y != myvar || L.halted) break;
+        L.H = setb(L.H, cur, 1); L.D = setb(L.D, cur, 0);
+        uint32_t p = prov[cur * 32 + lane];
+        prov[cur * 32 + lane] = (p & 0xFFFFu) | ((uint32_t)op.z << 16);
+        break;
+      }
+      case DFX_OP_DR: {   // device_read, dataflow.py:332-368
+        if (op.y != myvar || L.halted || getb(L.D, cur)) break;
+        if (vflags & DFX_V_ALLOW_STALE) {
+          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_SUPPRESS, 0);
+          L.D = setb(L.D, cur, 1); break;
+        }
+        if ((fl & DFX_F_FP) && getb(L.H, cur)) {
+          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_FIRSTPRIVATE, DFX_POS_KERNEL);
+          break;
+        }
+        L.presence = 1;
+        if (record && (vflags & DFX_V_DECL_LATE)) {
+          emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_ERR_DECL, 0);
+          L.halted = 1; break;
+        }
+        uint32_t lw = prov[cur * 32 + lane] >> 16;
+        bool in_region = lw != kNone && rbs >= 0 && st_start(span, lw) >= rbs;
+        if (!in_region) { L.to_comp = 1; L.D = setb(L.D, cur, 1); break; }
+        int lim = st_end(span, lw);
+        int pos, node;
+        if (fl & DFX_F_OVR) { pos = DFX_POS_BODY_END; node = op.w; }
+        else {
+          int a = hoist(fsites + op.w, lim);
+          if (a & DFX_AC_ERR) {
+            emit(events, event_count, event_cap, key, fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
+            L.halted = 1; break;
+          }
+          pos = DFX_POS_BEFORE; node = a;
+        }
+        log_plan(DFX_EV_UPDATE_TO, pos, node);
+        if (record) emit(events, event_count, event_cap, key, fi, var, node, DFX_EV_UPDATE_TO, pos);
+        L.D = setb(L.D, cur, 1);
+        break;
+      }
+      case DFX_OP_DW: {   // device_write, dataflow.py:370-378
+        if (op.y != myvar || L.halted) break;
+        L.presence = 1;
+        if (record && (vflags & DFX_V_DECL_LATE)) {
+          emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_ERR_DECL, 0);
+          L.halted = 1; break;
+        }
+        L.D = setb(L.D, cur, 1); L.H = setb(L.H, cur, 0);
+        uint32_t p = prov[cur * 32 + lane];
+        prov[cur * 32 + lane] = (p & 0xFFFF0000u) | (uint32_t)op.z;
+        break;
+      }
+      case DFX_OP_BR_BEGIN: {  // saved = self.state
+        if (lane == 0) {
+          if (c.nbr >= kMaxBr) c.fault = 1;
+          else {
+            BrFrame& b = c.br[c.nbr++];
+            b.saved = (int16_t)cur; c.ref[cur]++;
+            b.arm_base = (int16_t)c.narm; b.narms = 0;
+          }
+        }
+        __syncwarp();
+        break;
+      }
+      case DFX_OP_ARM_FORK:      // state = saved.copy()  (F_CAPTURE: the arm is this slot)
+      case DFX_OP_ARM_PASSIVE: { // arms += [(saved.copy(), None)]
+        if (lane == 0) {
+          BrFrame& b = c.br[c.nbr - 1];
+          int s = alloc_slot(c, nslots);
+          if (c.narm >= kMaxArmStk) c.fault = 1;
+          c.bc0 = s; c.bc1 = b.saved;
+          if (code == DFX_OP_ARM_FORK) {
+            c.ref[cur]--; c.cur = s;
+            if (fl & DFX_F_CAPTURE) { c.armstk[c.narm++] = (uint8_t)s; c.ref[s]++; b.narms++; }
+          } else {
+            c.armstk[c.narm++] = (uint8_t)s; b.narms++;
+          }
+        }
+        __syncwarp();
+        int s = c.bc0, saved = c.bc1;
+        copy_slot(s, saved);
+        cur = c.cur;
+        __syncwarp();
+        break;
+      }
+      case DFX_OP_ARM_CLOSE: {   // switch arm = current slot
+        if (lane == 0) {
+          BrFrame& b = c.br[c.nbr - 1];
+          if (c.narm >= kMaxArmStk) c.fault = 1;
+          else { c.armstk[c.narm++] = (uint8_t)cur; c.ref[cur]++; b.narms++; }
+        }
+        __syncwarp();
+        break;
+      }
+      case DFX_OP_BR_END: {      // _merge_arms, dataflow.py:525-564
+        const BrFrame b = c.br[c.nbr - 1];
+        const uint8_t* arm = c.armstk + b.arm_base;
+        const int n = b.narms;
+        if (!L.halted) {
+          int dev_newer = 0, host_newer = 0;
+          for (int i = 0; i < n; i++) {
+            int s = arm[i];
+            int h = getb(L.H, s), dd = getb(L.D, s);
+            dev_newer |= dd & !h;
+            host_newer |= h & !dd;
+          }
+          if (dev_newer && host_newer) {
+            for (int i = 0; i < n; i++) {
+              int s = arm[i];
+              if (!(getb(L.D, s) && !getb(L.H, s))) continue;
+              uint64_t k2 = key | ((uint64_t)rank << 8) | (uint64_t)i;
+              int kind = __ldg(farms + 2 * (op.y + i)), node = __ldg(farms + 2 * (op.y + i) + 1);
+              if (kind == DFX_ARM_ERR_ARM || kind == DFX_ARM_ERR_LOOP) {
+                emit(events, event_count, event_cap, k2, fi, var, node,
+                     kind == DFX_ARM_ERR_ARM ? DFX_EV_ERR_BRACES_ARM : DFX_EV_ERR_BRACES_LOOP, 0);
+                L.halted = 1; break;
+              }
+              int pos = kind == DFX_ARM_BEFORE ? DFX_POS_BEFORE : DFX_POS_AFTER;
+              log_plan(DFX_EV_UPDATE_FROM, pos, node);
+              if (record) emit(events, event_count, event_cap, k2, fi, var, node, DFX_EV_UPDATE_FROM, pos);
+              L.H = setb(L.H, s, 1);
+            }
+          }
+        }
+        for (int i = 1; i < n; i++) merge_conj(arm[0], arm[i]);
+        __syncwarp();
+        if (lane == 0) {
+          int m = arm[0];
+          c.ref[m]++; c.ref[cur]--; c.cur = m;
+          for (int i = 0; i < n; i++) c.ref[arm[i]]--;
+          c.ref[b.saved]--;
+          c.narm = b.arm_base;
+          c.nbr--;
+        }
+        __syncwarp();
+        cur = c.cur;
+        break;
+      }
+      case DFX_OP_LOOP_BEGIN: {  // _loop_rounds: entry = state.copy(); dry round
+        if (lane == 0) {
+          if (c.nlp >= kMaxLoop) c.fault = 1;
+          else {
+            LoopFrame& f = c.lp[c.nlp++];
+            f.stmt = op.y; f.loop_start = st_start(span, op.y);
+            f.may_skip = (fl & DFX_F_MAY_SKIP) != 0;
+            f.body_pc = pc + 1; f.round = 0; f.rec_saved = (int8_t)record;
+            f.slot = (int16_t)alloc_slot(c, nslots);
+            c.bc0 = f.slot;
+          }
+        }
+        __syncwarp();
+        if (!c.fault) copy_slot(c.bc0, cur);
+        record = 0;
+        __syncwarp();
+        break;
+      }
+      case DFX_OP_LOOP_END: {
+        const int lvl = c.nlp - 1;
+        LoopFrame& f = c.lp[lvl];
+        if (f.round == 0) {      // merge entry, weaken, planning round
+          merge_conj(cur, f.slot);
+          __syncwarp();
+          if (lane == 0) {
+            c.ref[f.slot]--;
+            f.slot = (int16_t)alloc_slot(c, nslots);
+            f.round = 1;
+          }
+          __syncwarp();
+          copy_slot(f.slot, cur);
+          record = f.rec_saved;
+          L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
+          pc = f.body_pc;
+          __syncwarp();
+          if (c.fault) goto fault;
+          continue;
+        }
+        if (f.may_skip) {        // zero-trip skip merge (dataflow.py:575-590)
+          int w = f.slot;
+          if (L.skipH & (1u << lvl)) L.H = setb(L.H, w, 1);
+          if (L.skipD & (1u << lvl)) L.D = setb(L.D, w, 1);
+          merge_conj(cur, w);
+        }
+        L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
+        __syncwarp();
+        if (lane == 0) { c.ref[f.slot]--; c.nlp--; }
+        __syncwarp();
+        break;
+      }
+      case DFX_OP_ERR: {
+        if (op.y == 1 && __ldg(item_chunk + item) == 0 && lane == 0)
+          emit(events, event_count, event_cap, key, fi, -1, op.z, DFX_EV_ERR_DATAMAP, 0);
+        goto halt_all;
+      }
+      default:
+        goto fault;
+    }
+    if (c.fault) goto fault;
+    pc++;
+  }
+  if (active) {
+    uint8_t o = 0;
+    if (L.presence) o |= DFX_OUT_PRESENCE;
+    if (L.to_comp) o |= DFX_OUT_TO;
+    if (L.from_comp) o |= DFX_OUT_FROM;
+    if (getb(L.H, cur)) o |= DFX_OUT_H;
+    if (getb(L.D, cur)) o |= DFX_OUT_D;
+    var_out[d.var_off + var] = L.halted ? 0 : o;
+  }
+  return;
+fault:
+  if (lane == 0)
+    emit(events, event_count, event_cap, seq << 24, fi, 0, 0, DFX_EV_ERR_ENGINE, 0);
+halt_all:
+  if (active) var_out[d.var_off + var] = 0;
+}
+
+int replay_launch(const ReplayDev& r, cudaStream_t stream) {
+  int slots = r.max_slots;
+  if (slots < 2) slots = 2;
+  if (slots > kMaxSlots) return DFX_E_LIMIT;
+  size_t smem = (size_t)kWarpsPerBlock * slots * 32 * sizeof(uint32_t);
+  int blocks = (r.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks == 0) return DFX_OK;
+  cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  replay_kernel<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
+      r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
+      r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+}  // namespace dfx

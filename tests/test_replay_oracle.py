@@ -1,0 +1,64 @@
+"""CPU: the replay oracle against the reference's golden outputs.
+
+The oracle (oracle/replay_oracle.c) is pinned here against (1) the committed
+raw fixtures and (2) -- when the reference front end is importable -- the
+reference `analyze_function` itself on fresh seeded programs.
+"""
+import numpy as np
+import pytest
+
+import _cases
+import _golden
+import _oracle
+from paper_2406_13881_b200._host import have_dartomp
+from paper_2406_13881_b200.dataflow import run_replay
+
+
+def test_oracle_matches_golden_raw():
+    batch, ev, vo = _golden.replay_fixture()
+    raw = run_replay(batch, runner=_oracle.replay_runner)
+    _golden.assert_raw_equal(raw.events, raw.var_out, ev, vo)
+
+
+def test_golden_covers_semantics():
+    """The fixture set exercises every event/position kind we claim parity on."""
+    plans = _golden.reference_plans()
+    seen = set()
+    for case in plans.values():
+        for res in case["functions"].values():
+            if res[0] == "err":
+                seen.add("err:" + res[1] + ":" + res[2].split(": error: ")[-1][:20])
+                continue
+            p = res[1]
+            if p["region"]:
+                seen.add("region")
+            for u in p["updates"]:
+                seen.add("upd:%s:%s" % (u[0], u[3]))
+            for k in p["kernel_clauses"]:
+                seen.add("kc:" + k[0])
+            if p["suppressed"]:
+                seen.add("suppressed")
+    for need in ("region", "upd:update_from:before", "upd:update_from:after",
+                 "upd:update_from:body_end", "upd:update_to:before",
+                 "kc:firstprivate", "kc:map_to", "kc:map_from", "kc:map_tofrom",
+                 "kc:map_alloc"):
+        assert need in seen, need
+    assert any(s.startswith("err:DeclPlacementError") for s in seen)
+    assert any(s.startswith("err:PreconditionError:braces") for s in seen)
+    assert any(s.startswith("err:PreconditionError:input already") for s in seen)
+
+
+@pytest.mark.skipif(not have_dartomp(), reason="reference front end not importable")
+@pytest.mark.parametrize("seed", list(range(1000, 1040)))
+def test_oracle_vs_reference_random(seed):
+    from dartomp.dataflow import analyze_function as ref_analyze
+    from dartomp.pipeline import load
+    from paper_2406_13881_b200.dataflow import analyze_functions
+    a = load(path="gen%d.c" % seed, text=_cases.random_program(seed))
+    names = list(a.cfgs)
+    items = [(a.src, a.cfgs[n], a.accesses[n], a.table) for n in names]
+    mine = analyze_functions(items, runner=_oracle.replay_runner)
+    for n, d in zip(names, mine):
+        ref = _cases.canon_result(lambda: ref_analyze(a.src, a.cfgs[n], a.accesses[n], a.table))
+        got = _cases.canon_result(d.get)
+        assert got == ref, n

@@ -142,6 +142,74 @@ typedef struct {
 /* Host buffers in, host buffers out (H2D + kernel + D2H). */
 int dfx_replay_batch(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
 
+/* ------------------------------------------------------------------------ */
+/* Kernels (a)+(b): CSR fixpoint and transfer requirements (north star)      */
+/* ------------------------------------------------------------------------ */
+/* The gen/kill core of dataflow.py:299-378 with the AND meet of
+ * dataflow.py:130-134 on an explicit predecessor CSR.  Bitplanes are
+ * node-major: plane[node * words + w], bit b of word w = variable 32*w + b.
+ *   host node  : H' = H | A        D' = D & ~B            (A = R|W, B = W)
+ *   kernel node: H' = H & ~B       D' = D | (A & ~(F & H_in)), F = A & ~B & S
+ * IN = AND over predecessors; nodes without predecessors take (H=1, D=0). */
+typedef struct dfx_csr dfx_csr;            /* device-resident problem */
+
+typedef struct {
+  int64_t n_nodes;
+  int32_t words;                /* V/32: multiple of 4, at most 512 */
+  int64_t nnz;
+  const int32_t *row_ptr;       /* [n_nodes+1] */
+  const int32_t *col;           /* [nnz] predecessor ids */
+  const uint8_t *node_kind;     /* [n_nodes] 0 host, 1 kernel */
+  const uint32_t *R;            /* [n_nodes*words] reads */
+  const uint32_t *W;            /* [n_nodes*words] writes */
+  const uint32_t *S;            /* [words] scalar-variable mask */
+} dfx_csr_in;
+
+typedef struct {                /* configuration C3 generator */
+  uint64_t seed;
+  int64_t n_nodes;
+  int32_t words;                /* word columns generated ... */
+  int32_t w0;                   /* ... starting at global word w0 */
+  int32_t n_scalar;             /* variables [0, n_scalar) are scalars */
+} dfx_c3_spec;
+
+typedef struct {                /* one insertion point: node x 32 variables */
+  int32_t node;
+  uint16_t word;
+  uint8_t kind;                 /* 1 update-from (host read of stale copy),
+                                   2 update-to (device read of stale copy),
+                                   3 firstprivate capture */
+  uint8_t pad;
+  uint32_t mask;
+} dfx_req_record;
+
+typedef struct {
+  int32_t rounds_h, rounds_d;   /* relaxation rounds per phase (incl. the last, unchanged one) */
+  int64_t evaluated;            /* node-row evaluations (both phases) */
+  int64_t rows_read, rows_written; /* 512-B-per-4096-var row transfers counted by the kernel */
+  float solve_ms;               /* device time of kernel (a), all rounds */
+  float req_ms;                 /* device time of kernel (b) incl. compaction */
+  int64_t n_records;
+} dfx_csr_stats;
+
+int dfx_set_stream(dfx_handle *h, void *cuda_stream);   /* NULL: the handle's own */
+int dfx_csr_create(dfx_handle *h, const dfx_csr_in *in, dfx_csr **out);   /* H2D */
+int dfx_csr_generate_c3(dfx_handle *h, const dfx_c3_spec *spec, dfx_csr **out);
+int dfx_csr_destroy(dfx_handle *h, dfx_csr *p);
+/* kernel (a); chunk_nodes <= 0 picks the default */
+int dfx_csr_solve(dfx_handle *h, dfx_csr *p, int32_t chunk_nodes, dfx_csr_stats *stats);
+/* kernel (b): requirement planes + order-preserving compaction into records
+ * (node-major, word-ascending; firstprivate records after a node's
+ * requirement records).  out may be NULL to only count. */
+int dfx_csr_requirements(dfx_handle *h, dfx_csr *p, dfx_req_record *out, int64_t cap,
+                         dfx_csr_stats *stats);
+/* D2H of the fixpoint OUT planes and the dense requirement plane (any NULL
+ * pointer is skipped) */
+int dfx_csr_download(dfx_handle *h, dfx_csr *p, uint32_t *out_h, uint32_t *out_d, uint32_t *req);
+/* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of records */
+int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_record *out, int64_t cap,
+                dfx_csr_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,176 @@
+"""Host wrapper of kernels (a)+(b): the CSR data-flow fixpoint engine.
+
+`CsrProblem` owns one device-resident problem (`dfx_csr`): predecessor CSR,
+node kinds, read/write bitplanes, and the fixpoint / requirement planes the
+kernels produce.  Build it from host arrays (`from_arrays`, an H2D copy
+through the C ABI) or generate configuration C3 directly in HBM
+(`generate_c3`).  No CPU fallback exists: a missing libdfx.so or CUDA device
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+
+
+class CsrIn(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("words", C.c_int32), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("node_kind", C.c_void_p),
+                ("R", C.c_void_p), ("W", C.c_void_p), ("S", C.c_void_p)]
+
+
+class C3Spec(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("n_nodes", C.c_int64), ("words", C.c_int32),
+                ("w0", C.c_int32), ("n_scalar", C.c_int32)]
+
+
+class CsrStats(C.Structure):
+    _fields_ = [("rounds_h", C.c_int32), ("rounds_d", C.c_int32),
+                ("evaluated", C.c_int64), ("rows_read", C.c_int64),
+                ("rows_written", C.c_int64), ("solve_ms", C.c_float),
+                ("req_ms", C.c_float), ("n_records", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+REC_DTYPE = np.dtype([("node", np.int32), ("word", np.uint16), ("kind", np.uint8),
+                      ("pad", np.uint8), ("mask", np.uint32)])
+assert REC_DTYPE.itemsize == 12
+
+REQ_UPDATE_FROM, REQ_UPDATE_TO, REQ_FIRSTPRIVATE = 1, 2, 3
+
+
+def _setup(lib):
+    for name in ("dfx_set_stream", "dfx_csr_create", "dfx_csr_generate_c3", "dfx_csr_destroy",
+                 "dfx_csr_solve", "dfx_csr_requirements", "dfx_csr_download", "dfx_mfp_csr"):
+        getattr(lib, name).restype = C.c_int
+
+
+@dataclass
+class C3Config:
+    """Configuration C3 (BASELINE.json configs[2]): 1M nodes x 4096 variables."""
+    n_nodes: int = 1 << 20
+    n_vars: int = 4096
+    seed: int = 0
+    w0: int = 0                   # first global word (V-sharding across GPUs)
+    scalar_frac: float = 0.02     # 2% of variables are firstprivate-eligible scalars
+
+    @property
+    def words(self) -> int:
+        return self.n_vars // 32
+
+    @property
+    def n_scalar(self) -> int:
+        return int(round(self.scalar_frac * self.n_vars))
+
+
+class CsrProblem:
+    def __init__(self, eng: _abi.Engine, handle: C.c_void_p, n_nodes: int, words: int):
+        self.eng = eng
+        self.h = handle
+        self.n_nodes = n_nodes
+        self.words = words
+        self.stats = CsrStats()
+
+    # ---- construction -----------------------------------------------------
+    @classmethod
+    def generate_c3(cls, cfg: C3Config, eng: _abi.Engine | None = None) -> "CsrProblem":
+        eng = eng or _abi.engine()
+        _setup(eng.lib)
+        spec = C3Spec(cfg.seed, cfg.n_nodes, cfg.words, cfg.w0, cfg.n_scalar)
+        h = C.c_void_p()
+        eng.check(eng.lib.dfx_csr_generate_c3(eng.h, C.byref(spec), C.byref(h)),
+                  "dfx_csr_generate_c3")
+        return cls(eng, h, cfg.n_nodes, cfg.words)
+
+    @classmethod
+    def from_arrays(cls, row_ptr, col, kind, R, W, S, eng: _abi.Engine | None = None) -> "CsrProblem":
+        eng = eng or _abi.engine()
+        _setup(eng.lib)
+        n, words = R.shape
+        arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, R, W, S)]
+        row_ptr, col, kind, R, W, S = arrs
+        assert row_ptr.dtype == np.int32 and col.dtype == np.int32 and kind.dtype == np.uint8
+        assert R.dtype == np.uint32 and W.dtype == np.uint32 and S.dtype == np.uint32
+        cin = CsrIn(n, words, int(col.shape[0]), *(a.ctypes.data for a in arrs))
+        h = C.c_void_p()
+        eng.check(eng.lib.dfx_csr_create(eng.h, C.byref(cin), C.byref(h)), "dfx_csr_create")
+        return cls(eng, h, n, words)
+
+    def close(self) -> None:
+        if self.h:
+            self.eng.lib.dfx_csr_destroy(self.eng.h, self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- kernels -------------------------------------------------------------
+    def solve(self, chunk_nodes: int = 0) -> CsrStats:
+        self.eng.check(self.eng.lib.dfx_csr_solve(self.eng.h, self.h, C.c_int32(chunk_nodes),
+                                                  C.byref(self.stats)), "dfx_csr_solve")
+        return self.stats
+
+    def requirements(self, capacity: int | None = None) -> np.ndarray:
+        """Kernel (b): compacted insertion-point records (REC_DTYPE)."""
+        if capacity is None:
+            self.eng.check(self.eng.lib.dfx_csr_requirements(self.eng.h, self.h, None, 0,
+                                                             C.byref(self.stats)),
+                           "dfx_csr_requirements(count)")
+            capacity = int(self.stats.n_records)
+        out = np.zeros(max(1, capacity), dtype=REC_DTYPE)
+        rc = self.eng.lib.dfx_csr_requirements(self.eng.h, self.h, C.c_void_p(out.ctypes.data),
+                                               C.c_int64(out.shape[0]), C.byref(self.stats))
+        if rc == _abi.DFX_E_NOSPC:
+            return self.requirements(int(self.stats.n_records))
+        self.eng.check(rc, "dfx_csr_requirements")
+        return out[: self.stats.n_records]
+
+    def download(self, out_h=True, out_d=True, req=False):
+        shape = (self.n_nodes, self.words)
+        oh = np.empty(shape, dtype=np.uint32) if out_h else None
+        od = np.empty(shape, dtype=np.uint32) if out_d else None
+        rq = np.empty(shape, dtype=np.uint32) if req else None
+        p = lambda a: C.c_void_p(a.ctypes.data) if a is not None else None  # noqa: E731
+        self.eng.check(self.eng.lib.dfx_csr_download(self.eng.h, self.h, p(oh), p(od), p(rq)),
+                       "dfx_csr_download")
+        return oh, od, rq
+
+
+def records_to_planes(rec: np.ndarray, n_nodes: int, words: int):
+    """Expand compacted records into (REQ, FP) planes (for checking)."""
+    req = np.zeros((n_nodes, words), dtype=np.uint32)
+    fp = np.zeros_like(req)
+    m = rec["kind"] == REQ_FIRSTPRIVATE
+    req[rec["node"][~m], rec["word"][~m]] = rec["mask"][~m]
+    fp[rec["node"][m], rec["word"][m]] = rec["mask"][m]
+    return req, fp
+
+
+def mfp_csr(row_ptr, col, kind, R, W, S, eng: _abi.Engine | None = None):
+    """All-in-one host-buffer call (`dfx_mfp_csr`): H2D, kernels (a)+(b), D2H
+    of the compacted records.  Returns (records, stats)."""
+    eng = eng or _abi.engine()
+    _setup(eng.lib)
+    n, words = R.shape
+    arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, R, W, S)]
+    cin = CsrIn(n, words, int(arrs[1].shape[0]), *(a.ctypes.data for a in arrs))
+    stats = CsrStats()
+    cap = max(1024, n * words // 4)
+    while True:
+        out = np.zeros(cap, dtype=REC_DTYPE)
+        rc = eng.lib.dfx_mfp_csr(eng.h, C.byref(cin), C.c_void_p(out.ctypes.data),
+                                 C.c_int64(cap), C.byref(stats))
+        if rc == _abi.DFX_E_NOSPC:
+            cap = int(stats.n_records)
+            continue
+        eng.check(rc, "dfx_mfp_csr")
+        return out[: stats.n_records], stats

@@ -10,10 +10,13 @@
 
 #include "../../include/dfx.h"
 #include "dfx_internal.h"
+#include "c3gen.cuh"
 
 struct dfx_handle {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the handle's own stream
+  cudaStream_t ext_stream = nullptr;  // caller's stream (dfx_set_stream)
+  cudaStream_t st() const { return ext_stream ? ext_stream : stream; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::unordered_map<std::string, std::pair<void*, size_t>> bufs;
 };
@@ -91,6 +94,12 @@ int dfx_close(dfx_handle* h) {
   return DFX_OK;
 }
 
+int dfx_set_stream(dfx_handle* h, void* stream) {
+  if (!h) return fail(DFX_E_ARG, "dfx_set_stream: null handle");
+  h->ext_stream = (cudaStream_t)stream;
+  return DFX_OK;
+}
+
 // ---------------------------------------------------------------------------
 // E1: dfx_replay_batch  (replaces dartomp.dataflow.analyze_function,
 // pkg/src/dartomp/dataflow.py:737-740, batched over functions)
@@ -133,14 +142,14 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   for (auto& p : parts) {
     *p.dst = dbuf(h, p.name, p.bytes + 16);
     if (!*p.dst) return fail(DFX_E_CUDA, "cudaMalloc %s (%zu B) failed", p.name, p.bytes);
-    if (p.bytes) CK(cudaMemcpyAsync(*p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, h->stream));
+    if (p.bytes) CK(cudaMemcpyAsync(*p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, h->st()));
   }
   const int64_t cap = out->event_cap;
   auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)(cap > 0 ? cap : 1));
   auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
   if (!d_ev || !d_cnt || !d_vout) return fail(DFX_E_CUDA, "cudaMalloc outputs failed");
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), h->stream));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), h->st()));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -156,21 +165,21 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   r.event_cap = cap;
   r.event_count = d_cnt;
   r.var_out = d_vout;
-  CK(cudaEventRecord(h->ev0, h->stream));
-  int rc = dfx::replay_launch(r, h->stream);
+  CK(cudaEventRecord(h->ev0, h->st()));
+  int rc = dfx::replay_launch(r, h->st());
   if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-  CK(cudaEventRecord(h->ev1, h->stream));
+  CK(cudaEventRecord(h->ev1, h->st()));
   unsigned long long count = 0;
-  CK(cudaMemcpyAsync(&count, d_cnt, sizeof count, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpyAsync(&count, d_cnt, sizeof count, cudaMemcpyDeviceToHost, h->st()));
+  CK(cudaStreamSynchronize(h->st()));
   size_t ncopy = count < (unsigned long long)cap ? (size_t)count : (size_t)cap;
   if (ncopy)
     CK(cudaMemcpyAsync(out->events, d_ev, sizeof(dfx_event) * ncopy, cudaMemcpyDeviceToHost,
-                       h->stream));
+                       h->st()));
   if (in->n_vars)
     CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost,
-                       h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+                       h->st()));
+  CK(cudaStreamSynchronize(h->st()));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   out->kernel_ms = ms;
@@ -178,6 +187,229 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if ((int64_t)count > cap) return fail(DFX_E_NOSPC, "event capacity %lld < %llu",
                                         (long long)cap, count);
   return DFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels (a) + (b): CSR fixpoint and transfer requirements
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct dfx_csr {
+  dfx::CsrDev p{};
+  std::vector<void*> allocs;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int32_t* counts = nullptr;
+  int64_t* offsets = nullptr;
+  dfx_req_record* d_records = nullptr;
+  int64_t records_cap = 0;
+  void* d_cnt = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+
+template <class T>
+T* csr_alloc(dfx_csr* c, size_t n) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(T) + 16) != cudaSuccess) return nullptr;
+  c->allocs.push_back(p);
+  return (T*)p;
+}
+
+int csr_destroy_impl(dfx_csr* c) {
+  if (!c) return DFX_OK;
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->d_records) cudaFree(c->d_records);
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  delete c;
+  return DFX_OK;
+}
+
+// allocate every device array of a problem with n nodes, `words` words
+int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t* S_host) {
+  dfx::CsrDev& p = c->p;
+  p.n_nodes = n;
+  p.words = words;
+  p.nnz = nnz;
+  const size_t plane = (size_t)n * words;
+  p.row_ptr = csr_alloc<int32_t>(c, n + 1);
+  p.col = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
+  p.kind = csr_alloc<uint8_t>(c, n);
+  p.A = csr_alloc<uint32_t>(c, plane);
+  p.B = csr_alloc<uint32_t>(c, plane);
+  p.USE = csr_alloc<uint32_t>(c, plane);
+  p.OH = csr_alloc<uint32_t>(c, plane);
+  p.OD = csr_alloc<uint32_t>(c, plane);
+  p.REQ = csr_alloc<uint32_t>(c, plane);
+  p.S = csr_alloc<uint32_t>(c, words);
+  p.stamp = csr_alloc<int32_t>(c, n);
+  p.fp_slot = csr_alloc<int32_t>(c, words / 4);
+  c->counts = csr_alloc<int32_t>(c, n);
+  c->offsets = csr_alloc<int64_t>(c, n + 1);
+  c->scratch_bytes = dfx::scan_scratch_bytes(n);
+  c->scratch = csr_alloc<uint8_t>(c, c->scratch_bytes);
+  c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_counters_bytes());
+  // scalar quads -> FP slots
+  std::vector<int32_t> slot(words / 4, -1);
+  int ns = 0;
+  for (int q = 0; q < words / 4; q++) {
+    const uint32_t* s = S_host + 4 * q;
+    if (s[0] | s[1] | s[2] | s[3]) slot[q] = ns++;
+  }
+  p.n_fp_slots = ns;
+  p.FPQ = csr_alloc<uint32_t>(c, (size_t)n * 4 * (ns > 0 ? ns : 1));
+  for (void* a : c->allocs)
+    if (!a) return fail(DFX_E_CUDA, "cudaMalloc failed for a %lld-node x %d-word problem",
+                        (long long)n, words);
+  if (c->allocs.size() != 17) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
+  CK(cudaMemcpy(p.S, S_host, sizeof(uint32_t) * words, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p.fp_slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice));
+  CK(cudaEventCreate(&c->e0));
+  CK(cudaEventCreate(&c->e1));
+  return DFX_OK;
+}
+
+int check_words(int64_t n, int words) {
+  if (n <= 0 || n > 0x7FFFFFFF) return fail(DFX_E_ARG, "n_nodes %lld out of range", (long long)n);
+  if (dfx::vpl_for(words) < 0)
+    return fail(DFX_E_LIMIT, "words=%d: need a multiple of 4 and at most 512", words);
+  return DFX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfx_csr_create(dfx_handle* h, const dfx_csr_in* in, dfx_csr** out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_csr_create: null argument");
+  CK(cudaSetDevice(h->device));
+  int rc = check_words(in->n_nodes, in->words);
+  if (rc) return rc;
+  auto* c = new dfx_csr();
+  rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
+  if (rc) { csr_destroy_impl(c); return rc; }
+  dfx::CsrDev& p = c->p;
+  const size_t plane = sizeof(uint32_t) * (size_t)in->n_nodes * in->words;
+  cudaStream_t st = h->st();
+  CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
+  if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.USE, in->R, plane, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
+  rc = dfx::or_planes(p, st);
+  if (rc) { csr_destroy_impl(c); return fail(rc, "or_planes launch failed"); }
+  *out = c;
+  return DFX_OK;
+}
+
+int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
+  if (!h || !spec || !out) return fail(DFX_E_ARG, "dfx_csr_generate_c3: null argument");
+  CK(cudaSetDevice(h->device));
+  int rc = check_words(spec->n_nodes, spec->words);
+  if (rc) return rc;
+  int64_t nnz = 0;
+  {  // exact edge count (host, cheap: one hash per node)
+    for (int64_t n = 1; n < spec->n_nodes; n++) nnz += 1 + dfx::c3_n_extra(spec->seed, n);
+  }
+  std::vector<uint32_t> S(spec->words);
+  for (int w = 0; w < spec->words; w++) S[w] = dfx::c3_scalar_word(spec->w0 + w, spec->n_scalar);
+  auto* c = new dfx_csr();
+  rc = csr_alloc_all(c, spec->n_nodes, spec->words, nnz, S.data());
+  if (rc) { csr_destroy_impl(c); return rc; }
+  rc = dfx::c3_generate(c->p, spec->seed, spec->w0, h->st(), c->scratch, c->scratch_bytes);
+  if (rc) { csr_destroy_impl(c); return fail(rc, "c3 generation failed"); }
+  CK(cudaStreamSynchronize(h->st()));
+  *out = c;
+  return DFX_OK;
+}
+
+int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
+  if (h) cudaSetDevice(h->device);
+  return csr_destroy_impl(p);
+}
+
+int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats* stats) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve: null argument");
+  CK(cudaSetDevice(h->device));
+  if (chunk_nodes <= 0) chunk_nodes = 256;
+  cudaStream_t st = h->st();
+  dfx::SolveStats s{};
+  CK(cudaEventRecord(c->e0, st));
+  int rc = dfx::mfp_solve(c->p, (dfx::RoundCounters*)c->d_cnt, st, chunk_nodes, 10000, &s);
+  if (rc) return fail(rc, "mfp_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
+  CK(cudaEventRecord(c->e1, st));
+  CK(cudaEventSynchronize(c->e1));
+  if (stats) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    stats->rounds_h = s.rounds[0];
+    stats->rounds_d = s.rounds[1];
+    stats->evaluated = s.evaluated;
+    stats->rows_read = s.rows_read;
+    stats->rows_written = s.rows_written;
+    stats->solve_ms = ms;
+  }
+  return DFX_OK;
+}
+
+int dfx_csr_requirements(dfx_handle* h, dfx_csr* c, dfx_req_record* out, int64_t cap,
+                         dfx_csr_stats* stats) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_requirements: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  // records buffer on device: sized from the previous count or the cap
+  int64_t want = cap > 0 ? cap : 0;
+  if (out && want > c->records_cap) {
+    if (c->d_records) cudaFree(c->d_records);
+    c->d_records = nullptr;
+    CK(cudaMalloc(&c->d_records, sizeof(dfx_req_record) * (size_t)want));
+    c->records_cap = want;
+  }
+  int64_t n_out = 0;
+  CK(cudaEventRecord(c->e0, st));
+  int rc = dfx::requirements(c->p, c->counts, c->offsets, c->scratch, c->scratch_bytes,
+                             out ? c->d_records : nullptr, out ? want : 0, &n_out, st);
+  if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
+  CK(cudaEventRecord(c->e1, st));
+  CK(cudaStreamSynchronize(st));
+  if (out && n_out) {
+    size_t ncopy = (size_t)(n_out < want ? n_out : want);
+    CK(cudaMemcpyAsync(out, c->d_records, sizeof(dfx_req_record) * ncopy, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  if (stats) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    stats->req_ms = ms;
+    stats->n_records = n_out;
+  }
+  if (out && n_out > want) return fail(DFX_E_NOSPC, "record capacity %lld < %lld", (long long)want, (long long)n_out);
+  return DFX_OK;
+}
+
+int dfx_csr_download(dfx_handle* h, dfx_csr* c, uint32_t* out_h, uint32_t* out_d, uint32_t* req) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_download: null argument");
+  CK(cudaSetDevice(h->device));
+  const size_t plane = sizeof(uint32_t) * (size_t)c->p.n_nodes * c->p.words;
+  cudaStream_t st = h->st();
+  if (out_h) CK(cudaMemcpyAsync(out_h, c->p.OH, plane, cudaMemcpyDeviceToHost, st));
+  if (out_d) CK(cudaMemcpyAsync(out_d, c->p.OD, plane, cudaMemcpyDeviceToHost, st));
+  if (req) CK(cudaMemcpyAsync(req, c->p.REQ, plane, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DFX_OK;
+}
+
+int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_record* out, int64_t cap,
+                dfx_csr_stats* stats) {
+  dfx_csr* c = nullptr;
+  int rc = dfx_csr_create(h, in, &c);
+  if (rc) return rc;
+  rc = dfx_csr_solve(h, c, 0, stats);
+  if (!rc) rc = dfx_csr_requirements(h, c, out, cap, stats);
+  dfx_csr_destroy(h, c);
+  return rc;
 }
 
 }  // extern "C"

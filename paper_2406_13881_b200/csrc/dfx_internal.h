@@ -27,3 +27,45 @@ struct ReplayDev {
 int replay_launch(const ReplayDev& r, cudaStream_t stream);
 
 }  // namespace dfx
+
+namespace dfx {
+
+struct CsrDev {
+  int64_t n_nodes;
+  int32_t words;
+  int64_t nnz;
+  int32_t* row_ptr;
+  int32_t* col;
+  uint8_t* kind;
+  uint32_t* A;      // R | W
+  uint32_t* B;      // W
+  uint32_t* USE;    // R
+  uint32_t* S;      // [words]
+  uint32_t* OH;
+  uint32_t* OD;
+  uint32_t* REQ;
+  uint32_t* FPQ;    // [n_nodes][n_fp_slots] uint4
+  int32_t* fp_slot; // [words/4] quad -> slot or -1
+  int32_t n_fp_slots;
+  int32_t* stamp;
+};
+
+struct SolveStats {
+  int rounds[2];
+  int64_t evaluated, rows_read, rows_written;
+};
+
+struct RoundCounters;
+
+int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch, size_t scratch_bytes);
+int or_planes(const CsrDev& p, cudaStream_t st);
+int vpl_for(int words);
+int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_nodes,
+              int max_rounds, SolveStats* stats);
+int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                 size_t scratch_bytes, dfx_req_record* out, int64_t cap, int64_t* n_out,
+                 cudaStream_t st);
+size_t scan_scratch_bytes(int64_t n);
+size_t round_counters_bytes();
+
+}  // namespace dfx

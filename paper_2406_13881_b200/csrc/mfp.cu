@@ -1,0 +1,497 @@
+// mfp.cu -- kernels (a) and (b): the CSR data-flow fixpoint and the
+// transfer-requirement pass, plus the configuration-C3 generator.
+//
+// Semantics (oracle/mfp_oracle.c restates them on the CPU):
+//   IN[n] = AND_{p in preds(n)} OUT[p]     IN[entry] = (H=1, D=0)
+//   host   node: H' = H | A          D' = D & ~B
+//   kernel node: H' = H & ~B         D' = D | (A & ~(F & H_in)),  F = A & ~B & S
+// (A = R|W, B = W, S = scalar-variable mask; gen/kill effects of
+// dartomp/dataflow.py:299-378, AND meet of dataflow.py:130-134.)
+// H does not depend on D: the H planes are solved to their greatest fixpoint
+// first, then D.
+//
+// Schedule: frontier-driven chaotic relaxation.  A warp owns one node row at
+// a time (V = 4096 variables = 512 B per plane row = one 16-B load per lane,
+// fully coalesced); warps pull chunks of consecutive nodes from an atomic
+// counter and sweep them in node order, carrying OUT[n-1] in registers (the
+// CFG's fall-through edge), so a round propagates information along the whole
+// chunk (Gauss-Seidel) instead of one edge (Jacobi).  Other predecessors are
+// read from HBM with whatever value they hold; every value read is >= the
+// fixpoint, so for this monotone framework the iteration converges to the
+// unique greatest fixpoint regardless of order.  A node is re-evaluated in
+// round r only if one of its predecessors changed in round r-1 or r
+// (per-node change stamps = the frontier); unchanged rows are not rewritten.
+// The host stops when a round changes nothing.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include "../../include/dfx.h"
+#include "c3gen.cuh"
+#include "dfx_internal.h"
+
+namespace dfx {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint4 and4(uint4 a, uint4 b) { return make_uint4(a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w); }
+__device__ __forceinline__ uint4 or4(uint4 a, uint4 b) { return make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w); }
+__device__ __forceinline__ uint4 andn4(uint4 a, uint4 b) { return make_uint4(a.x & ~b.x, a.y & ~b.y, a.z & ~b.z, a.w & ~b.w); }
+__device__ __forceinline__ bool nz4(uint4 a) { return (a.x | a.y | a.z | a.w) != 0u; }
+__device__ __forceinline__ bool ne4(uint4 a, uint4 b) { return ((a.x ^ b.x) | (a.y ^ b.y) | (a.z ^ b.z) | (a.w ^ b.w)) != 0u; }
+__device__ __forceinline__ uint4 all4() { return make_uint4(FULL, FULL, FULL, FULL); }
+__device__ __forceinline__ uint4 zero4() { return make_uint4(0u, 0u, 0u, 0u); }
+
+__device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
+// rows written by other warps during the same launch: bypass L1 (ld.global.cg)
+__device__ __forceinline__ uint4 ldcg4(const uint4* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------------------
+// C3 generator
+// ---------------------------------------------------------------------------
+__global__ void c3_degree_kernel(uint64_t seed, int64_t n_nodes, int32_t* deg) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x)
+    deg[n] = n == 0 ? 0 : 1 + c3_n_extra(seed, n);
+}
+
+__global__ void c3_cols_kernel(uint64_t seed, int64_t n_nodes, const int32_t* row_ptr,
+                               int32_t* col, uint8_t* kind) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    kind[n] = (uint8_t)c3_is_kernel(seed, n);
+    if (n == 0) continue;
+    int32_t e = row_ptr[n];
+    col[e++] = (int32_t)(n - 1);
+    int k = c3_n_extra(seed, n);
+    for (int j = 0; j < k; j++) col[e++] = (int32_t)c3_extra_pred(seed, n, j, n_nodes);
+  }
+}
+
+// one thread per (node, word)
+__global__ void c3_planes_kernel(uint64_t seed, int64_t n_nodes, int words, int w0,
+                                 uint32_t* A, uint32_t* B, uint32_t* USE) {
+  const int64_t total = n_nodes * words;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = i / words;
+    int w = (int)(i - n * words);
+    uint32_t r, wr;
+    c3_word(c3_node_key(seed, n), w0 + w, r, wr);
+    A[i] = r | wr;
+    B[i] = wr;
+    USE[i] = r;
+  }
+}
+
+// A = R | W from uploaded R (= USE) and W (= B) planes
+__global__ void or_planes_kernel(const uint4* R, const uint4* W, uint4* A, int64_t nq) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x)
+    A[i] = or4(ldg4(R + i), ldg4(W + i));
+}
+
+// ---------------------------------------------------------------------------
+// kernel (a): one relaxation round of one phase
+// ---------------------------------------------------------------------------
+struct RoundCounters {
+  unsigned long long chunk;      // work queue
+  unsigned long long changed;    // rows changed this round
+  unsigned long long evaluated;  // rows evaluated this round
+  unsigned long long rows_read;  // 16-B*32 row loads (state + planes)
+  unsigned long long rows_written;
+};
+
+template <int PHASE, int VPL>
+__global__ void __launch_bounds__(256)
+mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
+                 RoundCounters* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int nq = p.words >> 2;                 // uint4 per row
+  const uint4* A = reinterpret_cast<const uint4*>(p.A);
+  const uint4* B = reinterpret_cast<const uint4*>(p.B);
+  const uint4* OH = reinterpret_cast<const uint4*>(p.OH);
+  uint4* OUT = reinterpret_cast<uint4*>(PHASE == 0 ? p.OH : p.OD);
+  const uint4* S4 = reinterpret_cast<const uint4*>(p.S);
+
+  uint4 smask[VPL];
+  bool active[VPL];
+  bool any_s = false;
+#pragma unroll
+  for (int v = 0; v < VPL; v++) {
+    int q = lane + 32 * v;
+    active[v] = q < nq;
+    smask[v] = active[v] ? ldg4(S4 + q) : zero4();
+    any_s |= nz4(smask[v]);
+  }
+  const uint4 boundary = PHASE == 0 ? all4() : zero4();
+
+  unsigned long long n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;
+  for (;;) {
+    int chunk = 0;
+    if (lane == 0) chunk = (int)atomicAdd(&cnt->chunk, 1ull);
+    chunk = __shfl_sync(FULL, chunk, 0);
+    if (chunk >= n_chunks) break;
+    const int n0 = chunk * chunk_nodes;
+    const int n1 = min(n0 + chunk_nodes, (int)p.n_nodes);
+    uint4 prev[VPL];
+    int prev_n = -2;
+    for (int nb = n0; nb < n1; nb += 32) {
+      // per-node metadata for 32 nodes at once (lane = node)
+      const int n = nb + lane;
+      const bool valid = n < n1;
+      int rs = 0, re = 0, kd = 0;
+      bool dirty = false;
+      if (valid) {
+        rs = __ldg(p.row_ptr + n);
+        re = __ldg(p.row_ptr + n + 1);
+        kd = __ldg(p.kind + n);
+        dirty = first != 0;
+        if (!first)
+          for (int e = rs; e < re && !dirty; e++)
+            dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= round - 1;
+      }
+      unsigned dm = __ballot_sync(FULL, dirty);
+      while (dm) {
+        const int j = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int nn = nb + j;
+        const int nrs = __shfl_sync(FULL, rs, j), nre = __shfl_sync(FULL, re, j);
+        const bool kern = __shfl_sync(FULL, kd, j) != 0;
+        const size_t row = (size_t)nn * nq;
+        // transfer-plane rows
+        uint4 pa[VPL], pb[VPL], old[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; v++) {
+          const int q = lane + 32 * v;
+          pa[v] = pb[v] = zero4();
+          if (!active[v]) continue;
+          if (PHASE == 0) {
+            if (kern) pb[v] = ldg4(B + row + q); else pa[v] = ldg4(A + row + q);
+          } else {
+            if (kern) {
+              pa[v] = ldg4(A + row + q);
+              if (nz4(smask[v])) pb[v] = ldg4(B + row + q);
+            } else {
+              pb[v] = ldg4(B + row + q);
+            }
+          }
+          old[v] = first ? all4() : ldcg4(OUT + row + q);
+        }
+        n_read += 1 + (first ? 0 : 1);
+        // meet over predecessors
+        uint4 in[VPL], hin[VPL];
+        const bool need_hin = PHASE == 1 && kern && any_s;
+#pragma unroll
+        for (int v = 0; v < VPL; v++) { in[v] = nre == nrs ? boundary : all4(); hin[v] = all4(); }
+        for (int e = nrs; e < nre; e += 32) {
+          const int ce = min(32, nre - e);
+          const int pid = lane < ce ? __ldg(p.col + e + lane) : 0;
+          for (int t = 0; t < ce; t++) {
+            const int q = __shfl_sync(FULL, pid, t);
+            const bool chain = q == nn - 1 && prev_n == nn - 1;
+            if (chain) {
+#pragma unroll
+              for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
+            } else if (!first) {
+#pragma unroll
+              for (int v = 0; v < VPL; v++)
+                if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)q * nq + lane + 32 * v));
+              n_read++;
+            }
+            if (need_hin) {
+#pragma unroll
+              for (int v = 0; v < VPL; v++)
+                if (active[v] && nz4(smask[v]))
+                  hin[v] = and4(hin[v], ldg4(OH + (size_t)q * nq + lane + 32 * v));
+            }
+          }
+        }
+        // transfer
+        bool ch = false;
+        uint4 out[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; v++) {
+          if (PHASE == 0) {
+            out[v] = kern ? andn4(in[v], pb[v]) : or4(in[v], pa[v]);
+          } else if (kern) {
+            const uint4 f = and4(andn4(pa[v], pb[v]), smask[v]);
+            out[v] = or4(in[v], andn4(pa[v], and4(f, hin[v])));
+          } else {
+            out[v] = andn4(in[v], pb[v]);
+          }
+          ch |= active[v] && ne4(out[v], old[v]);
+        }
+        ch = __any_sync(FULL, ch);
+        n_eval++;
+        if (ch || first) {
+#pragma unroll
+          for (int v = 0; v < VPL; v++)
+            if (active[v]) __stcg(OUT + row + lane + 32 * v, out[v]);
+          n_written++;
+        }
+        if (lane == 0) p.stamp[nn] = ch ? round : (first ? 0 : p.stamp[nn]);
+        n_changed += ch;
+#pragma unroll
+        for (int v = 0; v < VPL; v++) prev[v] = out[v];
+        prev_n = nn;
+      }
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&cnt->changed, n_changed);
+    atomicAdd(&cnt->evaluated, n_eval);
+    atomicAdd(&cnt->rows_read, n_read);
+    atomicAdd(&cnt->rows_written, n_written);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel (b): requirement planes + per-node nonzero-word counts
+// ---------------------------------------------------------------------------
+template <int VPL>
+__global__ void __launch_bounds__(256)
+requirements_kernel(CsrDev p, int32_t* counts) {
+  const int lane = threadIdx.x & 31;
+  const int nq = p.words >> 2;
+  const uint4* A = reinterpret_cast<const uint4*>(p.A);
+  const uint4* B = reinterpret_cast<const uint4*>(p.B);
+  const uint4* U = reinterpret_cast<const uint4*>(p.USE);
+  const uint4* OH = reinterpret_cast<const uint4*>(p.OH);
+  const uint4* OD = reinterpret_cast<const uint4*>(p.OD);
+  uint4* REQ = reinterpret_cast<uint4*>(p.REQ);
+  uint4* FPQ = reinterpret_cast<uint4*>(p.FPQ);
+  const uint4* S4 = reinterpret_cast<const uint4*>(p.S);
+  uint4 smask[VPL];
+  bool active[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; v++) {
+    int q = lane + 32 * v;
+    active[v] = q < nq;
+    smask[v] = active[v] ? ldg4(S4 + q) : zero4();
+  }
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < p.n_nodes; n += warps) {
+    const int rs = __ldg(p.row_ptr + n), re = __ldg(p.row_ptr + n + 1);
+    const bool kern = __ldg(p.kind + n) != 0;
+    const size_t row = (size_t)n * nq;
+    uint4 ih[VPL], id[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; v++) { ih[v] = all4(); id[v] = re == rs ? zero4() : all4(); }
+    for (int e = rs; e < re; e++) {
+      const int q = __ldg(p.col + e);
+#pragma unroll
+      for (int v = 0; v < VPL; v++)
+        if (active[v]) {
+          ih[v] = and4(ih[v], ldg4(OH + (size_t)q * nq + lane + 32 * v));
+          id[v] = and4(id[v], ldg4(OD + (size_t)q * nq + lane + 32 * v));
+        }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int v = 0; v < VPL; v++) {
+      if (!active[v]) continue;
+      const int q = lane + 32 * v;
+      const uint4 use = ldg4(U + row + q);
+      uint4 req, fp = zero4();
+      if (!kern) {
+        req = andn4(use, ih[v]);
+      } else {
+        uint4 f = zero4();
+        if (nz4(smask[v])) f = and4(andn4(ldg4(A + row + q), ldg4(B + row + q)), smask[v]);
+        req = or4(andn4(andn4(use, f), id[v]), andn4(andn4(f, id[v]), ih[v]));
+        fp = and4(andn4(f, id[v]), ih[v]);
+      }
+      __stcs(REQ + row + q, req);
+      cnt += (req.x != 0) + (req.y != 0) + (req.z != 0) + (req.w != 0);
+      if (p.fp_slot[q] >= 0) {
+        FPQ[(size_t)n * p.n_fp_slots + p.fp_slot[q]] = fp;
+        cnt += (fp.x != 0) + (fp.y != 0) + (fp.z != 0) + (fp.w != 0);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    if (lane == 0) counts[n] = cnt;
+  }
+}
+
+// order-preserving compaction: node-major; requirement words ascending, then
+// firstprivate words ascending
+template <int VPL>
+__global__ void __launch_bounds__(256)
+compact_kernel(CsrDev p, const int64_t* offsets, dfx_req_record* out, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int nq = p.words >> 2;
+  const uint4* REQ = reinterpret_cast<const uint4*>(p.REQ);
+  const uint4* FPQ = reinterpret_cast<const uint4*>(p.FPQ);
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < p.n_nodes; n += warps) {
+    int64_t base = offsets[n];
+    const uint8_t kind = __ldg(p.kind + n) ? 2 : 1;
+    const size_t row = (size_t)n * nq;
+    for (int pass = 0; pass < 2; pass++) {
+#pragma unroll
+      for (int v = 0; v < VPL; v++) {
+        const int q = lane + 32 * v;
+        uint4 m = zero4();
+        if (q < nq) {
+          if (pass == 0) m = ldg4(REQ + row + q);
+          else if (p.fp_slot[q] >= 0) m = ldg4(FPQ + (size_t)n * p.n_fp_slots + p.fp_slot[q]);
+        }
+        uint32_t w4[4] = {m.x, m.y, m.z, m.w};
+        int c = (w4[0] != 0) + (w4[1] != 0) + (w4[2] != 0) + (w4[3] != 0);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int64_t pos = base + incl - c;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (w4[k]) {
+            if (pos < cap) {
+              dfx_req_record r;
+              r.node = n; r.word = (uint16_t)(4 * q + k); r.kind = pass ? 3 : kind; r.pad = 0;
+              r.mask = w4[k];
+              out[pos] = r;
+            }
+            pos++;
+          }
+        base += __shfl_sync(FULL, incl, 31);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side drivers
+// ---------------------------------------------------------------------------
+static int grid_for(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch,
+                size_t scratch_bytes) {
+  int32_t* deg = p.row_ptr + 1;  // degrees land in row_ptr[1..n], scanned in place
+  c3_degree_kernel<<<grid_for(p.n_nodes, 256), 256, 0, st>>>(seed, p.n_nodes, deg);
+  if (cudaMemsetAsync(p.row_ptr, 0, sizeof(int32_t), st) != cudaSuccess) return DFX_E_CUDA;
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, deg, deg, (int)p.n_nodes, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, deg, deg, (int)p.n_nodes, st);
+  c3_cols_kernel<<<grid_for(p.n_nodes, 256), 256, 0, st>>>(seed, p.n_nodes, p.row_ptr, p.col,
+                                                           p.kind);
+  c3_planes_kernel<<<grid_for(p.n_nodes * p.words, 256), 256, 0, st>>>(
+      seed, p.n_nodes, p.words, w0, p.A, p.B, p.USE);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int or_planes(const CsrDev& p, cudaStream_t st) {
+  int64_t nq = p.n_nodes * (p.words / 4);
+  or_planes_kernel<<<grid_for(nq, 256), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(p.USE), reinterpret_cast<const uint4*>(p.B),
+      reinterpret_cast<uint4*>(p.A), nq);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+template <int PHASE>
+static int launch_round(const CsrDev& p, int vpl, int round, int first, int chunk_nodes,
+                        int n_chunks, RoundCounters* cnt, cudaStream_t st, int blocks) {
+  switch (vpl) {
+    case 1: mfp_round_kernel<PHASE, 1><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
+    case 2: mfp_round_kernel<PHASE, 2><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
+    case 4: mfp_round_kernel<PHASE, 4><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
+    default: return DFX_E_LIMIT;
+  }
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int vpl_for(int words) {
+  int nq = words / 4;
+  if (words % 4) return -1;
+  if (nq <= 32) return 1;
+  if (nq <= 64) return 2;
+  if (nq <= 128) return 4;
+  return -1;
+}
+
+int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_nodes,
+              int max_rounds, SolveStats* stats) {
+  const int vpl = vpl_for(p.words);
+  if (vpl < 0) return DFX_E_LIMIT;
+  const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfp_round_kernel<0, 1>, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  int blocks = sms * per_sm;
+  stats->rounds[0] = stats->rounds[1] = 0;
+  stats->evaluated = stats->rows_read = stats->rows_written = 0;
+  RoundCounters h{};
+  for (int phase = 0; phase < 2; phase++) {
+    for (int r = 1; r <= max_rounds; r++) {
+      if (cudaMemsetAsync(d_cnt, 0, sizeof(RoundCounters), st) != cudaSuccess) return DFX_E_CUDA;
+      int rc = phase == 0 ? launch_round<0>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks)
+                          : launch_round<1>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks);
+      if (rc != DFX_OK) return rc;
+      if (cudaMemcpyAsync(&h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
+      if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
+      stats->rounds[phase] = r;
+      stats->evaluated += (int64_t)h.evaluated;
+      stats->rows_read += (int64_t)h.rows_read;
+      stats->rows_written += (int64_t)h.rows_written;
+      if (r > 1 && h.changed == 0) break;
+      if (r == max_rounds) return DFX_E_LIMIT;
+    }
+  }
+  return DFX_OK;
+}
+
+int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                 size_t scratch_bytes, dfx_req_record* out, int64_t cap, int64_t* n_out,
+                 cudaStream_t st) {
+  const int vpl = vpl_for(p.words);
+  int blocks = grid_for(p.n_nodes * 32, 256);
+  switch (vpl) {
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts); break;
+    default: return DFX_E_LIMIT;
+  }
+  // offsets[0] = 0; offsets[1..n] = inclusive prefix of counts
+  if (cudaMemsetAsync(offsets, 0, sizeof(int64_t), st) != cudaSuccess) return DFX_E_CUDA;
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, counts, offsets + 1, (int)p.n_nodes, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, counts, offsets + 1, (int)p.n_nodes, st);
+  if (cudaMemcpyAsync(n_out, offsets + p.n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, st) !=
+      cudaSuccess)
+    return DFX_E_CUDA;
+  if (out) {
+    switch (vpl) {
+      case 1: compact_kernel<1><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
+      case 2: compact_kernel<2><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
+      case 4: compact_kernel<4><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
+    }
+  }
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+size_t scan_scratch_bytes(int64_t n) {
+  size_t a = 0, b = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  cub::DeviceScan::InclusiveSum(nullptr, b, (int32_t*)nullptr, (int64_t*)nullptr, (int)n);
+  return (a > b ? a : b) + 256;
+}
+
+}  // namespace dfx
+
+namespace dfx {
+size_t round_counters_bytes() { return sizeof(RoundCounters); }
+}  // namespace dfx

@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: data-flow facts/sec to fixpoint on configuration C3.
+
+Workload (BASELINE.json configs[2], the HBM-roofline configuration): one
+synthetic CFG of 2^20 nodes, average in-degree 2.5, 4096 variables per GPU,
+20% kernel nodes, 1/32 access density, 2% firstprivate-eligible scalars
+(DESIGN.md §C3).  A step = one solve of kernel (a) to the fixpoint from
+scratch (both the host-valid and the device-valid phases, all rounds).
+Facts = nodes x variables.  Multi-GPU: V-sharded weak scaling -- rank r owns
+variables [4096 r, 4096 (r+1)) of the same graph; no collective touches the
+data path (variables are independent); timing is the max over
+ranks.
+
+Contract: python bench.py --gpus N --steps K --warmup W  (torchrun for N>1)
+prints ONE JSON line on rank 0.  `--impl reference` times the reference path
+on the host cores instead: the reference package cannot ingest a CSR graph
+(SURVEY §8c), so the reference arm is the C restatement of the same equations
+(oracle/mfp_oracle.c, "port"), all host threads, on a bounded column sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "dataflow facts/sec to fixpoint (CFG nodes×vars) at 1/2/4/8 B200; %HBM roofline"
+UNIT = "facts/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-nodes", type=int, default=1 << 20)
+    ap.add_argument("--vars-per-gpu", type=int, default=4096)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--chunk", type=int, default=0, help="nodes per warp task (0: default)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(args, world):
+    return {"workload": "C3: single synthetic CFG, %d nodes x %d vars/GPU, avg in-degree 2.5"
+                        % (args.n_nodes, args.vars_per_gpu),
+            "n_nodes": args.n_nodes, "vars_per_gpu": args.vars_per_gpu,
+            "total_vars": args.vars_per_gpu * world, "avg_in_degree": 2.5,
+            "kernel_node_frac": 0.2, "access_density": 1 / 32, "scalar_frac": 0.02,
+            "seed": args.seed, "parallelism": "V-sharded weak scaling, %d GPU(s)" % world,
+            "l2": "no flush needed: inputs+state 2.5 GB/GPU >> 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unparsed"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profiles():
+    p = ROOT / "profiles" / "roofline_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch"), d
+    return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the C restatement on the host cores
+# ---------------------------------------------------------------------------
+def cpu_sample(args, steps=1):
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _oracle  # noqa: E402  (cpu_baseline leg: the only bench use of oracle/)
+    threads = _oracle.num_threads()
+    words = max(4, min(args.vars_per_gpu // 32, 4 * threads))
+    n_scalar = int(round(0.02 * args.vars_per_gpu))
+    g = _oracle.c3_generate(args.seed, args.n_nodes, 0, words, n_scalar)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _oracle.c3_solve(g)
+        times.append(time.perf_counter() - t0)
+    facts = args.n_nodes * words * 32
+    t = statistics.median(times)
+    return {"value": facts / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "oracle/mfp_oracle.c Gauss-Seidel solve of the same C3 graph "
+                      "(%d nodes), variable columns 0..%d (%d of %d vars; variables are "
+                      "independent so the block is an exact sample), median of %d"
+                      % (args.n_nodes, words * 32 - 1, words * 32, args.vars_per_gpu, steps),
+            "seconds_per_sample": t}, times
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    base, times = cpu_sample(args, steps=args.warmup + args.steps)
+    timed = times[args.warmup:] or times
+    t = sum(timed) / len(timed)
+    words = int(base["sample"].split("columns 0..")[1].split(" ")[0]) + 1
+    facts = args.n_nodes * words
+    value = facts / t
+    base["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (counter-hash generator, DESIGN.md §C3)",
+            "config": workload_config(args, 1), "impl": "reference", "cpu_baseline": base,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_13881_b200 import _abi
+    from paper_2406_13881_b200.csr import C3Config, CsrProblem, c3_scalar_mask, mfp_csr
+
+    torch.cuda.set_device(local)
+    eng = _abi.engine(local)
+    stream = torch.cuda.current_stream()
+    eng.lib.dfx_set_stream(eng.h, __import__("ctypes").c_void_p(stream.cuda_stream))
+    cfg = C3Config(n_nodes=args.n_nodes, n_vars=args.vars_per_gpu, seed=args.seed,
+                   w0=rank * (args.vars_per_gpu // 32))
+    prob = CsrProblem.generate_c3(cfg, eng)
+    for _ in range(max(3, args.warmup)):
+        prob.solve(args.chunk)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    kernel_ms, launches, stats_last = 0.0, 0, None
+    barrier()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = prob.solve(args.chunk)
+            kernel_ms += st.kernel_ms
+            launches += st.rounds_h + st.rounds_d
+            stats_last = {k: getattr(st, k) for k, _ in st._fields_}
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    total_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    facts_total = args.n_nodes * args.vars_per_gpu * world
+    value = facts_total / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (mfp_round_kernel): algorithmic bytes
+    # counted by the kernel itself / its own launch time
+    rowb = cfg.words * 4
+    nnz = prob.eng.lib.dfx_csr_nnz(prob.h)
+    rounds = stats_last["rounds_h"] + stats_last["rounds_d"]
+    meta = rounds * (5 * args.n_nodes + 8 * nnz) + 4 * stats_last["evaluated"]
+    bytes_per_solve = (stats_last["rows_read"] + stats_last["rows_written"]) * rowb + meta
+    kernel_ms_per_solve = kernel_ms / args.steps
+    achieved = bytes_per_solve / (kernel_ms_per_solve / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic, _ = traffic_from_profiles()
+    survey_bytes = stats_last["evaluated"] * args.vars_per_gpu * (11 / 16)
+
+    # kernel (b) once (not part of the fixpoint metric), for the record
+    rec = prob.requirements()
+    req_ms = prob.stats.req_ms
+
+    # e2e: the reference-facing all-in-one C-ABI call with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        def pinned(shape, dtype):
+            n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            buf = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            return buf.numpy().view(dtype).reshape(shape)
+        rp, col, kind, R, W = prob.export_inputs(alloc=pinned)
+        S = c3_scalar_mask(cfg)
+        h2d = rp.nbytes + col.nbytes + kind.nbytes + R.nbytes + W.nbytes + S.nbytes
+        recs, _ = mfp_csr(rp, col, kind, R, W, S, eng)          # warm (allocates)
+        assert recs.shape[0] == rec.shape[0], "e2e records differ from device-resident run"
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.e2e_steps):
+            recs, _ = mfp_csr(rp, col, kind, R, W, S, eng)
+            d2h += recs.nbytes
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64,
+                          device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
+               "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h // args.e2e_steps),
+               "path": "dfx_mfp_csr (host buffers, pinned): H2D inputs, kernels (a)+(b), "
+                       "D2H compacted requirement records"}
+
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (counter-hash generator, DESIGN.md §C3)",
+            "config": workload_config(args, world),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "mfp_round_kernel",
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_solve": bytes_per_solve,
+                         "launches_per_solve": rounds,
+                         "kernel_ms_per_solve": kernel_ms_per_solve,
+                         "survey_formula_frac": survey_bytes / (kernel_ms_per_solve / 1e3) / 1e9 / peak},
+            "solve": {"rounds_h": stats_last["rounds_h"], "rounds_d": stats_last["rounds_d"],
+                      "evaluated_rows": stats_last["evaluated"],
+                      "rows_read": stats_last["rows_read"],
+                      "rows_written": stats_last["rows_written"],
+                      "device_ms_incl_round_checks": ms_per_step},
+            "requirements": {"kernel": "requirements_kernel + compact_kernel",
+                             "ms": req_ms, "records": int(rec.shape[0])}}
+    if world == 1 and not args.no_cpu_baseline:
+        base, _ = cpu_sample(args, steps=1)
+        line["cpu_baseline"] = base
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

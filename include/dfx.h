@@ -187,7 +187,9 @@ typedef struct {
   int32_t rounds_h, rounds_d;   /* relaxation rounds per phase (incl. the last, unchanged one) */
   int64_t evaluated;            /* node-row evaluations (both phases) */
   int64_t rows_read, rows_written; /* 512-B-per-4096-var row transfers counted by the kernel */
-  float solve_ms;               /* device time of kernel (a), all rounds */
+  float solve_ms;               /* device time of kernel (a), all rounds, incl. the
+                                   host round-trip that checks convergence */
+  float kernel_ms;              /* sum of the round-kernel durations alone */
   float req_ms;                 /* device time of kernel (b) incl. compaction */
   int64_t n_records;
 } dfx_csr_stats;
@@ -206,6 +208,11 @@ int dfx_csr_requirements(dfx_handle *h, dfx_csr *p, dfx_req_record *out, int64_t
 /* D2H of the fixpoint OUT planes and the dense requirement plane (any NULL
  * pointer is skipped) */
 int dfx_csr_download(dfx_handle *h, dfx_csr *p, uint32_t *out_h, uint32_t *out_d, uint32_t *req);
+/* D2H of the problem's inputs (row_ptr [n+1], col [nnz], node_kind [n],
+ * R, W [n*words]); any NULL pointer is skipped */
+int dfx_csr_export(dfx_handle *h, dfx_csr *p, int32_t *row_ptr, int32_t *col, uint8_t *node_kind,
+                   uint32_t *R, uint32_t *W);
+int64_t dfx_csr_nnz(dfx_csr *p);
 /* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of records */
 int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_record *out, int64_t cap,
                 dfx_csr_stats *stats);

@@ -32,7 +32,7 @@ class CsrStats(C.Structure):
     _fields_ = [("rounds_h", C.c_int32), ("rounds_d", C.c_int32),
                 ("evaluated", C.c_int64), ("rows_read", C.c_int64),
                 ("rows_written", C.c_int64), ("solve_ms", C.c_float),
-                ("req_ms", C.c_float), ("n_records", C.c_int64)]
+                ("kernel_ms", C.c_float), ("req_ms", C.c_float), ("n_records", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -47,8 +47,10 @@ REQ_UPDATE_FROM, REQ_UPDATE_TO, REQ_FIRSTPRIVATE = 1, 2, 3
 
 def _setup(lib):
     for name in ("dfx_set_stream", "dfx_csr_create", "dfx_csr_generate_c3", "dfx_csr_destroy",
-                 "dfx_csr_solve", "dfx_csr_requirements", "dfx_csr_download", "dfx_mfp_csr"):
+                 "dfx_csr_solve", "dfx_csr_requirements", "dfx_csr_download", "dfx_mfp_csr",
+                 "dfx_csr_export"):
         getattr(lib, name).restype = C.c_int
+    lib.dfx_csr_nnz.restype = C.c_int64
 
 
 @dataclass
@@ -67,6 +69,19 @@ class C3Config:
     @property
     def n_scalar(self) -> int:
         return int(round(self.scalar_frac * self.n_vars))
+
+
+def c3_scalar_mask(cfg: C3Config) -> np.ndarray:
+    """Scalar-variable mask of a C3 slab: variables [0, n_scalar) (global
+    numbering) are the firstprivate-eligible scalars."""
+    out = np.zeros(cfg.words, dtype=np.uint32)
+    for w in range(cfg.words):
+        lo = 32 * (cfg.w0 + w)
+        if cfg.n_scalar >= lo + 32:
+            out[w] = 0xFFFFFFFF
+        elif cfg.n_scalar > lo:
+            out[w] = (1 << (cfg.n_scalar - lo)) - 1
+    return out
 
 
 class CsrProblem:
@@ -133,6 +148,20 @@ class CsrProblem:
             return self.requirements(int(self.stats.n_records))
         self.eng.check(rc, "dfx_csr_requirements")
         return out[: self.stats.n_records]
+
+    def export_inputs(self, alloc=np.empty):
+        """D2H of the inputs (row_ptr, col, kind, R, W); `alloc(shape, dtype)`
+        lets callers supply pinned host memory."""
+        nnz = int(self.eng.lib.dfx_csr_nnz(self.h))
+        rp = alloc((self.n_nodes + 1,), np.int32)
+        col = alloc((max(1, nnz),), np.int32)
+        kind = alloc((self.n_nodes,), np.uint8)
+        R = alloc((self.n_nodes, self.words), np.uint32)
+        W = alloc((self.n_nodes, self.words), np.uint32)
+        p = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        self.eng.check(self.eng.lib.dfx_csr_export(self.eng.h, self.h, p(rp), p(col), p(kind),
+                                                   p(R), p(W)), "dfx_csr_export")
+        return rp, col[:nnz], kind, R, W
 
     def download(self, out_h=True, out_d=True, req=False):
         shape = (self.n_nodes, self.words)

@@ -12,12 +12,16 @@
 #include "dfx_internal.h"
 #include "c3gen.cuh"
 
+struct dfx_csr;
+namespace { int csr_destroy_impl(dfx_csr* c); }
+
 struct dfx_handle {
   int device = 0;
   cudaStream_t stream = nullptr;      // the handle's own stream
   cudaStream_t ext_stream = nullptr;  // caller's stream (dfx_set_stream)
   cudaStream_t st() const { return ext_stream ? ext_stream : stream; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct dfx_csr* csr_cache = nullptr;   // reused by dfx_mfp_csr across calls
   std::unordered_map<std::string, std::pair<void*, size_t>> bufs;
 };
 
@@ -89,6 +93,7 @@ int dfx_close(dfx_handle* h) {
     if (kv.second.first) cudaFree(kv.second.first);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->csr_cache) csr_destroy_impl(h->csr_cache);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return DFX_OK;
@@ -282,6 +287,33 @@ int check_words(int64_t n, int words) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// H2D of one problem's inputs into already-allocated buffers (+ A = R|W)
+int csr_upload(dfx_csr* c, const dfx_csr_in* in, cudaStream_t st) {
+  dfx::CsrDev& p = c->p;
+  const size_t plane = sizeof(uint32_t) * (size_t)in->n_nodes * in->words;
+  CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
+  if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.USE, in->R, plane, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
+  int rc = dfx::or_planes(p, st);
+  if (rc) return fail(rc, "or_planes launch failed");
+  return DFX_OK;
+}
+
+bool same_scalars(const dfx_csr* c, const uint32_t* S, int words) {
+  std::vector<uint32_t> cur(words);
+  if (cudaMemcpy(cur.data(), c->p.S, sizeof(uint32_t) * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return false;
+  return std::memcmp(cur.data(), S, sizeof(uint32_t) * words) == 0;
+}
+}  // namespace
+
+extern "C" {
+
 int dfx_csr_create(dfx_handle* h, const dfx_csr_in* in, dfx_csr** out) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_csr_create: null argument");
   CK(cudaSetDevice(h->device));
@@ -289,17 +321,8 @@ int dfx_csr_create(dfx_handle* h, const dfx_csr_in* in, dfx_csr** out) {
   if (rc) return rc;
   auto* c = new dfx_csr();
   rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
+  if (!rc) rc = csr_upload(c, in, h->st());
   if (rc) { csr_destroy_impl(c); return rc; }
-  dfx::CsrDev& p = c->p;
-  const size_t plane = sizeof(uint32_t) * (size_t)in->n_nodes * in->words;
-  cudaStream_t st = h->st();
-  CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
-  if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(p.USE, in->R, plane, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
-  rc = dfx::or_planes(p, st);
-  if (rc) { csr_destroy_impl(c); return fail(rc, "or_planes launch failed"); }
   *out = c;
   return DFX_OK;
 }
@@ -350,6 +373,7 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
     stats->rows_read = s.rows_read;
     stats->rows_written = s.rows_written;
     stats->solve_ms = ms;
+    stats->kernel_ms = s.kernel_ms;
   }
   return DFX_OK;
 }
@@ -401,14 +425,46 @@ int dfx_csr_download(dfx_handle* h, dfx_csr* c, uint32_t* out_h, uint32_t* out_d
   return DFX_OK;
 }
 
+int dfx_csr_export(dfx_handle* h, dfx_csr* c, int32_t* row_ptr, int32_t* col, uint8_t* kind,
+                   uint32_t* R, uint32_t* W) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_export: null argument");
+  CK(cudaSetDevice(h->device));
+  const dfx::CsrDev& p = c->p;
+  const size_t plane = sizeof(uint32_t) * (size_t)p.n_nodes * p.words;
+  cudaStream_t st = h->st();
+  if (row_ptr) CK(cudaMemcpyAsync(row_ptr, p.row_ptr, sizeof(int32_t) * (p.n_nodes + 1), cudaMemcpyDeviceToHost, st));
+  if (col && p.nnz) CK(cudaMemcpyAsync(col, p.col, sizeof(int32_t) * p.nnz, cudaMemcpyDeviceToHost, st));
+  if (kind) CK(cudaMemcpyAsync(kind, p.kind, p.n_nodes, cudaMemcpyDeviceToHost, st));
+  if (R) CK(cudaMemcpyAsync(R, p.USE, plane, cudaMemcpyDeviceToHost, st));
+  if (W) CK(cudaMemcpyAsync(W, p.B, plane, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DFX_OK;
+}
+
+int64_t dfx_csr_nnz(dfx_csr* c) { return c ? c->p.nnz : -1; }
+
 int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_record* out, int64_t cap,
                 dfx_csr_stats* stats) {
-  dfx_csr* c = nullptr;
-  int rc = dfx_csr_create(h, in, &c);
-  if (rc) return rc;
+  if (!h || !in) return fail(DFX_E_ARG, "dfx_mfp_csr: null argument");
+  CK(cudaSetDevice(h->device));
+  // device buffers persist in the handle across calls of the same shape
+  dfx_csr* c = h->csr_cache;
+  if (c && (c->p.n_nodes != in->n_nodes || c->p.words != in->words || c->p.nnz != in->nnz ||
+            !same_scalars(c, in->S, in->words))) {
+    csr_destroy_impl(c);
+    c = h->csr_cache = nullptr;
+  }
+  int rc;
+  if (!c) {
+    rc = dfx_csr_create(h, in, &c);
+    if (rc) return rc;
+    h->csr_cache = c;
+  } else {
+    rc = csr_upload(c, in, h->st());
+    if (rc) return rc;
+  }
   rc = dfx_csr_solve(h, c, 0, stats);
   if (!rc) rc = dfx_csr_requirements(h, c, out, cap, stats);
-  dfx_csr_destroy(h, c);
   return rc;
 }
 

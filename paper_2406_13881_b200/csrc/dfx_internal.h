@@ -53,6 +53,7 @@ struct CsrDev {
 struct SolveStats {
   int rounds[2];
   int64_t evaluated, rows_read, rows_written;
+  float kernel_ms;
 };
 
 struct RoundCounters;

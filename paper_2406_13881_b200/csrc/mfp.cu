@@ -434,14 +434,22 @@ int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_
   stats->rounds[0] = stats->rounds[1] = 0;
   stats->evaluated = stats->rows_read = stats->rows_written = 0;
   RoundCounters h{};
+  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (!ev[0]) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
+  stats->kernel_ms = 0.f;
   for (int phase = 0; phase < 2; phase++) {
     for (int r = 1; r <= max_rounds; r++) {
       if (cudaMemsetAsync(d_cnt, 0, sizeof(RoundCounters), st) != cudaSuccess) return DFX_E_CUDA;
+      cudaEventRecord(ev[0], st);
       int rc = phase == 0 ? launch_round<0>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks)
                           : launch_round<1>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks);
       if (rc != DFX_OK) return rc;
+      cudaEventRecord(ev[1], st);
       if (cudaMemcpyAsync(&h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
       if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
+      float kms = 0.f;
+      cudaEventElapsedTime(&kms, ev[0], ev[1]);
+      stats->kernel_ms += kms;
       stats->rounds[phase] = r;
       stats->evaluated += (int64_t)h.evaluated;
       stats->rows_read += (int64_t)h.rows_read;

@@ -173,15 +173,23 @@ typedef struct {                /* configuration C3 generator */
   int32_t n_scalar;             /* variables [0, n_scalar) are scalars */
 } dfx_c3_spec;
 
-typedef struct {                /* one insertion point: node x 32 variables */
-  int32_t node;
-  uint16_t word;
-  uint8_t kind;                 /* 1 update-from (host read of stale copy),
-                                   2 update-to (device read of stale copy),
-                                   3 firstprivate capture */
-  uint8_t pad;
-  uint32_t mask;
-} dfx_req_record;
+/* Kernel (b) output: order-preserving compaction of the requirement planes
+ * into sparse word-rows.  For node n, occ[n*occ_words .. +occ_words) holds
+ * two bitmaps of ceil(words/32) uint32 each: which requirement words and
+ * which firstprivate words are nonzero.  masks[row_off[n] .. row_off[n+1])
+ * lists the nonzero 32-variable masks: requirement words ascending, then
+ * firstprivate words ascending.  Requirement kind is implied by the node:
+ * host node -> update-from (host read of a stale host copy), kernel node ->
+ * update-to (device read of a stale device copy); firstprivate words mark
+ * scalars captured by value. */
+typedef struct {
+  int64_t *row_off;             /* [n_nodes+1] (NULL: not copied) */
+  uint32_t *occ;                /* [n_nodes*occ_words] (NULL: not copied) */
+  uint32_t *masks;              /* [cap] (NULL: count only) */
+  int64_t cap;
+  int64_t n_masks;              /* out */
+  int32_t occ_words;            /* out: 2*ceil(words/32) */
+} dfx_req_out;
 
 typedef struct {
   int32_t rounds_h, rounds_d;   /* relaxation rounds per phase (incl. the last, unchanged one) */
@@ -191,7 +199,7 @@ typedef struct {
                                    host round-trip that checks convergence */
   float kernel_ms;              /* sum of the round-kernel durations alone */
   float req_ms;                 /* device time of kernel (b) incl. compaction */
-  int64_t n_records;
+  int64_t n_masks;              /* kernel (b): nonzero 32-variable masks */
 } dfx_csr_stats;
 
 int dfx_set_stream(dfx_handle *h, void *cuda_stream);   /* NULL: the handle's own */
@@ -200,11 +208,9 @@ int dfx_csr_generate_c3(dfx_handle *h, const dfx_c3_spec *spec, dfx_csr **out);
 int dfx_csr_destroy(dfx_handle *h, dfx_csr *p);
 /* kernel (a); chunk_nodes <= 0 picks the default */
 int dfx_csr_solve(dfx_handle *h, dfx_csr *p, int32_t chunk_nodes, dfx_csr_stats *stats);
-/* kernel (b): requirement planes + order-preserving compaction into records
- * (node-major, word-ascending; firstprivate records after a node's
- * requirement records).  out may be NULL to only count. */
-int dfx_csr_requirements(dfx_handle *h, dfx_csr *p, dfx_req_record *out, int64_t cap,
-                         dfx_csr_stats *stats);
+/* kernel (b): requirement planes + order-preserving compaction (D2H of the
+ * parts of `out` that are non-NULL) */
+int dfx_csr_requirements(dfx_handle *h, dfx_csr *p, dfx_req_out *out, dfx_csr_stats *stats);
 /* D2H of the fixpoint OUT planes and the dense requirement plane (any NULL
  * pointer is skipped) */
 int dfx_csr_download(dfx_handle *h, dfx_csr *p, uint32_t *out_h, uint32_t *out_d, uint32_t *req);
@@ -213,9 +219,8 @@ int dfx_csr_download(dfx_handle *h, dfx_csr *p, uint32_t *out_h, uint32_t *out_d
 int dfx_csr_export(dfx_handle *h, dfx_csr *p, int32_t *row_ptr, int32_t *col, uint8_t *node_kind,
                    uint32_t *R, uint32_t *W);
 int64_t dfx_csr_nnz(dfx_csr *p);
-/* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of records */
-int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_record *out, int64_t cap,
-                dfx_csr_stats *stats);
+/* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of `out` */
+int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_out *out, dfx_csr_stats *stats);
 
 #ifdef __cplusplus
 }

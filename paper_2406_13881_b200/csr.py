@@ -32,17 +32,60 @@ class CsrStats(C.Structure):
     _fields_ = [("rounds_h", C.c_int32), ("rounds_d", C.c_int32),
                 ("evaluated", C.c_int64), ("rows_read", C.c_int64),
                 ("rows_written", C.c_int64), ("solve_ms", C.c_float),
-                ("kernel_ms", C.c_float), ("req_ms", C.c_float), ("n_records", C.c_int64)]
+                ("kernel_ms", C.c_float), ("req_ms", C.c_float), ("n_masks", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-REC_DTYPE = np.dtype([("node", np.int32), ("word", np.uint16), ("kind", np.uint8),
-                      ("pad", np.uint8), ("mask", np.uint32)])
-assert REC_DTYPE.itemsize == 12
+class ReqOut(C.Structure):
+    _fields_ = [("row_off", C.c_void_p), ("occ", C.c_void_p), ("masks", C.c_void_p),
+                ("cap", C.c_int64), ("n_masks", C.c_int64), ("occ_words", C.c_int32)]
+
 
 REQ_UPDATE_FROM, REQ_UPDATE_TO, REQ_FIRSTPRIVATE = 1, 2, 3
+
+
+@dataclass
+class ReqRows:
+    """Kernel (b) output: sparse word-rows of insertion points (include/dfx.h)."""
+    row_off: np.ndarray      # int64 [n+1]
+    occ: np.ndarray          # uint32 [n, occ_words]
+    masks: np.ndarray        # uint32 [n_masks]
+    words: int
+
+    @property
+    def nbytes(self) -> int:
+        return self.row_off.nbytes + self.occ.nbytes + self.masks.nbytes
+
+    def to_planes(self):
+        """Expand into dense (REQ, FP) planes [n, words]."""
+        n = self.row_off.shape[0] - 1
+        ow = self.occ.shape[1] // 2
+        bits = np.unpackbits(self.occ.view(np.uint8).reshape(n, 2 * ow, 4), axis=2,
+                             bitorder="little").reshape(n, 2, ow * 32)[:, :, : self.words]
+        req = np.zeros((n, self.words), dtype=np.uint32)
+        fp = np.zeros_like(req)
+        # order inside a node: requirement words ascending, then firstprivate
+        flat = np.concatenate([bits[:, 0, :], bits[:, 1, :]], axis=1).astype(bool)
+        assert int(flat.sum()) == self.masks.shape[0]
+        vals = np.zeros(flat.shape, dtype=np.uint32)
+        vals[flat] = self.masks
+        req[:] = vals[:, : self.words]
+        fp[:] = vals[:, self.words:]
+        return req, fp
+
+    def records(self, kind: np.ndarray):
+        """(node, word, kind, mask) records in stream order."""
+        req, fp = self.to_planes()
+        out = []
+        for n in range(req.shape[0]):
+            k = REQ_UPDATE_TO if kind[n] else REQ_UPDATE_FROM
+            for w in np.nonzero(req[n])[0]:
+                out.append((n, int(w), k, int(req[n, w])))
+            for w in np.nonzero(fp[n])[0]:
+                out.append((n, int(w), REQ_FIRSTPRIVATE, int(fp[n, w])))
+        return out
 
 
 def _setup(lib):
@@ -134,20 +177,16 @@ class CsrProblem:
                                                   C.byref(self.stats)), "dfx_csr_solve")
         return self.stats
 
-    def requirements(self, capacity: int | None = None) -> np.ndarray:
-        """Kernel (b): compacted insertion-point records (REC_DTYPE)."""
+    def requirements(self, capacity: int | None = None, alloc=np.empty) -> ReqRows:
+        """Kernel (b): requirement planes + order-preserving compaction."""
         if capacity is None:
-            self.eng.check(self.eng.lib.dfx_csr_requirements(self.eng.h, self.h, None, 0,
+            self.eng.check(self.eng.lib.dfx_csr_requirements(self.eng.h, self.h, None,
                                                              C.byref(self.stats)),
                            "dfx_csr_requirements(count)")
-            capacity = int(self.stats.n_records)
-        out = np.zeros(max(1, capacity), dtype=REC_DTYPE)
-        rc = self.eng.lib.dfx_csr_requirements(self.eng.h, self.h, C.c_void_p(out.ctypes.data),
-                                               C.c_int64(out.shape[0]), C.byref(self.stats))
-        if rc == _abi.DFX_E_NOSPC:
-            return self.requirements(int(self.stats.n_records))
-        self.eng.check(rc, "dfx_csr_requirements")
-        return out[: self.stats.n_records]
+            capacity = int(self.stats.n_masks)
+        return _req_call(lambda o: self.eng.lib.dfx_csr_requirements(
+            self.eng.h, self.h, C.byref(o), C.byref(self.stats)),
+            self.eng, self.n_nodes, self.words, capacity, alloc, self.stats)
 
     def export_inputs(self, alloc=np.empty):
         """D2H of the inputs (row_ptr, col, kind, R, W); `alloc(shape, dtype)`
@@ -174,32 +213,61 @@ class CsrProblem:
         return oh, od, rq
 
 
-def records_to_planes(rec: np.ndarray, n_nodes: int, words: int):
-    """Expand compacted records into (REQ, FP) planes (for checking)."""
-    req = np.zeros((n_nodes, words), dtype=np.uint32)
-    fp = np.zeros_like(req)
-    m = rec["kind"] == REQ_FIRSTPRIVATE
-    req[rec["node"][~m], rec["word"][~m]] = rec["mask"][~m]
-    fp[rec["node"][m], rec["word"][m]] = rec["mask"][m]
-    return req, fp
+def _req_call(call, eng, n_nodes, words, capacity, alloc, stats) -> ReqRows:
+    ow = 2 * ((words + 31) // 32)
+    while True:
+        row_off = alloc((n_nodes + 1,), np.int64)
+        occ = alloc((n_nodes, ow), np.uint32)
+        masks = alloc((max(1, capacity),), np.uint32)
+        o = ReqOut(row_off.ctypes.data, occ.ctypes.data, masks.ctypes.data,
+                   masks.shape[0], 0, 0)
+        rc = call(o)
+        if rc == _abi.DFX_E_NOSPC:
+            capacity = int(o.n_masks)
+            continue
+        eng.check(rc, "requirements")
+        return ReqRows(row_off, occ, masks[: o.n_masks], words)
+
+
+class MfpSession:
+    """Reference-facing all-in-one host-buffer path (`dfx_mfp_csr`): H2D of
+    the inputs, kernels (a)+(b), D2H of the compacted requirement rows.
+    Output host buffers are reused across calls (optionally pinned)."""
+
+    def __init__(self, eng: _abi.Engine | None = None, alloc=np.empty):
+        self.eng = eng or _abi.engine()
+        _setup(self.eng.lib)
+        self.alloc = alloc
+        self.capacity = 0
+        self.stats = CsrStats()
+        self._bufs = None
+
+    def run(self, row_ptr, col, kind, R, W, S) -> ReqRows:
+        n, words = R.shape
+        arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, R, W, S)]
+        cin = CsrIn(n, words, int(arrs[1].shape[0]), *(a.ctypes.data for a in arrs))
+        if self.capacity == 0:
+            self.capacity = max(1024, n * words // 2)
+        ow = 2 * ((words + 31) // 32)
+        while True:
+            if self._bufs is None or self._bufs[2].shape[0] < self.capacity \
+                    or self._bufs[0].shape[0] != n + 1:
+                self._bufs = (self.alloc((n + 1,), np.int64), self.alloc((n, ow), np.uint32),
+                              self.alloc((self.capacity,), np.uint32))
+            row_off, occ, masks = self._bufs
+            o = ReqOut(row_off.ctypes.data, occ.ctypes.data, masks.ctypes.data,
+                       masks.shape[0], 0, 0)
+            rc = self.eng.lib.dfx_mfp_csr(self.eng.h, C.byref(cin), C.byref(o),
+                                          C.byref(self.stats))
+            if rc == _abi.DFX_E_NOSPC:
+                self.capacity = int(o.n_masks)
+                continue
+            self.eng.check(rc, "dfx_mfp_csr")
+            return ReqRows(row_off, occ, masks[: o.n_masks], words)
 
 
 def mfp_csr(row_ptr, col, kind, R, W, S, eng: _abi.Engine | None = None):
-    """All-in-one host-buffer call (`dfx_mfp_csr`): H2D, kernels (a)+(b), D2H
-    of the compacted records.  Returns (records, stats)."""
-    eng = eng or _abi.engine()
-    _setup(eng.lib)
-    n, words = R.shape
-    arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, R, W, S)]
-    cin = CsrIn(n, words, int(arrs[1].shape[0]), *(a.ctypes.data for a in arrs))
-    stats = CsrStats()
-    cap = max(1024, n * words // 4)
-    while True:
-        out = np.zeros(cap, dtype=REC_DTYPE)
-        rc = eng.lib.dfx_mfp_csr(eng.h, C.byref(cin), C.c_void_p(out.ctypes.data),
-                                 C.c_int64(cap), C.byref(stats))
-        if rc == _abi.DFX_E_NOSPC:
-            cap = int(stats.n_records)
-            continue
-        eng.check(rc, "dfx_mfp_csr")
-        return out[: stats.n_records], stats
+    """One-shot all-in-one call; returns (ReqRows, stats)."""
+    sess = MfpSession(eng)
+    rows = sess.run(row_ptr, col, kind, R, W, S)
+    return rows, sess.stats

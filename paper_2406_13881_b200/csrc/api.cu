@@ -206,8 +206,9 @@ struct dfx_csr {
   size_t scratch_bytes = 0;
   int32_t* counts = nullptr;
   int64_t* offsets = nullptr;
-  dfx_req_record* d_records = nullptr;
-  int64_t records_cap = 0;
+  uint32_t* d_masks = nullptr;
+  int64_t masks_cap = 0;
+  uint32_t* d_occ = nullptr;
   void* d_cnt = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
@@ -225,7 +226,8 @@ T* csr_alloc(dfx_csr* c, size_t n) {
 int csr_destroy_impl(dfx_csr* c) {
   if (!c) return DFX_OK;
   for (void* p : c->allocs) cudaFree(p);
-  if (c->d_records) cudaFree(c->d_records);
+  if (c->d_masks) cudaFree(c->d_masks);
+  if (c->d_occ) cudaFree(c->d_occ);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   delete c;
@@ -378,38 +380,49 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
   return DFX_OK;
 }
 
-int dfx_csr_requirements(dfx_handle* h, dfx_csr* c, dfx_req_record* out, int64_t cap,
-                         dfx_csr_stats* stats) {
+int dfx_csr_requirements(dfx_handle* h, dfx_csr* c, dfx_req_out* out, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_requirements: null argument");
   CK(cudaSetDevice(h->device));
   cudaStream_t st = h->st();
-  // records buffer on device: sized from the previous count or the cap
-  int64_t want = cap > 0 ? cap : 0;
-  if (out && want > c->records_cap) {
-    if (c->d_records) cudaFree(c->d_records);
-    c->d_records = nullptr;
-    CK(cudaMalloc(&c->d_records, sizeof(dfx_req_record) * (size_t)want));
-    c->records_cap = want;
+  const dfx::CsrDev& p = c->p;
+  const int ow = 2 * ((p.words + 31) / 32);
+  if (!c->d_occ) {
+    CK(cudaMalloc(&c->d_occ, sizeof(uint32_t) * (size_t)p.n_nodes * ow));
+  }
+  int64_t want = (out && out->masks) ? out->cap : 0;
+  if (want > c->masks_cap) {
+    if (c->d_masks) cudaFree(c->d_masks);
+    c->d_masks = nullptr;
+    CK(cudaMalloc(&c->d_masks, sizeof(uint32_t) * (size_t)want));
+    c->masks_cap = want;
   }
   int64_t n_out = 0;
   CK(cudaEventRecord(c->e0, st));
-  int rc = dfx::requirements(c->p, c->counts, c->offsets, c->scratch, c->scratch_bytes,
-                             out ? c->d_records : nullptr, out ? want : 0, &n_out, st);
+  int rc = dfx::requirements(p, c->counts, c->offsets, c->scratch, c->scratch_bytes, c->d_occ,
+                             want ? c->d_masks : nullptr, want, &n_out, st);
   if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
   CK(cudaEventRecord(c->e1, st));
-  CK(cudaStreamSynchronize(st));
-  if (out && n_out) {
-    size_t ncopy = (size_t)(n_out < want ? n_out : want);
-    CK(cudaMemcpyAsync(out, c->d_records, sizeof(dfx_req_record) * ncopy, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));   // n_out is on the host now
+  if (out) {
+    out->n_masks = n_out;
+    out->occ_words = ow;
+    if (want && n_out) {
+      size_t ncopy = (size_t)(n_out < want ? n_out : want);
+      CK(cudaMemcpyAsync(out->masks, c->d_masks, sizeof(uint32_t) * ncopy, cudaMemcpyDeviceToHost, st));
+    }
+    if (want && out->occ)
+      CK(cudaMemcpyAsync(out->occ, c->d_occ, sizeof(uint32_t) * (size_t)p.n_nodes * ow, cudaMemcpyDeviceToHost, st));
+    if (want && out->row_off)
+      CK(cudaMemcpyAsync(out->row_off, c->offsets, sizeof(int64_t) * (size_t)(p.n_nodes + 1), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
   if (stats) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
     stats->req_ms = ms;
-    stats->n_records = n_out;
+    stats->n_masks = n_out;
   }
-  if (out && n_out > want) return fail(DFX_E_NOSPC, "record capacity %lld < %lld", (long long)want, (long long)n_out);
+  if (want && n_out > want) return fail(DFX_E_NOSPC, "mask capacity %lld < %lld", (long long)want, (long long)n_out);
   return DFX_OK;
 }
 
@@ -443,8 +456,7 @@ int dfx_csr_export(dfx_handle* h, dfx_csr* c, int32_t* row_ptr, int32_t* col, ui
 
 int64_t dfx_csr_nnz(dfx_csr* c) { return c ? c->p.nnz : -1; }
 
-int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_record* out, int64_t cap,
-                dfx_csr_stats* stats) {
+int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_out* out, dfx_csr_stats* stats) {
   if (!h || !in) return fail(DFX_E_ARG, "dfx_mfp_csr: null argument");
   CK(cudaSetDevice(h->device));
   // device buffers persist in the handle across calls of the same shape
@@ -464,7 +476,7 @@ int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_record* out, int64_
     if (rc) return rc;
   }
   rc = dfx_csr_solve(h, c, 0, stats);
-  if (!rc) rc = dfx_csr_requirements(h, c, out, cap, stats);
+  if (!rc) rc = dfx_csr_requirements(h, c, out, stats);
   return rc;
 }
 

@@ -64,8 +64,8 @@ int vpl_for(int words);
 int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_nodes,
               int max_rounds, SolveStats* stats);
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
-                 size_t scratch_bytes, dfx_req_record* out, int64_t cap, int64_t* n_out,
-                 cudaStream_t st);
+                 size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
+                 int64_t* n_out, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
 size_t round_counters_bytes();
 

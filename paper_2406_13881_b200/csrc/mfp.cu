@@ -136,6 +136,7 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
     const int n1 = min(n0 + chunk_nodes, (int)p.n_nodes);
     uint4 prev[VPL];
     int prev_n = -2;
+    bool carry = false;   // last node of the previous batch changed this round
     for (int nb = n0; nb < n1; nb += 32) {
       // per-node metadata for 32 nodes at once (lane = node)
       const int n = nb + lane;
@@ -152,6 +153,10 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
             dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= round - 1;
       }
       unsigned dm = __ballot_sync(FULL, dirty);
+      // fall-through successor of a node changed earlier in this sweep
+      if (carry && nb < n1) dm |= 1u;
+      carry = false;
+      const unsigned vmask = __ballot_sync(FULL, valid);
       while (dm) {
         const int j = __ffs(dm) - 1;
         dm &= dm - 1;
@@ -235,6 +240,10 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
 #pragma unroll
         for (int v = 0; v < VPL; v++) prev[v] = out[v];
         prev_n = nn;
+        if (ch && !first) {   // Gauss-Seidel: re-evaluate the successor now
+          if (j < 31) dm |= (1u << (j + 1)) & vmask;
+          else carry = true;
+        }
       }
     }
   }
@@ -315,19 +324,20 @@ requirements_kernel(CsrDev p, int32_t* counts) {
   }
 }
 
-// order-preserving compaction: node-major; requirement words ascending, then
-// firstprivate words ascending
+// order-preserving compaction into sparse word-rows: per node two occupancy
+// bitmaps (requirement words, firstprivate words) and the nonzero masks in
+// order (requirement words ascending, then firstprivate words ascending)
 template <int VPL>
 __global__ void __launch_bounds__(256)
-compact_kernel(CsrDev p, const int64_t* offsets, dfx_req_record* out, int64_t cap) {
+compact_kernel(CsrDev p, const int64_t* offsets, uint32_t* occ, uint32_t* masks, int64_t cap) {
   const int lane = threadIdx.x & 31;
   const int nq = p.words >> 2;
+  const int ow = (p.words + 31) >> 5;          // occupancy words per kind
   const uint4* REQ = reinterpret_cast<const uint4*>(p.REQ);
   const uint4* FPQ = reinterpret_cast<const uint4*>(p.FPQ);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < p.n_nodes; n += warps) {
     int64_t base = offsets[n];
-    const uint8_t kind = __ldg(p.kind + n) ? 2 : 1;
     const size_t row = (size_t)n * nq;
     for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
@@ -338,8 +348,15 @@ compact_kernel(CsrDev p, const int64_t* offsets, dfx_req_record* out, int64_t ca
           if (pass == 0) m = ldg4(REQ + row + q);
           else if (p.fp_slot[q] >= 0) m = ldg4(FPQ + (size_t)n * p.n_fp_slots + p.fp_slot[q]);
         }
-        uint32_t w4[4] = {m.x, m.y, m.z, m.w};
-        int c = (w4[0] != 0) + (w4[1] != 0) + (w4[2] != 0) + (w4[3] != 0);
+        const uint32_t w4[4] = {m.x, m.y, m.z, m.w};
+        const uint32_t nib = (w4[0] != 0) | ((w4[1] != 0) << 1) | ((w4[2] != 0) << 2) | ((w4[3] != 0) << 3);
+        // occupancy word (q / 8) gathers the nibbles of 8 consecutive lanes
+        uint32_t ov = nib << (4 * (q & 7));
+        ov |= __shfl_xor_sync(FULL, ov, 1);
+        ov |= __shfl_xor_sync(FULL, ov, 2);
+        ov |= __shfl_xor_sync(FULL, ov, 4);
+        if ((q & 7) == 0 && (q >> 3) < ow) occ[(size_t)n * 2 * ow + pass * ow + (q >> 3)] = ov;
+        const int c = __popc(nib);
         int incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -350,12 +367,7 @@ compact_kernel(CsrDev p, const int64_t* offsets, dfx_req_record* out, int64_t ca
 #pragma unroll
         for (int k = 0; k < 4; k++)
           if (w4[k]) {
-            if (pos < cap) {
-              dfx_req_record r;
-              r.node = n; r.word = (uint16_t)(4 * q + k); r.kind = pass ? 3 : kind; r.pad = 0;
-              r.mask = w4[k];
-              out[pos] = r;
-            }
+            if (pos < cap) masks[pos] = w4[k];
             pos++;
           }
         base += __shfl_sync(FULL, incl, 31);
@@ -462,8 +474,8 @@ int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_
 }
 
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
-                 size_t scratch_bytes, dfx_req_record* out, int64_t cap, int64_t* n_out,
-                 cudaStream_t st) {
+                 size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
+                 int64_t* n_out, cudaStream_t st) {
   const int vpl = vpl_for(p.words);
   int blocks = grid_for(p.n_nodes * 32, 256);
   switch (vpl) {
@@ -481,11 +493,11 @@ int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scrat
   if (cudaMemcpyAsync(n_out, offsets + p.n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, st) !=
       cudaSuccess)
     return DFX_E_CUDA;
-  if (out) {
+  if (masks) {
     switch (vpl) {
-      case 1: compact_kernel<1><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
-      case 2: compact_kernel<2><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
-      case 4: compact_kernel<4><<<blocks, 256, 0, st>>>(p, offsets, out, cap); break;
+      case 1: compact_kernel<1><<<blocks, 256, 0, st>>>(p, offsets, occ, masks, cap); break;
+      case 2: compact_kernel<2><<<blocks, 256, 0, st>>>(p, offsets, occ, masks, cap); break;
+      case 4: compact_kernel<4><<<blocks, 256, 0, st>>>(p, offsets, occ, masks, cap); break;
     }
   }
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;

@@ -4,8 +4,7 @@ import pytest
 
 import _mfp_ref
 import _oracle
-from paper_2406_13881_b200.csr import (C3Config, CsrProblem, REC_DTYPE, mfp_csr,
-                                       records_to_planes)
+from paper_2406_13881_b200.csr import C3Config, CsrProblem, mfp_csr
 
 pytestmark = pytest.mark.gpu
 
@@ -16,15 +15,16 @@ def _check(prob, g, chunk=0):
     eh, ed, _ = _oracle.c3_solve(g)
     assert np.array_equal(OH, eh), "H planes differ in %d words" % (OH != eh).sum()
     assert np.array_equal(OD, ed), "D planes differ in %d words" % (OD != ed).sum()
-    rec = prob.requirements()
+    rows = prob.requirements()
     REQ, FP = _oracle.c3_requirements(g, eh, ed)
-    rq, rf = records_to_planes(rec, prob.n_nodes, prob.words)
+    rq, rf = rows.to_planes()
     assert np.array_equal(rq, REQ) and np.array_equal(rf, FP)
-    # order-preserving compaction: node-major, requirement words before
-    # firstprivate words, words ascending within each
-    key = rec["node"].astype(np.int64) * 4096 + (rec["kind"] == 3) * 2048 + rec["word"]
-    assert np.all(np.diff(key) > 0)
-    assert len(rec) == int((REQ != 0).sum() + (FP != 0).sum())
+    # order-preserving compaction: row offsets are the prefix of per-node
+    # nonzero-word counts; masks follow node order, requirement words first
+    cnt = (REQ != 0).sum(axis=1) + (FP != 0).sum(axis=1)
+    assert np.array_equal(np.diff(rows.row_off), cnt) and rows.row_off[0] == 0
+    nz = np.concatenate([REQ, FP], axis=1)
+    assert np.array_equal(nz[nz != 0], rows.masks)
     return st
 
 
@@ -32,7 +32,7 @@ def _check(prob, g, chunk=0):
 def test_c3_generated_on_device_matches_oracle(words):
     n = 1 << 15 if words >= 256 else 1 << 16
     cfg = C3Config(n_nodes=n, n_vars=32 * words, seed=11, w0=0)
-    g = _oracle.c3_generate(cfg.seed, n, cfg.w0, words, 82)
+    g = _oracle.c3_generate(cfg.seed, n, cfg.w0, words, cfg.n_scalar)
     prob = CsrProblem.generate_c3(cfg)
     st = _check(prob, g)
     assert st.rounds_h >= 2 and st.rounds_d >= 2
@@ -40,7 +40,7 @@ def test_c3_generated_on_device_matches_oracle(words):
 
 def test_c3_shard_offset_matches_oracle():
     cfg = C3Config(n_nodes=1 << 14, n_vars=4096, seed=5, w0=128)   # rank-1 slab
-    g = _oracle.c3_generate(cfg.seed, cfg.n_nodes, cfg.w0, cfg.words, 82)
+    g = _oracle.c3_generate(cfg.seed, cfg.n_nodes, cfg.w0, cfg.words, cfg.n_scalar)
     _check(CsrProblem.generate_c3(cfg), g)
 
 
@@ -63,10 +63,10 @@ def test_random_graphs_entries_selfloops_duplicates(seed):
 
 def test_all_in_one_host_call():
     g = _oracle.c3_generate(9, 1 << 14, 0, 128, 82)
-    rec, stats = mfp_csr(g["row_ptr"], g["col"], g["kind"], g["USE"], g["B"], g["S"])
+    rows, stats = mfp_csr(g["row_ptr"], g["col"], g["kind"], g["USE"], g["B"], g["S"])
     eh, ed, _ = _oracle.c3_solve(g)
     REQ, FP = _oracle.c3_requirements(g, eh, ed)
-    rq, rf = records_to_planes(rec, 1 << 14, 128)
+    rq, rf = rows.to_planes()
     assert np.array_equal(rq, REQ) and np.array_equal(rf, FP)
     assert stats.solve_ms > 0
 

@@ -235,7 +235,7 @@ def run_ours(args, rank, world, local):
     rowb = cfg.words * 4
     nnz = prob.eng.lib.dfx_csr_nnz(prob.h)
     rounds = stats_last["rounds_h"] + stats_last["rounds_d"]
-    meta = rounds * (5 * args.n_nodes + 8 * nnz) + 4 * stats_last["evaluated"]
+    meta = rounds * (5 * args.n_nodes + 8 * nnz) + 12 * stats_last["evaluated"]
     bytes_per_solve = (stats_last["rows_read"] + stats_last["rows_written"]) * rowb + meta
     kernel_ms_per_solve = kernel_ms / args.steps
     achieved = bytes_per_solve / (kernel_ms_per_solve / 1e3) / 1e9

@@ -252,6 +252,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   p.REQ = csr_alloc<uint32_t>(c, plane);
   p.S = csr_alloc<uint32_t>(c, words);
   p.stamp = csr_alloc<int32_t>(c, n);
+  p.popc = csr_alloc<int32_t>(c, n);
   p.fp_slot = csr_alloc<int32_t>(c, words / 4);
   c->counts = csr_alloc<int32_t>(c, n);
   c->offsets = csr_alloc<int64_t>(c, n + 1);
@@ -270,7 +271,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   for (void* a : c->allocs)
     if (!a) return fail(DFX_E_CUDA, "cudaMalloc failed for a %lld-node x %d-word problem",
                         (long long)n, words);
-  if (c->allocs.size() != 17) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
+  if (c->allocs.size() != 18) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
   CK(cudaMemcpy(p.S, S_host, sizeof(uint32_t) * words, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(p.fp_slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice));
   CK(cudaEventCreate(&c->e0));
@@ -358,7 +359,7 @@ int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
 int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 256;
+  if (chunk_nodes <= 0) chunk_nodes = 32;
   cudaStream_t st = h->st();
   dfx::SolveStats s{};
   CK(cudaEventRecord(c->e0, st));

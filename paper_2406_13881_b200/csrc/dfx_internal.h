@@ -48,6 +48,7 @@ struct CsrDev {
   int32_t* fp_slot; // [words/4] quad -> slot or -1
   int32_t n_fp_slots;
   int32_t* stamp;
+  int32_t* popc;    // per-node population count of the current OUT row
 };
 
 struct SolveStats {

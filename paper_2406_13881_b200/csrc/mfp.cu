@@ -25,6 +25,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <cstdlib>
+#include <cstdio>
 
 #include "../../include/dfx.h"
 #include "c3gen.cuh"
@@ -33,6 +35,7 @@
 namespace dfx {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int KP = 4;   // predecessor ids preloaded per node (Poisson(1.5)+1: 93% of nodes)
 
 __device__ __forceinline__ uint4 and4(uint4 a, uint4 b) { return make_uint4(a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w); }
 __device__ __forceinline__ uint4 or4(uint4 a, uint4 b) { return make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w); }
@@ -102,8 +105,8 @@ struct RoundCounters {
   unsigned long long rows_written;
 };
 
-template <int PHASE, int VPL>
-__global__ void __launch_bounds__(256)
+template <int PHASE, int VPL, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
                  RoundCounters* cnt) {
   const int lane = threadIdx.x & 31;
@@ -138,19 +141,33 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
     int prev_n = -2;
     bool carry = false;   // last node of the previous batch changed this round
     for (int nb = n0; nb < n1; nb += 32) {
-      // per-node metadata for 32 nodes at once (lane = node)
+      // per-node metadata for 32 nodes at once (lane = node): CSR bounds,
+      // kind, previous popcount and the first KP predecessor ids, all issued
+      // as independent loads so a node's row gathers later need no
+      // dependent index load
       const int n = nb + lane;
       const bool valid = n < n1;
-      int rs = 0, re = 0, kd = 0;
+      int rs = 0, re = 0, kd = 0, opc = 0;
+      int pr[KP];
       bool dirty = false;
+#pragma unroll
+      for (int k = 0; k < KP; k++) pr[k] = 0;
       if (valid) {
         rs = __ldg(p.row_ptr + n);
         re = __ldg(p.row_ptr + n + 1);
         kd = __ldg(p.kind + n);
+        opc = first ? 32 * p.words : __ldcg(p.popc + n);
+#pragma unroll
+        for (int k = 0; k < KP; k++)
+          if (k < re - rs) pr[k] = __ldg(p.col + rs + k);
         dirty = first != 0;
-        if (!first)
-          for (int e = rs; e < re && !dirty; e++)
+        if (!first) {
+#pragma unroll
+          for (int k = 0; k < KP; k++)
+            if (k < re - rs) dirty |= __ldcg(p.stamp + pr[k]) >= round - 1;
+          for (int e = rs + KP; e < re && !dirty; e++)
             dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= round - 1;
+        }
       }
       unsigned dm = __ballot_sync(FULL, dirty);
       // fall-through successor of a node changed earlier in this sweep
@@ -163,57 +180,79 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
         const int nn = nb + j;
         const int nrs = __shfl_sync(FULL, rs, j), nre = __shfl_sync(FULL, re, j);
         const bool kern = __shfl_sync(FULL, kd, j) != 0;
+        const int old_pc = __shfl_sync(FULL, opc, j);
+        int q[KP];
+#pragma unroll
+        for (int k = 0; k < KP; k++) q[k] = __shfl_sync(FULL, pr[k], j);
+        const int deg = nre - nrs;
         const size_t row = (size_t)nn * nq;
         // transfer-plane rows
-        uint4 pa[VPL], pb[VPL], old[VPL];
+        uint4 pa[VPL], pb[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; v++) {
-          const int q = lane + 32 * v;
+          const int qq = lane + 32 * v;
           pa[v] = pb[v] = zero4();
           if (!active[v]) continue;
           if (PHASE == 0) {
-            if (kern) pb[v] = ldg4(B + row + q); else pa[v] = ldg4(A + row + q);
+            if (kern) pb[v] = ldg4(B + row + qq); else pa[v] = ldg4(A + row + qq);
           } else {
             if (kern) {
-              pa[v] = ldg4(A + row + q);
-              if (nz4(smask[v])) pb[v] = ldg4(B + row + q);
+              pa[v] = ldg4(A + row + qq);
+              if (nz4(smask[v])) pb[v] = ldg4(B + row + qq);
             } else {
-              pb[v] = ldg4(B + row + q);
+              pb[v] = ldg4(B + row + qq);
             }
           }
-          old[v] = first ? all4() : ldcg4(OUT + row + q);
         }
-        n_read += 1 + (first ? 0 : 1);
-        // meet over predecessors
+        n_read += 1;
+        // meet over predecessors (change detection uses the popcount: every
+        // value only decreases -- monotone descent from top -- so a row
+        // changed iff its population count dropped; no old-row re-read)
         uint4 in[VPL], hin[VPL];
         const bool need_hin = PHASE == 1 && kern && any_s;
 #pragma unroll
-        for (int v = 0; v < VPL; v++) { in[v] = nre == nrs ? boundary : all4(); hin[v] = all4(); }
-        for (int e = nrs; e < nre; e += 32) {
-          const int ce = min(32, nre - e);
-          const int pid = lane < ce ? __ldg(p.col + e + lane) : 0;
-          for (int t = 0; t < ce; t++) {
-            const int q = __shfl_sync(FULL, pid, t);
-            const bool chain = q == nn - 1 && prev_n == nn - 1;
-            if (chain) {
+        for (int v = 0; v < VPL; v++) { in[v] = deg == 0 ? boundary : all4(); hin[v] = all4(); }
+        const bool have_prev = prev_n == nn - 1;
 #pragma unroll
-              for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
-            } else if (!first) {
+        for (int k = 0; k < KP; k++) {
+          if (k >= deg) break;
+          const int qk = q[k];
+          if (qk == nn - 1 && have_prev) {
 #pragma unroll
-              for (int v = 0; v < VPL; v++)
-                if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)q * nq + lane + 32 * v));
-              n_read++;
-            }
-            if (need_hin) {
+            for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
+          } else if (!first) {
 #pragma unroll
-              for (int v = 0; v < VPL; v++)
-                if (active[v] && nz4(smask[v]))
-                  hin[v] = and4(hin[v], ldg4(OH + (size_t)q * nq + lane + 32 * v));
-            }
+            for (int v = 0; v < VPL; v++)
+              if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)qk * nq + lane + 32 * v));
+            n_read++;
+          }
+          if (need_hin) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++)
+              if (active[v] && nz4(smask[v]))
+                hin[v] = and4(hin[v], ldg4(OH + (size_t)qk * nq + lane + 32 * v));
+          }
+        }
+        for (int e = nrs + KP; e < nre; e++) {     // rare: more than KP preds
+          const int qk = __ldg(p.col + e);
+          if (qk == nn - 1 && have_prev) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
+          } else if (!first) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++)
+              if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)qk * nq + lane + 32 * v));
+            n_read++;
+          }
+          if (need_hin) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++)
+              if (active[v] && nz4(smask[v]))
+                hin[v] = and4(hin[v], ldg4(OH + (size_t)qk * nq + lane + 32 * v));
           }
         }
         // transfer
-        bool ch = false;
+        int pc = 0;
         uint4 out[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; v++) {
@@ -225,9 +264,11 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
           } else {
             out[v] = andn4(in[v], pb[v]);
           }
-          ch |= active[v] && ne4(out[v], old[v]);
+          if (active[v]) pc += __popc(out[v].x) + __popc(out[v].y) + __popc(out[v].z) + __popc(out[v].w);
         }
-        ch = __any_sync(FULL, ch);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+        const bool ch = pc != old_pc;
         n_eval++;
         if (ch || first) {
 #pragma unroll
@@ -235,7 +276,10 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
             if (active[v]) __stcg(OUT + row + lane + 32 * v, out[v]);
           n_written++;
         }
-        if (lane == 0) p.stamp[nn] = ch ? round : (first ? 0 : p.stamp[nn]);
+        if (lane == 0) {
+          if (ch || first) p.popc[nn] = pc;
+          p.stamp[nn] = ch ? round : (first ? 0 : p.stamp[nn]);
+        }
         n_changed += ch;
 #pragma unroll
         for (int v = 0; v < VPL; v++) prev[v] = out[v];
@@ -412,13 +456,24 @@ int or_planes(const CsrDev& p, cudaStream_t st) {
 
 template <int PHASE>
 static int launch_round(const CsrDev& p, int vpl, int round, int first, int chunk_nodes,
-                        int n_chunks, RoundCounters* cnt, cudaStream_t st, int blocks) {
-  switch (vpl) {
-    case 1: mfp_round_kernel<PHASE, 1><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
-    case 2: mfp_round_kernel<PHASE, 2><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
-    case 4: mfp_round_kernel<PHASE, 4><<<blocks, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, cnt); break;
-    default: return DFX_E_LIMIT;
-  }
+                        int n_chunks, RoundCounters* cnt, cudaStream_t st, int minb) {
+  // grid = resident blocks: a persistent-style launch pulling chunks
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define DFX_LAUNCH(V, M)                                                                     \
+  do {                                                                                       \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfp_round_kernel<PHASE, V, M>, 256, 0); \
+    mfp_round_kernel<PHASE, V, M><<<sms * (per_sm > 0 ? per_sm : 1), 256, 0, st>>>(          \
+        p, round, first, chunk_nodes, n_chunks, cnt);                                        \
+  } while (0)
+  if (vpl == 1 && minb >= 6) DFX_LAUNCH(1, 6);
+  else if (vpl == 1 && minb == 4) DFX_LAUNCH(1, 4);
+  else if (vpl == 1) DFX_LAUNCH(1, 1);
+  else if (vpl == 2) DFX_LAUNCH(2, 1);
+  else if (vpl == 4) DFX_LAUNCH(4, 1);
+  else return DFX_E_LIMIT;
+#undef DFX_LAUNCH
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
@@ -436,13 +491,12 @@ int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_
   const int vpl = vpl_for(p.words);
   if (vpl < 0) return DFX_E_LIMIT;
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfp_round_kernel<0, 1>, 256, 0);
-  if (per_sm < 1) per_sm = 1;
-  int blocks = sms * per_sm;
+  static int minb = -1;
+  if (minb < 0) {
+    const char* e = getenv("DFX_MINB");
+    minb = e ? atoi(e) : 4;
+  }
+  const int blocks = minb;
   stats->rounds[0] = stats->rounds[1] = 0;
   stats->evaluated = stats->rows_read = stats->rows_written = 0;
   RoundCounters h{};
@@ -462,6 +516,12 @@ int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_
       float kms = 0.f;
       cudaEventElapsedTime(&kms, ev[0], ev[1]);
       stats->kernel_ms += kms;
+      static int trace = -1;
+      if (trace < 0) trace = getenv("DFX_TRACE") ? 1 : 0;
+      if (trace)
+        fprintf(stderr, "dfx-trace phase %d round %d evaluated %llu changed %llu rows_read %llu "
+                "rows_written %llu kernel_ms %.4f\n", phase, r, h.evaluated, h.changed,
+                h.rows_read, h.rows_written, kms);
       stats->rounds[phase] = r;
       stats->evaluated += (int64_t)h.evaluated;
       stats->rows_read += (int64_t)h.rows_read;

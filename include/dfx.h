@@ -222,6 +222,49 @@ int64_t dfx_csr_nnz(dfx_csr *p);
 /* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of `out` */
 int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_out *out, dfx_csr_stats *stats);
 
+/* ------------------------------------------------------------------------ */
+/* Kernel (c): interprocedural summaries (interproc.py:90-156)              */
+/* ------------------------------------------------------------------------ */
+/* One byte per (function, slot): bit0 R, bit1 W, bit2 HOST, bit3 DEVICE.
+ * Slots: [0, n_params) pointer parameters, [n_params, n_slots) globals.
+ * The engine replays the reference's Gauss-Seidel passes exactly (dict
+ * order, interproc.py:105-143): each pass rebuilds every function from its
+ * sources in order -- a static slot list (its own accesses, calls to
+ * external or undefined functions) or a call to a defined function (callee
+ * parameter i bound to a caller slot, callee globals copied, spaces forced
+ * to DEVICE for calls inside kernels) -- and tracks each summary's insertion
+ * order (the order of the reference's dicts).  Sources: int32 x4 rows
+ * (kind | dev << 8, a, b, c): STATIC: a = offset into slist, b = length;
+ * CALL: a = callee, b = offset into bind, c = number of bindings.
+ * Functions of one wave read no same-pass result of another, so a wave runs
+ * in parallel; waves run in order; passes repeat until no set changes. */
+typedef struct {
+  int32_t n_funcs, n_slots, n_params, n_waves, max_passes;
+  const uint8_t *init_bits;    /* [n_funcs * n_slots] pass-0 summaries */
+  const int16_t *init_list;    /* [n_funcs * n_slots] pass-0 insertion order */
+  const int32_t *init_len;     /* [n_funcs] */
+  const uint8_t *direct;       /* [n_funcs * n_slots] static-source bits */
+  const int32_t *src_off;      /* [n_funcs+1] */
+  const int32_t *src;          /* [n_src*4] */
+  const int16_t *slist;        /* [n_slist] */
+  const int32_t *bind;         /* [n_bind*2] (callee param, caller slot) */
+  const int32_t *wave_off;     /* [n_waves+1] */
+  const int32_t *wave_fns;     /* [n_funcs] */
+  int64_t n_src, n_slist, n_bind;
+} dfx_cg_in;
+
+typedef struct {
+  uint8_t *bits;               /* [n_funcs * n_slots] final summaries (host) */
+  int16_t *list;               /* [n_funcs * n_slots] insertion order (host) */
+  int32_t *len;                /* [n_funcs] */
+  int32_t passes;              /* passes run, as the reference counts them */
+  int32_t launches;            /* wave kernel launches */
+  float kernel_ms;
+} dfx_cg_out;
+
+/* replaces dartomp.interproc.summarize_all: host buffers in and out */
+int dfx_summaries(dfx_handle *h, const dfx_cg_in *in, dfx_cg_out *out);
+
 #ifdef __cplusplus
 }
 #endif

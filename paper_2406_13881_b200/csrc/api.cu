@@ -481,4 +481,117 @@ int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_out* out, dfx_csr_s
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// kernel (c): interprocedural summaries
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct dfx_cg {
+  dfx::CgDev g{};
+  std::vector<int32_t> wave_off;
+  std::vector<void*> allocs;
+  int* d_changed = nullptr;
+};
+
+namespace {
+int cg_destroy_impl(dfx_cg* c) {
+  if (!c) return DFX_OK;
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+  return DFX_OK;
+}
+void* cg_alloc(dfx_cg* c, size_t bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes + 16) != cudaSuccess) return nullptr;
+  c->allocs.push_back(p);
+  return p;
+}
+// pad [rows][ns] (elem bytes each) to [rows][nsp]
+template <class T>
+std::vector<T> pad_rows(const T* src, int rows, int ns, int nsp) {
+  std::vector<T> out((size_t)rows * nsp, T(0));
+  for (int r = 0; r < rows; r++) std::memcpy(&out[(size_t)r * nsp], src + (size_t)r * ns, sizeof(T) * ns);
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+// replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
+int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const int nf = in->n_funcs, ns = in->n_slots;
+  const int nsp = ((ns + 31) / 32) * 32;
+  auto* c = new dfx_cg();
+  dfx::CgDev& g = c->g;
+  g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = in->n_waves;
+  auto up = [&](const void* src, size_t bytes) -> void* {
+    void* p = cg_alloc(c, bytes);
+    if (p && bytes && src) cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st);
+    return p;
+  };
+  auto direct = pad_rows(in->direct, nf, ns, nsp);
+  auto ibits = pad_rows(in->init_bits, nf, ns, nsp);
+  auto ilist = pad_rows(in->init_list, nf, ns, nsp);
+  g.direct = (const uint8_t*)up(direct.data(), direct.size());
+  g.src_off = (const int32_t*)up(in->src_off, sizeof(int32_t) * (nf + 1));
+  g.src = (const int32_t*)up(in->src, sizeof(int32_t) * 4 * in->n_src);
+  g.slist = (const int16_t*)up(in->slist, sizeof(int16_t) * in->n_slist);
+  g.bind = (const int32_t*)up(in->bind, sizeof(int32_t) * 2 * in->n_bind);
+  g.wave_fns = (const int32_t*)up(in->wave_fns, sizeof(int32_t) * nf);
+  c->wave_off.assign(in->wave_off, in->wave_off + in->n_waves + 1);
+  g.h_wave_off = c->wave_off.data();
+  uint8_t* bits[2];
+  int16_t* list[2];
+  int32_t* len[2];
+  for (int k = 0; k < 2; k++) {
+    bits[k] = (uint8_t*)up(k == 0 ? ibits.data() : nullptr, ibits.size());
+    list[k] = (int16_t*)up(k == 0 ? ilist.data() : nullptr, sizeof(int16_t) * ilist.size());
+    len[k] = (int32_t*)up(k == 0 ? in->init_len : nullptr, sizeof(int32_t) * nf);
+  }
+  c->d_changed = (int*)cg_alloc(c, sizeof(int));
+  for (void* p : c->allocs)
+    if (!p) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
+  if (c->allocs.size() != 13) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
+  int prev = 0, passes = 0, launches = 0, rc = DFX_OK;
+  CK(cudaEventRecord(h->ev0, st));
+  while (passes < in->max_passes) {
+    passes++;
+    const int cur = prev ^ 1;
+    CK(cudaMemsetAsync(c->d_changed, 0, sizeof(int), st));
+    for (int w = 0; w < g.n_waves && rc == DFX_OK; w++) {
+      rc = dfx::cg_wave(g, bits[prev], list[prev], len[prev], bits[cur], list[cur], len[cur],
+                        w, 0, 1, c->d_changed, st);
+      launches++;
+    }
+    if (rc) break;
+    int changed = 0;
+    CK(cudaMemcpyAsync(&changed, c->d_changed, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    prev = cur;
+    if (!changed) break;
+  }
+  CK(cudaEventRecord(h->ev1, st));
+  if (rc) { cg_destroy_impl(c); return fail(rc, "cg_wave failed: %s", cudaGetErrorString(cudaGetLastError())); }
+  std::vector<uint8_t> hb((size_t)nf * nsp);
+  std::vector<int16_t> hl((size_t)nf * nsp);
+  CK(cudaMemcpyAsync(hb.data(), bits[prev], hb.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hl.data(), list[prev], sizeof(int16_t) * hl.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out->len, len[prev], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int f = 0; f < nf; f++) {
+    std::memcpy(out->bits + (size_t)f * ns, &hb[(size_t)f * nsp], ns);
+    std::memcpy(out->list + (size_t)f * ns, &hl[(size_t)f * nsp], sizeof(int16_t) * ns);
+  }
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  out->kernel_ms = ms;
+  out->passes = passes;
+  out->launches = launches;
+  cg_destroy_impl(c);
+  return DFX_OK;
+}
+
 }  // extern "C"

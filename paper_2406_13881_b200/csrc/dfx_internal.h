@@ -71,3 +71,22 @@ size_t scan_scratch_bytes(int64_t n);
 size_t round_counters_bytes();
 
 }  // namespace dfx
+
+namespace dfx {
+
+struct CgDev {
+  int32_t n_funcs, n_slots, nsp, n_params, n_waves;
+  const uint8_t* direct;     // [n_funcs * nsp]
+  const int32_t* src_off;
+  const int32_t* src;        // int32 x4 rows
+  const int16_t* slist;
+  const int32_t* bind;
+  const int32_t* wave_fns;
+  const int32_t* h_wave_off; // host copy
+};
+
+int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8_t* cbits,
+            int16_t* clist, int32_t* clen, int wave, int shard, int nshards, int* d_changed,
+            cudaStream_t st);
+
+}  // namespace dfx

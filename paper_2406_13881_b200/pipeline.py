@@ -1,0 +1,92 @@
+"""Drop-in driver: the reference's `load` / `plan_transform` / `transform`
+(`dartomp/pipeline.py:38-105`) with the hot path swapped for the engine.
+
+The front end (lexer, parser, AST-CFG, access classification) and the
+emitter (`rewriter.apply_plans`, `report.plan_lines`) are the host package's
+own; `summarize_all` runs on kernel (c) and every function's data-flow
+analysis runs in ONE batched launch of the E1 replay kernel.
+
+`install()` patches a live `dartomp` in place (its `pipeline` and `cli`
+modules pick the engine up), which is how an existing user -- including
+`python -m dartomp ...` -- switches over.
+"""
+from __future__ import annotations
+
+from ._host import import_dartomp
+
+import_dartomp()
+from dartomp.access import VariableTable, classify_accesses  # noqa: E402
+from dartomp.astcfg import build_astcfg  # noqa: E402
+from dartomp.lexer import expand_defines  # noqa: E402
+from dartomp.nodes import defined_functions  # noqa: E402
+from dartomp.parser import parse  # noqa: E402
+from dartomp.pipeline import Analysis, check_transform_preconditions  # noqa: E402
+from dartomp.rewriter import apply_plans  # noqa: E402
+from dartomp.source import SourceFile  # noqa: E402
+
+from .dataflow import analyze_function, analyze_functions  # noqa: E402
+from .interproc import apply_call_effects, summarize_all  # noqa: E402
+
+
+def load(path: str | None = None, text: str | None = None,
+         sizes: dict[str, int] | None = None, pointer_default: int = 1024,
+         summary_runner=None) -> Analysis:
+    """`dartomp.pipeline.load` (`pipeline.py:38-62`) with kernel (c)."""
+    if text is not None:
+        src = SourceFile.from_text(text, path=path or "<string>")
+    else:
+        src = SourceFile.from_path(path)
+    pre = expand_defines(src)
+    tu, pwarnings = parse(src, pre)
+    table = VariableTable(src, tu, sizes=sizes, pointer_default=pointer_default)
+    warnings = list(pre.warnings) + list(pwarnings)
+    cfgs, raw = {}, {}
+    for name, fn in defined_functions(tu).items():
+        cfg = build_astcfg(src, fn)
+        cfgs[name] = cfg
+        warnings.extend(cfg.warnings)
+        raw[name] = classify_accesses(src, cfg, table)
+    summaries = summarize_all(src, tu, cfgs, raw, table, runner=summary_runner)
+    expanded = {name: apply_call_effects(src, cfgs[name], raw[name], summaries, table)
+                for name in cfgs}
+    return Analysis(src=src, tu=tu, table=table, cfgs=cfgs, raw_accesses=raw,
+                    accesses=expanded, summaries=summaries,
+                    defines=dict(pre.defines), warnings=warnings)
+
+
+def plan_transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset(),
+                   replay_runner=None) -> list:
+    """`dartomp.pipeline.plan_transform` (`pipeline.py:85-96`), one launch."""
+    check_transform_preconditions(analysis)
+    names = list(analysis.cfgs)
+    items = [(analysis.src, analysis.cfgs[n], analysis.accesses[n], analysis.table)
+             for n in names]
+    plans = []
+    for res in analyze_functions(items, allow_stale, runner=replay_runner):
+        plan = res.get()            # raises the reference's error for that function
+        if plan.region is not None or plan.all_plans:
+            plans.append(plan)
+    return plans
+
+
+def transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset(),
+              indent_unit: str | None = None, replay_runner=None):
+    """`dartomp.pipeline.transform` (`pipeline.py:99-105`)."""
+    plans = plan_transform(analysis, allow_stale, replay_runner=replay_runner)
+    result = apply_plans(analysis.src, plans, indent_unit=indent_unit)
+    return result, plans
+
+
+def install() -> None:
+    """Route an imported `dartomp` through the engine (plugin drop-in)."""
+    import dartomp.cli as cli
+    import dartomp.dataflow as df
+    import dartomp.interproc as ip
+    import dartomp.pipeline as pl
+    df.analyze_function = analyze_function
+    ip.summarize_all = summarize_all
+    pl.analyze_function = analyze_function
+    pl.summarize_all = summarize_all
+    pl.plan_transform = plan_transform
+    pl.transform = transform
+    cli.transform = transform

@@ -96,3 +96,7 @@ def c3_requirements(g, OH, OD):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def summaries_runner(cin, cout) -> int:
+    return lib().oracle_summaries(C.byref(cin), C.byref(cout))

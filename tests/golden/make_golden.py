@@ -45,8 +45,13 @@ import _oracle  # noqa: E402
 from paper_2406_13881_b200 import _abi  # noqa: E402
 from paper_2406_13881_b200.dataflow import decode, pack, run_replay  # noqa: E402
 from paper_2406_13881_b200.lower import lower_function  # noqa: E402
+from paper_2406_13881_b200 import interproc as ip  # noqa: E402
+from paper_2406_13881_b200.gen.callgraph import CallGraphConfig  # noqa: E402
+from paper_2406_13881_b200.gen.callgraph import generate as gen_callgraph  # noqa: E402
+from dartomp.interproc import summarize_all as ref_summarize  # noqa: E402
 
 N_RANDOM = 120
+N_CALLGRAPH = 6          # generated call-graph programs (configuration C5 shape)
 
 
 def cases():
@@ -122,5 +127,55 @@ def main() -> None:
           % (len(plans_json), len(progs), evs.shape[0], batch.ops.shape[0]))
 
 
+def summary_cases():
+    corpus = pathlib.Path("/root/reference/pkg/tests/corpus")
+    for p in sorted(corpus.glob("*/*.c")):
+        yield "corpus/%s/%s" % (p.parent.name, p.name), p.read_text()
+    for s in range(40):
+        yield "random/%d" % s, _cases.random_program(s)
+    for s in range(N_CALLGRAPH):
+        n = 1200 if s == 0 else 240
+        yield "callgraph/%d" % s, gen_callgraph(s, CallGraphConfig(n_funcs=n, depth=12))
+
+
+def summaries_main() -> None:
+    """Fixtures for kernel (c): lowered call graphs + the reference's
+    summaries (sets and dict insertion orders), checked through the oracle."""
+    arrays = {}
+    expected = {}
+    n = 0
+    for name, text in summary_cases():
+        a = load(path=name, text=text)
+        ref = ref_summarize(a.src, a.tu, a.cfgs, a.raw_accesses, a.table)
+        g = ip.lower_call_graph(a.src, a.tu, a.cfgs, a.raw_accesses, a.table)
+        r = ip.solve_call_graph(g, runner=_oracle.summaries_runner)
+        mine = ip.summaries_from_result(g, r)
+        assert list(mine) == list(ref), name
+        for k in ref:
+            assert mine[k].snapshot() == ref[k].snapshot(), (name, k)
+            assert list(mine[k].param_effects.items()) == list(ref[k].param_effects.items()), (name, k)
+            assert list(mine[k].global_effects.items()) == list(ref[k].global_effects.items()), (name, k)
+        key = "c%d" % n
+        for fld in ("init_bits", "init_list", "init_len", "direct", "src_off", "src", "slist",
+                    "bind", "wave_off", "wave_fns"):
+            arrays["%s_%s" % (key, fld)] = getattr(g, fld)
+        arrays["%s_meta" % key] = np.array([g.n_funcs, g.n_params, r.passes], dtype=np.int64)
+        arrays["%s_exp_bits" % key] = r.bits
+        arrays["%s_exp_list" % key] = r.list
+        arrays["%s_exp_len" % key] = r.len
+        expected[key] = {"case": name, "functions": g.n_funcs, "slots": int(g.init_bits.shape[1]),
+                         "passes": int(r.passes),
+                         "snapshots": {k: repr(v.snapshot()) for k, v in list(ref.items())[:3]}}
+        n += 1
+    np.savez_compressed(HERE / "summary_cases.npz", **arrays)
+    with open(HERE / "summary_cases.json", "w") as fh:
+        json.dump(expected, fh, indent=0, sort_keys=True)
+    print("summary cases %d -> fixtures written" % n)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "summaries":
+        summaries_main()
+    else:
+        main()
+        summaries_main()

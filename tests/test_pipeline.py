@@ -1,0 +1,89 @@
+"""Drop-in pipeline (load + transform through the engine) vs the reference
+pipeline: byte-identical rewritten source, identical report lines and errors."""
+import pathlib
+
+import pytest
+
+import _cases
+import _e2e
+import _oracle
+from paper_2406_13881_b200._host import have_dartomp
+
+pytestmark = pytest.mark.skipif(not have_dartomp(), reason="host front end not importable")
+PROBES = sorted((pathlib.Path(__file__).parent / "golden" / "probes").glob("*.c"))
+CPU = {"replay_runner": _oracle.replay_runner, "summary_runner": _oracle.summaries_runner}
+
+
+@pytest.mark.parametrize("path", PROBES, ids=[p.name for p in PROBES])
+def test_probes_cpu_oracle(path):
+    _e2e.compare(path.read_text(), path.name, **CPU)
+
+
+@pytest.mark.parametrize("seed", range(500, 520))
+def test_random_cpu_oracle(seed):
+    _e2e.compare(_cases.random_program(seed), "r%d.c" % seed, **CPU)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", PROBES, ids=[p.name for p in PROBES])
+def test_probes_cuda(path):
+    _e2e.compare(path.read_text(), path.name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(600, 640))
+def test_random_cuda(seed):
+    _e2e.compare(_cases.random_program(seed), "r%d.c" % seed)
+
+
+@pytest.mark.gpu
+def test_callgraph_program_cuda():
+    from paper_2406_13881_b200.gen.callgraph import CallGraphConfig, generate
+    _e2e.compare(generate(7, CallGraphConfig(n_funcs=120, depth=12)), "cg.c")
+
+
+@pytest.mark.gpu
+def test_install_patches_reference_cli(tmp_path, capsys):
+    import dartomp.cli as cli
+    from paper_2406_13881_b200.pipeline import install
+    p = tmp_path / "t.c"
+    p.write_text(PROBES[0].read_text())
+    rc_ref = cli.run(["report", str(p)])
+    ref_out = capsys.readouterr().out
+    install()
+    rc = cli.run(["report", str(p)])
+    assert rc == rc_ref and capsys.readouterr().out == ref_out
+
+
+CORPUS = pathlib.Path("/root/reference/pkg/tests/corpus")
+
+
+@pytest.mark.skipif(not CORPUS.exists(), reason="reference corpus not present (GPU box)")
+def test_corpus_matches_golden_report_and_text_cpu_oracle():
+    """Every corpus file through the drop-in pipeline reproduces the golden
+    `report` lines and the sha256 of the `transform` output."""
+    import hashlib
+    import _golden
+    from dartomp.report import plan_lines
+    from paper_2406_13881_b200.pipeline import load, transform
+    gold = _golden.reference_plans()
+    n = 0
+    for p in sorted(CORPUS.glob("*/*.c")):
+        key = "corpus/%s/%s" % (p.parent.name, p.name)
+        exp = gold[key]
+        a = load(path=key, text=p.read_text(), summary_runner=_oracle.summaries_runner)
+        try:
+            result, plans = transform(a, replay_runner=_oracle.replay_runner)
+        except Exception as e:
+            got = ["<%s: %s>" % (type(e).__name__, e.render())]
+            assert got == exp["report"], key
+            n += 1
+            continue
+        assert hashlib.sha256(result.text.encode()).hexdigest() == exp["transform_sha256"], key
+        try:
+            lines = plan_lines(a.src, plans)
+        except KeyError as e:
+            lines = ["<KeyError %s>" % e]
+        assert lines == exp["report"], key
+        n += 1
+    assert n == 27

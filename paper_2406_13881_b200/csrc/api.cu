@@ -210,6 +210,7 @@ struct dfx_csr {
   int64_t masks_cap = 0;
   uint32_t* d_occ = nullptr;
   void* d_cnt = nullptr;
+  uint8_t* flags = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -253,12 +254,16 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   p.S = csr_alloc<uint32_t>(c, words);
   p.stamp = csr_alloc<int32_t>(c, n);
   p.popc = csr_alloc<int32_t>(c, n);
+  p.desc = csr_alloc<int32_t>(c, (size_t)n * 8);
   p.fp_slot = csr_alloc<int32_t>(c, words / 4);
   c->counts = csr_alloc<int32_t>(c, n);
   c->offsets = csr_alloc<int64_t>(c, n + 1);
   c->scratch_bytes = dfx::scan_scratch_bytes(n);
   c->scratch = csr_alloc<uint8_t>(c, c->scratch_bytes);
-  c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_counters_bytes());
+  c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_ctl_bytes());
+  p.succ_ptr = csr_alloc<int32_t>(c, n + 1);
+  p.succ = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
+  c->flags = csr_alloc<uint8_t>(c, 2 * (size_t)n);   // >= 2 * n_chunks for chunk_nodes >= 1
   // scalar quads -> FP slots
   std::vector<int32_t> slot(words / 4, -1);
   int ns = 0;
@@ -267,11 +272,14 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
     if (s[0] | s[1] | s[2] | s[3]) slot[q] = ns++;
   }
   p.n_fp_slots = ns;
+  p.s_quads_low = 1;
+  for (int q = 8; q < words / 4; q++)
+    if (slot[q] >= 0) p.s_quads_low = 0;
   p.FPQ = csr_alloc<uint32_t>(c, (size_t)n * 4 * (ns > 0 ? ns : 1));
   for (void* a : c->allocs)
     if (!a) return fail(DFX_E_CUDA, "cudaMalloc failed for a %lld-node x %d-word problem",
                         (long long)n, words);
-  if (c->allocs.size() != 18) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
+  if (c->allocs.size() != 22) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
   CK(cudaMemcpy(p.S, S_host, sizeof(uint32_t) * words, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(p.fp_slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice));
   CK(cudaEventCreate(&c->e0));
@@ -303,7 +311,9 @@ int csr_upload(dfx_csr* c, const dfx_csr_in* in, cudaStream_t st) {
   CK(cudaMemcpyAsync(p.USE, in->R, plane, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
   int rc = dfx::or_planes(p, st);
-  if (rc) return fail(rc, "or_planes launch failed");
+  if (!rc) rc = dfx::build_desc(p, st);
+  if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
+  if (rc) return fail(rc, "or_planes/build_desc launch failed");
   return DFX_OK;
 }
 
@@ -345,6 +355,8 @@ int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
   rc = csr_alloc_all(c, spec->n_nodes, spec->words, nnz, S.data());
   if (rc) { csr_destroy_impl(c); return rc; }
   rc = dfx::c3_generate(c->p, spec->seed, spec->w0, h->st(), c->scratch, c->scratch_bytes);
+  if (!rc) rc = dfx::build_desc(c->p, h->st());
+  if (!rc) rc = dfx::build_succ(c->p, c->scratch, c->scratch_bytes, c->counts, h->st());
   if (rc) { csr_destroy_impl(c); return fail(rc, "c3 generation failed"); }
   CK(cudaStreamSynchronize(h->st()));
   *out = c;
@@ -359,11 +371,11 @@ int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
 int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 32;
+  if (chunk_nodes <= 0) chunk_nodes = 64;
   cudaStream_t st = h->st();
   dfx::SolveStats s{};
   CK(cudaEventRecord(c->e0, st));
-  int rc = dfx::mfp_solve(c->p, (dfx::RoundCounters*)c->d_cnt, st, chunk_nodes, 10000, &s);
+  int rc = dfx::mfp_solve(c->p, c->d_cnt, c->flags, st, chunk_nodes, &s);
   if (rc) return fail(rc, "mfp_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
   CK(cudaEventRecord(c->e1, st));
   CK(cudaEventSynchronize(c->e1));

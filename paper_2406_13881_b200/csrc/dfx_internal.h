@@ -49,6 +49,10 @@ struct CsrDev {
   int32_t n_fp_slots;
   int32_t* stamp;
   int32_t* popc;    // per-node population count of the current OUT row
+  int32_t s_quads_low;  // every nonzero scalar quad has index < 8
+  int32_t* desc;        // [n_nodes][8] node descriptors (rs, deg|kind<<30, p0..p3)
+  int32_t* succ_ptr;    // [n_nodes+1] successor (reverse) CSR
+  int32_t* succ;        // [nnz]
 };
 
 struct SolveStats {
@@ -57,18 +61,19 @@ struct SolveStats {
   float kernel_ms;
 };
 
-struct RoundCounters;
 
 int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch, size_t scratch_bytes);
 int or_planes(const CsrDev& p, cudaStream_t st);
+int build_desc(const CsrDev& p, cudaStream_t st);
 int vpl_for(int words);
-int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_nodes,
-              int max_rounds, SolveStats* stats);
+int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
+              SolveStats* stats);
+int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st);
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
                  size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
                  int64_t* n_out, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
-size_t round_counters_bytes();
+size_t round_ctl_bytes();
 
 }  // namespace dfx
 

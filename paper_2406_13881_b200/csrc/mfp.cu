@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <cuda_pipeline.h>
 #include <cstdlib>
 #include <cstdio>
 
@@ -105,10 +106,50 @@ struct RoundCounters {
   unsigned long long rows_written;
 };
 
+constexpr int kMaxRounds = 64;
+
+// device-side round control of one phase: rounds are launched back to back
+// without host round trips; the last block of a round that changed nothing
+// raises `done`, and every later launch of the phase returns at once
+struct RoundCtl {
+  RoundCounters cnt[kMaxRounds + 1];
+  unsigned int blocks_done[kMaxRounds + 1];
+  int done;
+};
+
+// per-warp counters -> round totals; the last block to finish decides
+// termination (a round r > 1 that changed no row ends the phase)
+__device__ __forceinline__ void round_epilogue(RoundCtl* ctl, int round, int lane,
+                                               unsigned long long n_changed,
+                                               unsigned long long n_eval,
+                                               unsigned long long n_read,
+                                               unsigned long long n_written) {
+  RoundCounters* cnt = &ctl->cnt[round];
+  if (lane == 0) {
+    if (n_changed) atomicAdd(&cnt->changed, n_changed);
+    if (n_eval) atomicAdd(&cnt->evaluated, n_eval);
+    if (n_read) atomicAdd(&cnt->rows_read, n_read);
+    if (n_written) atomicAdd(&cnt->rows_written, n_written);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->blocks_done[round], 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long ch = atomicAdd(&cnt->changed, 0ull);
+      if (round > 1 && ch == 0) atomicExch(&ctl->done, 1);
+    }
+  }
+}
+
+
 template <int PHASE, int VPL, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
-                 RoundCounters* cnt) {
+                 RoundCtl* ctl, uint8_t* flags_cur, uint8_t* flags_next) {
+  if (__ldcg(&ctl->done)) return;
+  RoundCounters* cnt = &ctl->cnt[round];
   const int lane = threadIdx.x & 31;
   const int nq = p.words >> 2;                 // uint4 per row
   const uint4* A = reinterpret_cast<const uint4*>(p.A);
@@ -291,12 +332,226 @@ mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
       }
     }
   }
-  if (lane == 0) {
-    atomicAdd(&cnt->changed, n_changed);
-    atomicAdd(&cnt->evaluated, n_eval);
-    atomicAdd(&cnt->rows_read, n_read);
-    atomicAdd(&cnt->rows_written, n_written);
+  round_epilogue(ctl, round, lane, n_changed, n_eval, n_read, n_written);
+}
+
+
+// ---------------------------------------------------------------------------
+// per-node descriptor (32 B, built once per problem): CSR start, degree,
+// kind and the first four predecessor ids -- one 2x16-B load replaces the
+// dependent row_ptr -> col chain in the round kernels
+// ---------------------------------------------------------------------------
+__global__ void build_desc_kernel(int64_t n_nodes, const int32_t* row_ptr, const int32_t* col,
+                                  const uint8_t* kind, int4* desc) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int rs = row_ptr[n], deg = row_ptr[n + 1] - rs;
+    int pr[4];
+    for (int k = 0; k < 4; k++) pr[k] = k < deg ? col[rs + k] : 0;
+    desc[2 * n] = make_int4(rs, deg | ((int)kind[n] << 30), pr[0], pr[1]);
+    desc[2 * n + 1] = make_int4(pr[2], pr[3], 0, 0);
   }
+}
+
+__global__ void succ_count_kernel(int64_t nnz, const int32_t* col, int32_t* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[e], 1);
+}
+__global__ void succ_fill_kernel(int64_t n_nodes, const int32_t* row_ptr, const int32_t* col,
+                                 int32_t* cursor, int32_t* succ) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x)
+    for (int e = row_ptr[n]; e < row_ptr[n + 1]; e++) succ[atomicAdd(cursor + col[e], 1)] = (int32_t)n;
+}
+
+// reverse (successor) CSR: succ_ptr [n+1], succ [nnz]; order inside a row
+// is irrelevant (it only feeds chunk dirty flags)
+int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st) {
+  int g = (int)((p.nnz + 255) / 256);
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  if (cudaMemsetAsync(p.succ_ptr, 0, sizeof(int32_t) * (p.n_nodes + 1), st) != cudaSuccess) return DFX_E_CUDA;
+  if (p.nnz) succ_count_kernel<<<g, 256, 0, st>>>(p.nnz, p.col, p.succ_ptr + 1);
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
+  if (cudaMemcpyAsync(tmp, p.succ_ptr, sizeof(int32_t) * p.n_nodes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return DFX_E_CUDA;
+  int gn = (int)((p.n_nodes + 255) / 256);
+  if (gn > 148 * 64) gn = 148 * 64;
+  succ_fill_kernel<<<gn, 256, 0, st>>>(p.n_nodes, p.row_ptr, p.col, tmp, p.succ);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int build_desc(const CsrDev& p, cudaStream_t st) {
+  int g = (int)((p.n_nodes + 255) / 256);
+  if (g > 148 * 64) g = 148 * 64;
+  build_desc_kernel<<<g, 256, 0, st>>>(p.n_nodes, p.row_ptr, p.col, p.kind,
+                                       reinterpret_cast<int4*>(p.desc));
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// kernel (a), V <= 4096 fast path: node descriptors prefetched one 32-node
+// batch ahead, so the only dependent metadata latency per batch is the
+// predecessor change stamps; otherwise identical to mfp_round_kernel
+// ---------------------------------------------------------------------------
+template <int PHASE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
+                    RoundCtl* ctl, uint8_t* flags_cur, uint8_t* flags_next) {
+  if (__ldcg(&ctl->done)) return;
+  RoundCounters* cnt = &ctl->cnt[round];
+  const int lane = threadIdx.x & 31;
+  const int nq = p.words >> 2;
+  const bool act = lane < nq;
+  const uint4* A = reinterpret_cast<const uint4*>(p.A);
+  const uint4* B = reinterpret_cast<const uint4*>(p.B);
+  const uint4* OH = reinterpret_cast<const uint4*>(p.OH);
+  uint4* OUT = reinterpret_cast<uint4*>(PHASE == 0 ? p.OH : p.OD);
+  const int4* desc = reinterpret_cast<const int4*>(p.desc);
+  const uint4 smask = act ? ldg4(reinterpret_cast<const uint4*>(p.S) + lane) : zero4();
+  const bool has_s = nz4(smask);
+  const bool any_s = __any_sync(FULL, has_s);
+  const uint4 boundary = PHASE == 0 ? all4() : zero4();
+  unsigned long long n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;
+
+  for (;;) {
+    int chunk = 0;
+    if (lane == 0) chunk = (int)atomicAdd(&cnt->chunk, 1ull);
+    chunk = __shfl_sync(FULL, chunk, 0);
+    if (chunk >= n_chunks) break;
+    const int n0 = chunk * chunk_nodes;
+    const int n1 = min(n0 + chunk_nodes, (int)p.n_nodes);
+    uint4 prev = zero4();
+    int prev_n = -2;
+    bool carry = false;
+    // descriptors of the first batch
+    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
+    int opc = 0;
+    if (n0 + lane < n1) {
+      d0 = __ldg(desc + 2 * (n0 + lane));
+      d1 = __ldg(desc + 2 * (n0 + lane) + 1);
+      if (!first) opc = __ldcg(p.popc + n0 + lane);
+    }
+    for (int nb = n0; nb < n1; nb += 32) {
+      const int n = nb + lane;
+      const bool valid = n < n1;
+      const int rs = d0.x, deg = d0.y & 0x3FFFFFFF, kd = (d0.y >> 30) & 1;
+      const int pr0 = d0.z, pr1 = d0.w, pr2 = d1.x, pr3 = d1.y;
+      const int cur_opc = first ? 32 * p.words : opc;
+      // issue the change-stamp loads of this batch and the next batch's descriptors
+      bool dirty = first != 0;
+      int st0 = -4, st1 = -4, st2 = -4, st3 = -4;
+      if (valid && !first) {
+        if (deg > 0) st0 = __ldcg(p.stamp + pr0);
+        if (deg > 1) st1 = __ldcg(p.stamp + pr1);
+        if (deg > 2) st2 = __ldcg(p.stamp + pr2);
+        if (deg > 3) st3 = __ldcg(p.stamp + pr3);
+      }
+      const int nn1 = nb + 32 + lane;
+      if (nn1 < n1) {
+        d0 = __ldg(desc + 2 * nn1);
+        d1 = __ldg(desc + 2 * nn1 + 1);
+        if (!first) opc = __ldcg(p.popc + nn1);
+      }
+      if (valid && !first) {
+        const int lim = round - 1;
+        dirty = st0 >= lim || st1 >= lim || st2 >= lim || st3 >= lim;
+        for (int e = rs + KP; e < rs + deg && !dirty; e++)
+          dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= lim;
+      }
+      unsigned dm = __ballot_sync(FULL, valid && dirty);
+      if (carry && nb < n1) dm |= 1u;
+      carry = false;
+      const unsigned vmask = __ballot_sync(FULL, valid);
+      while (dm) {
+        const int j = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int nn = nb + j;
+        const int nrs = __shfl_sync(FULL, rs, j);
+        const int ndeg = __shfl_sync(FULL, deg, j);
+        const bool kern = __shfl_sync(FULL, kd, j) != 0;
+        const int old_pc = __shfl_sync(FULL, cur_opc, j);
+        const int q0 = __shfl_sync(FULL, pr0, j), q1 = __shfl_sync(FULL, pr1, j);
+        const int q2 = __shfl_sync(FULL, pr2, j), q3 = __shfl_sync(FULL, pr3, j);
+        const size_t row = (size_t)nn * nq;
+        const bool need_hin = PHASE == 1 && kern && any_s;
+        const bool have_prev = prev_n == nn - 1;
+        const uint4* plane = (PHASE == 0) == kern ? B : A;
+        uint4 pl = zero4(), b0 = zero4(), hin = all4();
+        uint4 in = ndeg == 0 ? boundary : all4();
+        if (act) {
+          pl = ldg4(plane + row + lane);
+          if (need_hin && has_s) b0 = ldg4(B + row + lane);
+        }
+        // gathers: all issued before use
+        uint4 g[KP];
+        bool use[KP];
+        const int qs[KP] = {q0, q1, q2, q3};
+#pragma unroll
+        for (int k = 0; k < KP; k++) {
+          use[k] = false;
+          g[k] = all4();
+          if (k >= ndeg) continue;
+          if (qs[k] == nn - 1 && have_prev) { g[k] = prev; continue; }
+          if (first) continue;
+          use[k] = true;
+          if (act) g[k] = ldcg4(OUT + (size_t)qs[k] * nq + lane);
+        }
+        if (need_hin && has_s) {
+#pragma unroll
+          for (int k = 0; k < KP; k++)
+            if (k < ndeg) hin = and4(hin, ldg4(OH + (size_t)qs[k] * nq + lane));
+        }
+#pragma unroll
+        for (int k = 0; k < KP; k++) { in = and4(in, g[k]); n_read += use[k]; }
+        for (int e = nrs + KP; e < nrs + ndeg; e++) {      // rare: more than KP preds
+          const int qk = __ldg(p.col + e);
+          if (qk == nn - 1 && have_prev) in = and4(in, prev);
+          else if (!first) {
+            if (act) in = and4(in, ldcg4(OUT + (size_t)qk * nq + lane));
+            n_read++;
+          }
+          if (need_hin && has_s) hin = and4(hin, ldg4(OH + (size_t)qk * nq + lane));
+        }
+        uint4 out;
+        if (PHASE == 0) {
+          out = kern ? andn4(in, pl) : or4(in, pl);
+        } else if (kern) {
+          const uint4 x = and4(and4(andn4(pl, b0), smask), hin);   // F & H_in
+          out = or4(in, andn4(pl, x));
+        } else {
+          out = andn4(in, pl);
+        }
+        int pc = act ? __popc(out.x) + __popc(out.y) + __popc(out.z) + __popc(out.w) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+        const bool ch = pc != old_pc;
+        n_eval++;
+        n_read++;
+        if (ch || first) {
+          if (act) __stcg(OUT + row + lane, out);
+          n_written++;
+        }
+        if (lane == 0) {
+          if (ch || first) p.popc[nn] = pc;
+          if (ch) p.stamp[nn] = round;
+          else if (first) p.stamp[nn] = 0;
+        }
+        n_changed += ch;
+        prev = out;
+        prev_n = nn;
+        if (ch && !first) {
+          if (j < 31) dm |= (1u << (j + 1)) & vmask;
+          else carry = true;
+        }
+      }
+    }
+  }
+  round_epilogue(ctl, round, lane, n_changed, n_eval, n_read, n_written);
 }
 
 // ---------------------------------------------------------------------------
@@ -456,22 +711,26 @@ int or_planes(const CsrDev& p, cudaStream_t st) {
 
 template <int PHASE>
 static int launch_round(const CsrDev& p, int vpl, int round, int first, int chunk_nodes,
-                        int n_chunks, RoundCounters* cnt, cudaStream_t st, int minb) {
+                        int n_chunks, RoundCtl* ctl, uint8_t* fcur, uint8_t* fnext,
+                        cudaStream_t st) {
   // grid = resident blocks: a persistent-style launch pulling chunks
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#define DFX_LAUNCH(V, M)                                                                     \
-  do {                                                                                       \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfp_round_kernel<PHASE, V, M>, 256, 0); \
-    mfp_round_kernel<PHASE, V, M><<<sms * (per_sm > 0 ? per_sm : 1), 256, 0, st>>>(          \
-        p, round, first, chunk_nodes, n_chunks, cnt);                                        \
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 1;
+#define DFX_LAUNCH(K)                                                                          \
+  do {                                                                                         \
+    static int occ_ = 0;                                                                       \
+    if (!occ_) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, K, 256, 0);               \
+    per_sm = occ_ > 0 ? occ_ : 1;                                                              \
+    K<<<sms * per_sm, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, ctl, fcur, fnext); \
   } while (0)
-  if (vpl == 1 && minb >= 6) DFX_LAUNCH(1, 6);
-  else if (vpl == 1 && minb == 4) DFX_LAUNCH(1, 4);
-  else if (vpl == 1) DFX_LAUNCH(1, 1);
-  else if (vpl == 2) DFX_LAUNCH(2, 1);
-  else if (vpl == 4) DFX_LAUNCH(4, 1);
+  if (vpl == 1) DFX_LAUNCH((mfp_round_v1_kernel<PHASE, 4>));      // V <= 4096 fast path
+  else if (vpl == 2) DFX_LAUNCH((mfp_round_kernel<PHASE, 2, 1>));
+  else if (vpl == 4) DFX_LAUNCH((mfp_round_kernel<PHASE, 4, 1>));
   else return DFX_E_LIMIT;
 #undef DFX_LAUNCH
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
@@ -486,49 +745,63 @@ int vpl_for(int words) {
   return -1;
 }
 
-int mfp_solve(const CsrDev& p, RoundCounters* d_cnt, cudaStream_t st, int chunk_nodes,
-              int max_rounds, SolveStats* stats) {
+size_t round_ctl_bytes() { return sizeof(RoundCtl); }
+
+// Both phases to their fixpoints.  Rounds are queued in batches of
+// `kBatch` launches with no host synchronisation in between; a round
+// launched after the phase converged returns immediately.
+int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
+              SolveStats* stats) {
   const int vpl = vpl_for(p.words);
   if (vpl < 0) return DFX_E_LIMIT;
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
-  static int minb = -1;
-  if (minb < 0) {
-    const char* e = getenv("DFX_MINB");
-    minb = e ? atoi(e) : 4;
-  }
-  const int blocks = minb;
+  constexpr int kBatch = 8;
+  RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctl_mem);
+  static thread_local cudaEvent_t ev[2 * (kMaxRounds + 1)] = {};
+  if (!ev[0])
+    for (auto& e : ev) cudaEventCreate(&e);
+  static int trace = -1;
+  if (trace < 0) trace = getenv("DFX_TRACE") ? 1 : 0;
   stats->rounds[0] = stats->rounds[1] = 0;
   stats->evaluated = stats->rows_read = stats->rows_written = 0;
-  RoundCounters h{};
-  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
-  if (!ev[0]) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
   stats->kernel_ms = 0.f;
+  static thread_local RoundCtl h;
   for (int phase = 0; phase < 2; phase++) {
-    for (int r = 1; r <= max_rounds; r++) {
-      if (cudaMemsetAsync(d_cnt, 0, sizeof(RoundCounters), st) != cudaSuccess) return DFX_E_CUDA;
-      cudaEventRecord(ev[0], st);
-      int rc = phase == 0 ? launch_round<0>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks)
-                          : launch_round<1>(p, vpl, r, r == 1, chunk_nodes, n_chunks, d_cnt, st, blocks);
-      if (rc != DFX_OK) return rc;
-      cudaEventRecord(ev[1], st);
-      if (cudaMemcpyAsync(&h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
+    if (cudaMemsetAsync(ctl, 0, sizeof(RoundCtl), st) != cudaSuccess) return DFX_E_CUDA;
+    if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
+    int launched = 0;
+    for (;;) {
+      for (int k = 0; k < kBatch && launched < kMaxRounds; k++) {
+        const int r = ++launched;
+        uint8_t* fcur = flags + (size_t)(r & 1) * n_chunks;
+        uint8_t* fnext = flags + (size_t)((r + 1) & 1) * n_chunks;
+        cudaEventRecord(ev[2 * r], st);
+        int rc = phase == 0 ? launch_round<0>(p, vpl, r, r == 1, chunk_nodes, n_chunks, ctl, fcur, fnext, st)
+                            : launch_round<1>(p, vpl, r, r == 1, chunk_nodes, n_chunks, ctl, fcur, fnext, st);
+        if (rc != DFX_OK) return rc;
+        cudaEventRecord(ev[2 * r + 1], st);
+      }
+      if (cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
       if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
+      if (h.done) break;
+      if (launched >= kMaxRounds) return DFX_E_LIMIT;
+    }
+    int rounds = 0;
+    for (int r = 1; r <= launched; r++) {
+      const RoundCounters& c = h.cnt[r];
       float kms = 0.f;
-      cudaEventElapsedTime(&kms, ev[0], ev[1]);
+      cudaEventElapsedTime(&kms, ev[2 * r], ev[2 * r + 1]);
       stats->kernel_ms += kms;
-      static int trace = -1;
-      if (trace < 0) trace = getenv("DFX_TRACE") ? 1 : 0;
       if (trace)
         fprintf(stderr, "dfx-trace phase %d round %d evaluated %llu changed %llu rows_read %llu "
-                "rows_written %llu kernel_ms %.4f\n", phase, r, h.evaluated, h.changed,
-                h.rows_read, h.rows_written, kms);
-      stats->rounds[phase] = r;
-      stats->evaluated += (int64_t)h.evaluated;
-      stats->rows_read += (int64_t)h.rows_read;
-      stats->rows_written += (int64_t)h.rows_written;
-      if (r > 1 && h.changed == 0) break;
-      if (r == max_rounds) return DFX_E_LIMIT;
+                "rows_written %llu kernel_ms %.4f\n", phase, r, c.evaluated, c.changed,
+                c.rows_read, c.rows_written, kms);
+      stats->evaluated += (int64_t)c.evaluated;
+      stats->rows_read += (int64_t)c.rows_read;
+      stats->rows_written += (int64_t)c.rows_written;
+      if (!rounds && r > 1 && c.changed == 0 && h.blocks_done[r]) rounds = r;
     }
+    stats->rounds[phase] = rounds;
   }
   return DFX_OK;
 }
@@ -572,6 +845,4 @@ size_t scan_scratch_bytes(int64_t n) {
 
 }  // namespace dfx
 
-namespace dfx {
-size_t round_counters_bytes() { return sizeof(RoundCounters); }
-}  // namespace dfx
+

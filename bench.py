@@ -47,6 +47,10 @@ def parse_args():
     ap.add_argument("--chunk", type=int, default=0, help="nodes per warp task (0: default)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
+                    help="c3: 1M-node x 4096-var CSR fixpoint (default, the roofline "
+                         "config); c4: 100k-function E1 batch, LPT-sharded")
+    ap.add_argument("--c4-funcs", type=int, default=100_000)
     return ap.parse_args()
 
 
@@ -312,6 +316,106 @@ def run_ours(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def run_c4(args, rank, world, local):
+    """Configuration C4: 100k independent functions through the E1 replay
+    kernel, LPT-sharded over the ranks (strong scaling: total work fixed)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_13881_b200 import _abi
+    from paper_2406_13881_b200.batch import (C4Config, ReplayBatch, c4_cost, c4_generate,
+                                             c4_shapes, lpt_shards)
+    from paper_2406_13881_b200.dataflow import run_replay
+
+    torch.cuda.set_device(local)
+    eng = _abi.engine(local)
+    stream = torch.cuda.current_stream()
+    eng.lib.dfx_set_stream(eng.h, __import__("ctypes").c_void_p(stream.cuda_stream))
+    cfg = C4Config(n_funcs=args.c4_funcs, seed=args.seed)
+    N, V = c4_shapes(cfg)
+    shards = lpt_shards(c4_cost(N, V), world)
+    mine = shards[rank]
+    batch, facts_mine = c4_generate(cfg, mine)
+    facts_total = int((N.astype(np.int64) * V).sum())
+    rb = ReplayBatch(batch, eng=eng)
+    for _ in range(max(3, args.warmup)):
+        rb.run()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    kernel_ms = 0.0
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            n_ev, kms = rb.run()
+            kernel_ms += kms
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1) / args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item())
+    value = facts_total / (ms_per_step / 1e3)
+    # e2e: the host-buffer C-ABI call (dfx_replay_batch: H2D, kernel, D2H)
+    e2e = None
+    if args.e2e_steps > 0:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.e2e_steps):
+            raw = run_replay(batch, event_cap=rb.cap)
+            d2h += raw.events.nbytes + raw.var_out.nbytes
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = sum(a.nbytes for a in (batch.fns, batch.ops, batch.var_flags, batch.stmt_span,
+                                     batch.sites, batch.arms))
+        e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
+               "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h // args.e2e_steps),
+               "path": "dfx_replay_batch (host buffers): H2D programs, E1 kernel, D2H events"}
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (dfx_gen_c4 structured-program generator)",
+            "config": {"workload": "C4: batch of %d independent functions, 64-2048 nodes, "
+                                   "32-512 vars, LPT-sharded" % cfg.n_funcs,
+                       "functions": cfg.n_funcs, "facts_total": facts_total,
+                       "parallelism": "function-sharded (LPT), %d GPU(s)" % world,
+                       "l2": "programs %.1f GB > 126 MB L2" % (batch.ops.nbytes / 1e9)},
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": args.steps,
+            "replay": {"kernel": "replay_kernel", "kernel_ms_per_step": kernel_ms / args.steps,
+                       "events": n_ev, "functions_rank0": int(len(mine)),
+                       "ops_rank0": int(batch.ops.shape[0])}}
+    if world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import _oracle  # noqa: E402  (cpu_baseline leg)
+        sample = np.arange(0, cfg.n_funcs, max(1, cfg.n_funcs // 300), dtype=np.int32)[:300]
+        sb, sfacts = c4_generate(cfg, sample)
+        t0 = time.perf_counter()
+        run_replay(sb, runner=_oracle.replay_runner)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": sfacts / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": "oracle/replay_oracle.c on %d functions of the same "
+                                          "batch (every %d-th)" % (len(sample), cfg.n_funcs // 300),
+                                "seconds_per_sample": dt}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
@@ -326,6 +430,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.workload == "c4":
+            run_c4(args, rank, world, local)
         else:
             run_ours(args, rank, world, local)
     finally:

@@ -142,6 +142,25 @@ typedef struct {
 /* Host buffers in, host buffers out (H2D + kernel + D2H). */
 int dfx_replay_batch(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
 
+/* Device-resident batch (configuration C4 timing): upload once, replay many
+ * times; dfx_replay_run leaves events/bits on the device and reports counts. */
+typedef struct dfx_replay dfx_replay;
+int dfx_replay_create(dfx_handle *h, const dfx_replay_in *in, int64_t event_cap, dfx_replay **out);
+int dfx_replay_run(dfx_handle *h, dfx_replay *r, int64_t *n_events, float *kernel_ms);
+int dfx_replay_fetch(dfx_handle *h, dfx_replay *r, dfx_replay_out *out);
+int dfx_replay_destroy(dfx_handle *h, dfx_replay *r);
+
+/* Configuration C4 generator: synthetic structured functions emitted
+ * directly as replay programs (csrc/c4gen.cpp).  dfx_gen_c4 takes the
+ * function ids to generate; call it with NULL arrays first to get the sizes
+ * (ops, vars, stmts, sites, arms). */
+int dfx_gen_c4_shapes(uint64_t seed, int32_t n, int32_t n_min, int32_t n_max,
+                      const int32_t *var_choices, int32_t n_choices, int32_t *N, int32_t *V);
+int dfx_gen_c4(uint64_t seed, const int32_t *fids, int32_t n, int32_t n_min, int32_t n_max,
+               const int32_t *var_choices, int32_t n_choices, dfx_fn_desc *fns, int32_t *ops,
+               int32_t *var_flags, int32_t *stmt_span, int32_t *sites, int32_t *arms,
+               int64_t *sizes, int64_t *facts_out);
+
 /* ------------------------------------------------------------------------ */
 /* Kernels (a)+(b): CSR fixpoint and transfer requirements (north star)      */
 /* ------------------------------------------------------------------------ */

@@ -106,6 +106,125 @@ int dfx_set_stream(dfx_handle* h, void* stream) {
 }
 
 // ---------------------------------------------------------------------------
+// E1: device-resident replay batches
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct dfx_replay {
+  std::vector<void*> allocs;
+  dfx::ReplayDev r{};
+  int64_t n_vars = 0;
+  int32_t n_funcs = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ~dfx_replay() {
+    for (void* p : allocs) cudaFree(p);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+};
+
+extern "C" {
+
+int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap, dfx_replay** out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_replay_create: null argument");
+  CK(cudaSetDevice(h->device));
+  const int nf = in->n_funcs;
+  std::vector<int32_t> item_fn, item_chunk;
+  int max_slots = 2;
+  for (int f = 0; f < nf; f++) {
+    const dfx_fn_desc& d = in->fns[f];
+    if (d.n_slots > 64 || d.max_loop_depth > 24 || d.max_br_depth > 48 || d.max_arms > 192)
+      return fail(DFX_E_LIMIT, "function %d exceeds replay limits (slots %d, loops %d, "
+                  "branches %d, arms %d)", f, d.n_slots, d.max_loop_depth, d.max_br_depth,
+                  d.max_arms);
+    if (d.n_slots > max_slots) max_slots = d.n_slots;
+    int chunks = (d.n_vars + 31) / 32;
+    if (chunks == 0) chunks = 1;
+    for (int c = 0; c < chunks; c++) {
+      item_fn.push_back(f);
+      item_chunk.push_back(c);
+    }
+  }
+  auto* rp = new dfx_replay();
+  cudaStream_t st = h->st();
+  auto up = [&](const void* src, size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes + 16) != cudaSuccess) return nullptr;
+    rp->allocs.push_back(p);
+    if (src && bytes) cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st);
+    return p;
+  };
+  dfx::ReplayDev& r = rp->r;
+  r.fns = (const dfx_fn_desc*)up(in->fns, sizeof(dfx_fn_desc) * (size_t)nf);
+  r.ops = (const int32_t*)up(in->ops, sizeof(int32_t) * 4 * (size_t)in->n_ops);
+  r.var_flags = (const int32_t*)up(in->var_flags, sizeof(int32_t) * (size_t)in->n_vars);
+  r.stmt_span = (const int32_t*)up(in->stmt_span, sizeof(int32_t) * 2 * (size_t)in->n_stmts);
+  r.sites = (const int32_t*)up(in->sites, sizeof(int32_t) * (size_t)in->n_sites);
+  r.arms = (const int32_t*)up(in->arms, sizeof(int32_t) * 2 * (size_t)in->n_arms);
+  r.item_fn = (const int32_t*)up(item_fn.data(), sizeof(int32_t) * item_fn.size());
+  r.item_chunk = (const int32_t*)up(item_chunk.data(), sizeof(int32_t) * item_chunk.size());
+  r.n_items = (int)item_fn.size();
+  r.max_slots = max_slots;
+  r.event_cap = event_cap > 0 ? event_cap : 1;
+  r.events = (dfx_event*)up(nullptr, sizeof(dfx_event) * (size_t)r.event_cap);
+  r.event_count = (unsigned long long*)up(nullptr, sizeof(unsigned long long));
+  r.var_out = (uint8_t*)up(nullptr, (size_t)in->n_vars + 1);
+  for (void* p : rp->allocs)
+    if (!p) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
+  if (rp->allocs.size() != 11) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
+  rp->n_vars = in->n_vars;
+  rp->n_funcs = nf;
+  CK(cudaEventCreate(&rp->e0));
+  CK(cudaEventCreate(&rp->e1));
+  CK(cudaStreamSynchronize(st));
+  *out = rp;
+  return DFX_OK;
+}
+
+int dfx_replay_run(dfx_handle* h, dfx_replay* rp, int64_t* n_events, float* kernel_ms) {
+  if (!h || !rp) return fail(DFX_E_ARG, "dfx_replay_run: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  CK(cudaMemsetAsync(rp->r.event_count, 0, sizeof(unsigned long long), st));
+  CK(cudaEventRecord(rp->e0, st));
+  int rc = dfx::replay_launch(rp->r, st);
+  if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  CK(cudaEventRecord(rp->e1, st));
+  unsigned long long count = 0;
+  CK(cudaMemcpyAsync(&count, rp->r.event_count, sizeof count, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, rp->e0, rp->e1));
+  if (n_events) *n_events = (int64_t)count;
+  if (kernel_ms) *kernel_ms = ms;
+  if ((int64_t)count > rp->r.event_cap)
+    return fail(DFX_E_NOSPC, "event capacity %lld < %llu", (long long)rp->r.event_cap, count);
+  return DFX_OK;
+}
+
+int dfx_replay_fetch(dfx_handle* h, dfx_replay* rp, dfx_replay_out* out) {
+  if (!h || !rp || !out) return fail(DFX_E_ARG, "dfx_replay_fetch: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  unsigned long long count = 0;
+  CK(cudaMemcpyAsync(&count, rp->r.event_count, sizeof count, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t n = (int64_t)count < out->event_cap ? (int64_t)count : out->event_cap;
+  if (n > rp->r.event_cap) n = rp->r.event_cap;
+  if (n) CK(cudaMemcpyAsync(out->events, rp->r.events, sizeof(dfx_event) * (size_t)n, cudaMemcpyDeviceToHost, st));
+  if (rp->n_vars) CK(cudaMemcpyAsync(out->var_out, rp->r.var_out, (size_t)rp->n_vars, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out->n_events = (int64_t)count;
+  return (int64_t)count > out->event_cap ? DFX_E_NOSPC : DFX_OK;
+}
+
+int dfx_replay_destroy(dfx_handle* h, dfx_replay* rp) {
+  if (h) cudaSetDevice(h->device);
+  delete rp;
+  return DFX_OK;
+}
+
+// ---------------------------------------------------------------------------
 // E1: dfx_replay_batch  (replaces dartomp.dataflow.analyze_function,
 // pkg/src/dartomp/dataflow.py:737-740, batched over functions)
 // ---------------------------------------------------------------------------

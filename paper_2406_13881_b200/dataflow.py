@@ -59,7 +59,7 @@ class PackedBatch:
         r.n_vars = int(self.var_flags.shape[0])
         r.n_stmts = int(self.stmt_span.shape[0])
         r.n_sites = int(self.sites.shape[0])
-        r.n_arms = int(self.arms.shape[0])
+        r.n_arms = int(self.arms.shape[0]) // 2     # units of (kind, node) pairs
         return r
 
 

@@ -284,6 +284,21 @@ typedef struct {
 /* replaces dartomp.interproc.summarize_all: host buffers in and out */
 int dfx_summaries(dfx_handle *h, const dfx_cg_in *in, dfx_cg_out *out);
 
+/* Sharded building blocks (multi-GPU: one process per GPU; the caller
+ * all-gathers the rows each shard computed after every wave).  Tables are
+ * caller-owned DEVICE memory: bits [n_funcs * nsp] uint8, list
+ * [n_funcs * nsp] int16, len [n_funcs] int32, nsp = dfx_cg_nsp(). */
+typedef struct dfx_cg dfx_cg;
+typedef struct { uint8_t *bits; int16_t *list; int32_t *len; } dfx_cg_tables;
+int dfx_cg_create(dfx_handle *h, const dfx_cg_in *in, dfx_cg **out);
+int dfx_cg_destroy(dfx_handle *h, dfx_cg *cg);
+int32_t dfx_cg_nsp(dfx_cg *cg);
+/* rebuild the functions of `wave` at positions p (p % nshards == shard) into
+ * `cur`, reading callees from `cur` (earlier in dict order) or `prev`;
+ * *changed = 1 if any rebuilt bit set differs from `prev` */
+int dfx_cg_wave(dfx_handle *h, dfx_cg *cg, const dfx_cg_tables *prev, dfx_cg_tables *cur,
+                int32_t wave, int32_t shard, int32_t nshards, int32_t *changed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -648,9 +648,8 @@ std::vector<T> pad_rows(const T* src, int rows, int ns, int nsp) {
 
 extern "C" {
 
-// replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
-int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
-  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");
+int dfx_cg_create(dfx_handle* h, const dfx_cg_in* in, dfx_cg** out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_cg_create: null argument");
   CK(cudaSetDevice(h->device));
   cudaStream_t st = h->st();
   const int nf = in->n_funcs, ns = in->n_slots;
@@ -664,8 +663,6 @@ int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
     return p;
   };
   auto direct = pad_rows(in->direct, nf, ns, nsp);
-  auto ibits = pad_rows(in->init_bits, nf, ns, nsp);
-  auto ilist = pad_rows(in->init_list, nf, ns, nsp);
   g.direct = (const uint8_t*)up(direct.data(), direct.size());
   g.src_off = (const int32_t*)up(in->src_off, sizeof(int32_t) * (nf + 1));
   g.src = (const int32_t*)up(in->src, sizeof(int32_t) * 4 * in->n_src);
@@ -674,27 +671,69 @@ int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
   g.wave_fns = (const int32_t*)up(in->wave_fns, sizeof(int32_t) * nf);
   c->wave_off.assign(in->wave_off, in->wave_off + in->n_waves + 1);
   g.h_wave_off = c->wave_off.data();
-  uint8_t* bits[2];
-  int16_t* list[2];
-  int32_t* len[2];
-  for (int k = 0; k < 2; k++) {
-    bits[k] = (uint8_t*)up(k == 0 ? ibits.data() : nullptr, ibits.size());
-    list[k] = (int16_t*)up(k == 0 ? ilist.data() : nullptr, sizeof(int16_t) * ilist.size());
-    len[k] = (int32_t*)up(k == 0 ? in->init_len : nullptr, sizeof(int32_t) * nf);
-  }
   c->d_changed = (int*)cg_alloc(c, sizeof(int));
   for (void* p : c->allocs)
-    if (!p) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
-  if (c->allocs.size() != 13) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
-  int prev = 0, passes = 0, launches = 0, rc = DFX_OK;
+    if (!p) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_cg_create: allocation failed"); }
+  if (c->allocs.size() != 7) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_cg_create: allocation failed"); }
+  CK(cudaStreamSynchronize(st));
+  *out = c;
+  return DFX_OK;
+}
+
+int dfx_cg_destroy(dfx_handle* h, dfx_cg* c) {
+  if (h) cudaSetDevice(h->device);
+  return cg_destroy_impl(c);
+}
+
+int32_t dfx_cg_nsp(dfx_cg* c) { return c ? c->g.nsp : -1; }
+
+int dfx_cg_wave(dfx_handle* h, dfx_cg* c, const dfx_cg_tables* prev, dfx_cg_tables* cur,
+                int32_t wave, int32_t shard, int32_t nshards, int32_t* changed) {
+  if (!h || !c || !prev || !cur) return fail(DFX_E_ARG, "dfx_cg_wave: null argument");
+  if (wave < 0 || wave >= c->g.n_waves || nshards < 1 || shard < 0 || shard >= nshards)
+    return fail(DFX_E_ARG, "dfx_cg_wave: bad wave/shard");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  CK(cudaMemsetAsync(c->d_changed, 0, sizeof(int), st));
+  int rc = dfx::cg_wave(c->g, prev->bits, prev->list, prev->len, cur->bits, cur->list, cur->len,
+                        wave, shard, nshards, c->d_changed, st);
+  if (rc) return fail(rc, "cg_wave failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (changed) {
+    CK(cudaMemcpyAsync(changed, c->d_changed, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return DFX_OK;
+}
+
+// replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
+int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");
+  dfx_cg* c = nullptr;
+  int rc = dfx_cg_create(h, in, &c);
+  if (rc) return rc;
+  cudaStream_t st = h->st();
+  const int nf = in->n_funcs, ns = in->n_slots, nsp = c->g.nsp;
+  auto ibits = pad_rows(in->init_bits, nf, ns, nsp);
+  auto ilist = pad_rows(in->init_list, nf, ns, nsp);
+  dfx_cg_tables t[2];
+  for (int k = 0; k < 2; k++) {
+    t[k].bits = (uint8_t*)cg_alloc(c, ibits.size());
+    t[k].list = (int16_t*)cg_alloc(c, sizeof(int16_t) * ilist.size());
+    t[k].len = (int32_t*)cg_alloc(c, sizeof(int32_t) * nf);
+    if (!t[k].bits || !t[k].list || !t[k].len) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
+  }
+  CK(cudaMemcpyAsync(t[0].bits, ibits.data(), ibits.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t[0].list, ilist.data(), sizeof(int16_t) * ilist.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t[0].len, in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  int prev = 0, passes = 0, launches = 0;
   CK(cudaEventRecord(h->ev0, st));
   while (passes < in->max_passes) {
     passes++;
     const int cur = prev ^ 1;
     CK(cudaMemsetAsync(c->d_changed, 0, sizeof(int), st));
-    for (int w = 0; w < g.n_waves && rc == DFX_OK; w++) {
-      rc = dfx::cg_wave(g, bits[prev], list[prev], len[prev], bits[cur], list[cur], len[cur],
-                        w, 0, 1, c->d_changed, st);
+    for (int w = 0; w < c->g.n_waves && rc == DFX_OK; w++) {
+      rc = dfx::cg_wave(c->g, t[prev].bits, t[prev].list, t[prev].len, t[cur].bits, t[cur].list,
+                        t[cur].len, w, 0, 1, c->d_changed, st);
       launches++;
     }
     if (rc) break;
@@ -708,9 +747,9 @@ int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
   if (rc) { cg_destroy_impl(c); return fail(rc, "cg_wave failed: %s", cudaGetErrorString(cudaGetLastError())); }
   std::vector<uint8_t> hb((size_t)nf * nsp);
   std::vector<int16_t> hl((size_t)nf * nsp);
-  CK(cudaMemcpyAsync(hb.data(), bits[prev], hb.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hl.data(), list[prev], sizeof(int16_t) * hl.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(out->len, len[prev], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hb.data(), t[prev].bits, hb.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hl.data(), t[prev].list, sizeof(int16_t) * hl.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out->len, t[prev].len, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int f = 0; f < nf; f++) {
     std::memcpy(out->bits + (size_t)f * ns, &hb[(size_t)f * nsp], ns);

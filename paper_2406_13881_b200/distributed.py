@@ -1,0 +1,145 @@
+"""Multi-GPU drivers: one process per GPU, `torch.distributed` for plumbing.
+
+* Kernel (c) across GPUs (`ShardedSummaries`): each wave of the reference's
+  pass schedule is split round-robin over the ranks; a rank rebuilds its
+  share of the wave's functions on its GPU (`dfx_cg_wave`), then the ranks
+  all-gather the rebuilt summary rows (bits + insertion order + length) --
+  the only data exchanged, over NCCL/NVLink on GPUs (north star: "only
+  function summaries are exchanged, by NCCL allgather").  A pass ends with a
+  MAX all-reduce of the changed flag (the reference's termination test).
+* Kernels (a)+(b) and E1 shard without communication (variables and
+  functions are independent, SURVEY F3 / SPEC.md:345): see `bench.py`
+  (`C3Config.w0`, `batch.lpt_shards`).
+
+`wave_impl` is pluggable so the exchange protocol is tested on CPU with the
+gloo backend (tests/test_distributed.py) against a CPU wave restatement.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _abi
+
+
+class CgTables(C.Structure):
+    _fields_ = [("bits", C.c_void_p), ("list", C.c_void_p), ("len", C.c_void_p)]
+
+
+class ShardedSummaries:
+    def __init__(self, g, rank: int = 0, world: int = 1, device: str | torch.device = "cuda",
+                 wave_impl=None, max_passes: int | None = None):
+        self.g = g
+        self.rank, self.world = rank, world
+        self.device = torch.device(device)
+        nf, ns = g.init_bits.shape
+        self.nf, self.ns = nf, ns
+        self.nsp = ((ns + 31) // 32) * 32
+        self.max_passes = max_passes or max(16, nf + 1)
+        self.t = []
+        for k in range(2):
+            bits = torch.zeros((nf, self.nsp), dtype=torch.uint8, device=self.device)
+            lst = torch.zeros((nf, self.nsp), dtype=torch.int16, device=self.device)
+            ln = torch.zeros(nf, dtype=torch.int32, device=self.device)
+            self.t.append({"bits": bits, "list": lst, "len": ln})
+        self.t[0]["bits"][:, :ns] = torch.from_numpy(g.init_bits)
+        self.t[0]["list"][:, :ns] = torch.from_numpy(g.init_list)
+        self.t[0]["len"][:] = torch.from_numpy(g.init_len)
+        self.wave_impl = wave_impl or self._gpu_wave
+        self.cg = None
+        self.launches = 0
+        if wave_impl is None:
+            from .interproc import cg_struct
+            self.eng = _abi.engine(self.device.index or 0)
+            lib = self.eng.lib
+            for n in ("dfx_cg_create", "dfx_cg_destroy", "dfx_cg_wave"):
+                getattr(lib, n).restype = C.c_int
+            lib.dfx_cg_nsp.restype = C.c_int32
+            self._keep: list = []
+            cin = cg_struct(g, self._keep, self.max_passes)
+            h = C.c_void_p()
+            self.eng.check(lib.dfx_cg_create(self.eng.h, C.byref(cin), C.byref(h)), "dfx_cg_create")
+            self.cg = h
+            assert lib.dfx_cg_nsp(h) == self.nsp
+
+    def _tables(self, k) -> CgTables:
+        t = self.t[k]
+        return CgTables(t["bits"].data_ptr(), t["list"].data_ptr(), t["len"].data_ptr())
+
+    def _gpu_wave(self, prev: int, cur: int, w: int) -> int:
+        changed = C.c_int32(0)
+        pt, ct = self._tables(prev), self._tables(cur)
+        self.eng.check(self.eng.lib.dfx_cg_wave(self.eng.h, self.cg, C.byref(pt), C.byref(ct),
+                                                C.c_int32(w), C.c_int32(self.rank),
+                                                C.c_int32(self.world), C.byref(changed)),
+                       "dfx_cg_wave")
+        return int(changed.value)
+
+    def _exchange(self, cur: int, w: int) -> None:
+        """All-gather the rows each rank rebuilt in wave `w` into every rank's
+        `cur` tables."""
+        if self.world == 1:
+            return
+        lo, hi = int(self.g.wave_off[w]), int(self.g.wave_off[w + 1])
+        fns = torch.from_numpy(self.g.wave_fns[lo:hi].astype(np.int64)).to(self.device)
+        m = (hi - lo + self.world - 1) // self.world
+        if m == 0:
+            return
+        t = self.t[cur]
+        rowb = self.nsp + 2 * self.nsp + 4
+        mine = fns[self.rank::self.world]
+        send = torch.zeros((m, rowb), dtype=torch.uint8, device=self.device)
+        if mine.numel():
+            send[:mine.numel(), :self.nsp] = t["bits"].index_select(0, mine)
+            send[:mine.numel(), self.nsp:3 * self.nsp] = \
+                t["list"].index_select(0, mine).view(torch.uint8)
+            send[:mine.numel(), 3 * self.nsp:] = \
+                t["len"].index_select(0, mine).view(torch.uint8).view(-1, 4)
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(recv, send)
+        for r in range(self.world):
+            ids = fns[r::self.world]
+            k = ids.numel()
+            if k == 0 or r == self.rank:
+                continue
+            rows = recv[r][:k]
+            t["bits"].index_copy_(0, ids, rows[:, :self.nsp].contiguous())
+            t["list"].index_copy_(0, ids, rows[:, self.nsp:3 * self.nsp].contiguous().view(torch.int16))
+            t["len"].index_copy_(0, ids, rows[:, 3 * self.nsp:].contiguous().view(torch.int32).view(-1))
+
+    def solve(self):
+        """Returns (bits uint8 [nf, ns], list int16 [nf, ns], len int32, passes)."""
+        prev, passes = 0, 0
+        n_waves = self.g.wave_off.shape[0] - 1
+        while passes < self.max_passes:
+            passes += 1
+            cur = prev ^ 1
+            changed = 0
+            for w in range(n_waves):
+                changed |= self.wave_impl(prev, cur, w)
+                self.launches += 1
+                self._exchange(cur, w)
+            if self.world > 1:
+                flag = torch.tensor([changed], dtype=torch.int32, device=self.device)
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+                changed = int(flag.item())
+            prev = cur
+            if not changed:
+                break
+        t = self.t[prev]
+        return (t["bits"][:, :self.ns].cpu().numpy(), t["list"][:, :self.ns].cpu().numpy(),
+                t["len"].cpu().numpy(), passes)
+
+    def close(self):
+        if self.cg is not None:
+            self.eng.lib.dfx_cg_destroy(self.eng.h, self.cg)
+            self.cg = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

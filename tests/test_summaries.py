@@ -49,3 +49,20 @@ def test_oracle_vs_reference_fresh_callgraph(seed):
 @pytest.mark.parametrize("seed", [200, 201, 202])
 def test_cuda_vs_reference_fresh_callgraph(seed):
     _compare_with_reference(seed, 240, None)
+
+
+@pytest.mark.gpu
+def test_cuda_sharded_driver_world1_and_c5_scale():
+    """The multi-GPU driver path (dfx_cg_create/dfx_cg_wave on torch-owned
+    tables) at world size 1, on a 10k-function C5 graph."""
+    import numpy as np
+    from paper_2406_13881_b200.distributed import ShardedSummaries
+    from paper_2406_13881_b200.gen.c5 import generate_c5
+    g = generate_c5(seed=1)
+    exp = solve_call_graph(g, runner=_oracle.summaries_runner)
+    bits, lst, ln, passes = ShardedSummaries(g, 0, 1, device="cuda").solve()
+    assert passes == exp.passes and np.array_equal(bits, exp.bits) and np.array_equal(ln, exp.len)
+    for f in range(ln.shape[0]):
+        assert np.array_equal(lst[f, :ln[f]], exp.list[f, :ln[f]])
+    r = solve_call_graph(g)          # single-call path
+    _golden.assert_summary_equal(r, (exp.bits, exp.list, exp.len, exp.passes))

@@ -177,8 +177,18 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     prov[a * 32 + lane] = dp | (lw << 16);
   };
 
+  // op window: lane i holds op (wbase + i); an op is fetched by shuffles
+  // instead of a dependent global load per op
+  int wbase = -64;
+  int4 wop = make_int4(0, 0, 0, 0);
   for (;;) {
-    const int4 op = __ldg(fops + pc);
+    if (pc < wbase || pc >= wbase + 32) {
+      wbase = pc;
+      if (wbase + lane < d.n_ops) wop = __ldg(fops + wbase + lane);
+    }
+    const int src = pc - wbase;
+    const int4 op = make_int4(__shfl_sync(0xFFFFFFFFu, wop.x, src), __shfl_sync(0xFFFFFFFFu, wop.y, src),
+                              __shfl_sync(0xFFFFFFFFu, wop.z, src), __shfl_sync(0xFFFFFFFFu, wop.w, src));
     const int code = op.x & 0xFF, fl = op.x;
     seq++;
     const uint64_t key = seq << 24;

@@ -87,3 +87,17 @@ def test_corpus_matches_golden_report_and_text_cpu_oracle():
         assert lines == exp["report"], key
         n += 1
     assert n == 27
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_c2_lulesh_shaped_cpu_oracle(seed):
+    """Configuration C2: ~40 kernels over ~200 arrays in a time-step loop."""
+    from paper_2406_13881_b200.gen.lulesh import generate_lulesh
+    _e2e.compare(generate_lulesh(seed), "lulesh%d.c" % seed, **CPU)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4, 8))
+def test_c2_lulesh_shaped_cuda(seed):
+    from paper_2406_13881_b200.gen.lulesh import generate_lulesh
+    _e2e.compare(generate_lulesh(seed), "lulesh%d.c" % seed)

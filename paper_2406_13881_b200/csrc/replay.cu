@@ -116,7 +116,8 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 
   const int fi = __ldg(item_fn + item);
   const dfx_fn_desc d = fns[fi];
-  const int var = __ldg(item_chunk + item) * 32 + lane;
+  const int chunk = __ldg(item_chunk + item);
+  const int var = chunk * 32 + lane;
   const bool active = var < d.n_vars;
   const int myvar = active ? var : -1;
   int vflags = 0, rank = 0;
@@ -187,8 +188,16 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       if (wbase + lane < d.n_ops) wop = __ldg(fops + wbase + lane);
     }
     const int src = pc - wbase;
-    const int4 op = make_int4(__shfl_sync(0xFFFFFFFFu, wop.x, src), __shfl_sync(0xFFFFFFFFu, wop.y, src),
-                              __shfl_sync(0xFFFFFFFFu, wop.z, src), __shfl_sync(0xFFFFFFFFu, wop.w, src));
+    const int opx = __shfl_sync(0xFFFFFFFFu, wop.x, src), opy = __shfl_sync(0xFFFFFFFFu, wop.y, src);
+    // fast path: an access op on a variable outside this warp's 32-variable
+    // chunk only advances the visit counter (uniform across the warp)
+    if ((unsigned)((opx & 0xFF) - DFX_OP_HR) <= (unsigned)(DFX_OP_DW - DFX_OP_HR) && (opy >> 5) != chunk) {
+      seq++;
+      pc++;
+      continue;
+    }
+    const int4 op = make_int4(opx, opy, __shfl_sync(0xFFFFFFFFu, wop.z, src),
+                              __shfl_sync(0xFFFFFFFFu, wop.w, src));
     const int code = op.x & 0xFF, fl = op.x;
     seq++;
     const uint64_t key = seq << 24;

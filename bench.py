@@ -58,6 +58,11 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DFX_BENCH_SHARE_GPU=1 (testing only): several ranks on one GPU, gloo
+    # collectives -- exercises the multi-rank code path on a 1-GPU box
+    if os.environ.get("DFX_BENCH_SHARE_GPU"):
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return rank, world, local
 
 
@@ -426,7 +431,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            dist.init_process_group("gloo" if os.environ.get("DFX_BENCH_SHARE_GPU") else "nccl")
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)

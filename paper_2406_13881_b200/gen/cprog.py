@@ -34,6 +34,7 @@ class GenConfig:
     p_jump: float = 0.04
     p_braceless: float = 0.0      # braceless loop/if bodies (may trigger braces errors)
     p_late_decl: float = 0.0      # declare a local after the first kernel
+    p_fp_clause: float = 0.15     # kernels with an explicit firstprivate(...) clause
     size: int = 64
     n_ptr_params: int = 2
 
@@ -102,7 +103,7 @@ class ProgramGen:
         arrays, scalars = ctx["arrays"], ctx["scalars"]
         k = self.fresh("k")
         clauses = ""
-        if r.random() < 0.15 and scalars:
+        if r.random() < self.cfg.p_fp_clause and scalars:
             clauses = " firstprivate(%s)" % r.choice(scalars)
         kind = r.choice(["target teams distribute parallel for",
                          "target teams distribute parallel for",

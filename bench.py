@@ -199,7 +199,8 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2406_13881_b200 import _abi
-    from paper_2406_13881_b200.csr import C3Config, CsrProblem, MfpSession, c3_scalar_mask
+    from paper_2406_13881_b200.csr import (AccSession, C3Config, CsrProblem, MfpSession,
+                                           c3_scalar_mask)
 
     torch.cuda.set_device(local)
     eng = _abi.engine(local)
@@ -256,38 +257,62 @@ def run_ours(args, rank, world, local):
     rows = prob.requirements()
     req_ms = prob.stats.req_ms
 
-    # e2e: the reference-facing all-in-one C-ABI call with host buffers
+    # e2e: the reference-facing all-in-one C-ABI calls with pinned host
+    # buffers, host<->device copies inside the timed region.  Headline:
+    # dfx_mfp_acc -- per-node access lists in (the reference's per-statement
+    # MemoryAccess lists), per-node requirement variable lists out.  Beside
+    # it: dfx_mfp_csr on dense R/W bitplanes in, compacted mask rows out.
     e2e = None
     if args.e2e_steps > 0:
         def pinned(shape, dtype):
             n = int(np.prod(shape)) * np.dtype(dtype).itemsize
             buf = torch.empty(n, dtype=torch.uint8, pin_memory=True)
             return buf.numpy().view(dtype).reshape(shape)
+
+        def timed(run):
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            d2h = 0
+            for _ in range(args.e2e_steps):
+                d2h += run().nbytes
+            e1.record(stream)
+            torch.cuda.synchronize()
+            et = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64,
+                              device="cuda")
+            if world > 1:
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            return float(et.item()), d2h // args.e2e_steps
+
         rp, col, kind, R, W = prob.export_inputs(alloc=pinned)
         S = c3_scalar_mask(cfg)
-        h2d = rp.nbytes + col.nbytes + kind.nbytes + R.nbytes + W.nbytes + S.nbytes
+        n_req_bits = int(np.bitwise_count(rows.masks).sum())
+        # dense-plane path
+        h2d_planes = rp.nbytes + col.nbytes + kind.nbytes + R.nbytes + W.nbytes + S.nbytes
         sess = MfpSession(eng, alloc=pinned)
         out = sess.run(rp, col, kind, R, W, S)                   # warm (allocates)
         assert out.masks.shape[0] == rows.masks.shape[0], "e2e output differs from device run"
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        d2h = 0
-        for _ in range(args.e2e_steps):
-            out = sess.run(rp, col, kind, R, W, S)
-            d2h += out.nbytes
-        e1.record(stream)
-        torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64,
-                          device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
-               "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h // args.e2e_steps),
-               "path": "dfx_mfp_csr (host buffers, pinned): H2D inputs, kernels (a)+(b), "
-                       "D2H compacted requirement rows (offsets, occupancy, masks)"}
+        ms_planes, d2h_planes = timed(lambda: sess.run(rp, col, kind, R, W, S))
+        del R, W, out, sess
+        # list path (headline)
+        acc_off, acc = prob.export_acc(alloc=pinned)
+        h2d = rp.nbytes + col.nbytes + kind.nbytes + acc_off.nbytes + acc.nbytes + S.nbytes
+        asess = AccSession(eng, alloc=pinned)
+        out = asess.run(rp, col, kind, acc_off, acc, S, cfg.words)   # warm (allocates)
+        assert out.vars.shape[0] == n_req_bits, "list output differs from the mask rows"
+        ms, d2h = timed(lambda: asess.run(rp, col, kind, acc_off, acc, S, cfg.words))
+        e2e = {"value": facts_total / (ms / 1e3), "unit": UNIT,
+               "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "dfx_mfp_acc (pinned host buffers): H2D CSR + per-node access lists "
+                       "(uint16 var|kind), expansion to bitplanes, kernels (a)+(b), D2H per-node "
+                       "requirement variable lists (uint16) + row offsets",
+               "accesses": int(acc.shape[0]), "requirements": int(out.vars.shape[0]),
+               "dense_planes_path": {
+                   "value": facts_total / (ms_planes / 1e3), "ms_per_step": ms_planes,
+                   "h2d_bytes_per_step": int(h2d_planes), "d2h_bytes_per_step": int(d2h_planes),
+                   "path": "dfx_mfp_csr: H2D dense R/W bitplanes, D2H compacted mask rows"}}
 
     if rank != 0:
         return

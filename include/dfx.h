@@ -241,6 +241,51 @@ int64_t dfx_csr_nnz(dfx_csr *p);
 /* all-in-one host-buffer call: H2D, kernel (a), kernel (b), D2H of `out` */
 int dfx_mfp_csr(dfx_handle *h, const dfx_csr_in *in, dfx_req_out *out, dfx_csr_stats *stats);
 
+/* List forms of the same problem (csrc/acc.cu).  The reference describes each
+ * statement by its list of memory accesses (access.py:58-86 `MemoryAccess`,
+ * kind READ/WRITE/READWRITE) and answers with per-statement directive plans
+ * naming variables (dataflow.py:37-95).  Entries are uint16:
+ *   access      : var | kind << 14, kind 1 = read, 2 = write, 3 = read+write
+ *   requirement : var, | DFX_REQ_FIRSTPRIVATE for a firstprivate capture
+ * so the boundary moves accesses and planned transfers, not nodes x vars.
+ * V = 32 * words <= 16384. */
+#define DFX_ACC_READ 1
+#define DFX_ACC_WRITE 2
+#define DFX_REQ_FIRSTPRIVATE 0x8000
+
+typedef struct {
+  int64_t n_nodes;
+  int32_t words;                /* V/32: multiple of 4, at most 512 */
+  int64_t nnz;
+  int64_t n_acc;
+  const int32_t *row_ptr;       /* [n_nodes+1] */
+  const int32_t *col;           /* [nnz] predecessor ids */
+  const uint8_t *node_kind;     /* [n_nodes] 0 host, 1 kernel */
+  const int64_t *acc_off;       /* [n_nodes+1] node n's accesses: acc[acc_off[n] .. acc_off[n+1]) */
+  const uint16_t *acc;          /* [n_acc] any order; duplicates OR together */
+  const uint32_t *S;            /* [words] scalar-variable mask */
+} dfx_acc_in;
+
+/* Kernel (b) as per-node variable lists: node n's entries are
+ * vars[row_off[n] .. row_off[n+1]): transfer requirements ascending (update
+ * from at host nodes, update to at kernel nodes), then firstprivate captures
+ * ascending (DFX_REQ_FIRSTPRIVATE set). */
+typedef struct {
+  int64_t *row_off;             /* [n_nodes+1] (NULL: not copied) */
+  uint16_t *vars;               /* [cap] (NULL: count only) */
+  int64_t cap;
+  int64_t n_out;                /* out: total entries */
+} dfx_req_list;
+
+int dfx_csr_create_acc(dfx_handle *h, const dfx_acc_in *in, dfx_csr **out);   /* H2D + expand */
+int dfx_csr_requirements_list(dfx_handle *h, dfx_csr *p, dfx_req_list *out, dfx_csr_stats *stats);
+/* D2H of the problem's accesses as lists; acc == NULL: only *n_acc and acc_off */
+int dfx_csr_export_acc(dfx_handle *h, dfx_csr *p, int64_t *acc_off, uint16_t *acc, int64_t cap,
+                       int64_t *n_acc);
+/* all-in-one host-buffer call on lists: H2D, expand, kernel (a), kernel (b),
+ * D2H of the requirement lists */
+int dfx_mfp_acc(dfx_handle *h, const dfx_acc_in *in, dfx_req_list *out, dfx_csr_stats *stats);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel (c): interprocedural summaries (interproc.py:90-156)              */
 /* ------------------------------------------------------------------------ */

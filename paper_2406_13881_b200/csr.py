@@ -45,6 +45,72 @@ class ReqOut(C.Structure):
 
 REQ_UPDATE_FROM, REQ_UPDATE_TO, REQ_FIRSTPRIVATE = 1, 2, 3
 
+# list forms (include/dfx.h, csrc/acc.cu)
+ACC_READ, ACC_WRITE = 1, 2
+REQ_FP_FLAG = 0x8000
+
+
+class AccIn(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("words", C.c_int32), ("nnz", C.c_int64),
+                ("n_acc", C.c_int64), ("row_ptr", C.c_void_p), ("col", C.c_void_p),
+                ("node_kind", C.c_void_p), ("acc_off", C.c_void_p), ("acc", C.c_void_p),
+                ("S", C.c_void_p)]
+
+
+class ReqListOut(C.Structure):
+    _fields_ = [("row_off", C.c_void_p), ("vars", C.c_void_p), ("cap", C.c_int64),
+                ("n_out", C.c_int64)]
+
+
+@dataclass
+class ReqList:
+    """Kernel (b) output as per-node variable lists (include/dfx.h
+    dfx_req_list): node n's entries are vars[row_off[n]:row_off[n+1]],
+    transfer requirements ascending, then firstprivate captures (REQ_FP_FLAG)."""
+    row_off: np.ndarray      # int64 [n+1]
+    vars: np.ndarray         # uint16 [n_out]
+    words: int
+
+    @property
+    def nbytes(self) -> int:
+        return self.row_off.nbytes + self.vars.nbytes
+
+    def to_planes(self):
+        """Expand into dense (REQ, FP) planes [n, words]."""
+        return lists_to_planes(self.row_off, self.vars, self.words, REQ_FP_FLAG)
+
+
+def planes_to_acc(R: np.ndarray, W: np.ndarray):
+    """Dense read/write planes [n, words] -> (acc_off int64 [n+1], acc uint16):
+    per node, accessed variables ascending, entry = var | kind << 14."""
+    n, words = R.shape
+    rb = np.unpackbits(np.ascontiguousarray(R).view(np.uint8).reshape(n, words * 4), axis=1,
+                       bitorder="little").astype(np.uint16)
+    wb = np.unpackbits(np.ascontiguousarray(W).view(np.uint8).reshape(n, words * 4), axis=1,
+                       bitorder="little").astype(np.uint16)
+    k = rb * ACC_READ + wb * ACC_WRITE
+    nodes, vars_ = np.nonzero(k)
+    acc = (vars_.astype(np.uint16) | (k[nodes, vars_] << 14)).astype(np.uint16)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(nodes, minlength=n), out=off[1:])
+    return off, acc
+
+
+def lists_to_planes(off: np.ndarray, entries: np.ndarray, words: int, flag: int):
+    """Per-node variable lists -> two dense planes [n, words]: entries without
+    `flag` and entries with it (variable = low 14 bits)."""
+    n = off.shape[0] - 1
+    node = np.repeat(np.arange(n), np.diff(off))
+    var = (entries & 0x3FFF).astype(np.int64)
+    second = (entries & flag) != 0
+    planes = []
+    for sel in (~second, second):
+        bits = np.zeros((n, words * 32), dtype=np.uint8)
+        bits[node[sel], var[sel]] = 1
+        planes.append(np.packbits(bits, axis=1, bitorder="little").view(np.uint32)
+                      .reshape(n, words).copy())
+    return planes[0], planes[1]
+
 
 @dataclass
 class ReqRows:
@@ -91,7 +157,8 @@ class ReqRows:
 def _setup(lib):
     for name in ("dfx_set_stream", "dfx_csr_create", "dfx_csr_generate_c3", "dfx_csr_destroy",
                  "dfx_csr_solve", "dfx_csr_requirements", "dfx_csr_download", "dfx_mfp_csr",
-                 "dfx_csr_export"):
+                 "dfx_csr_export", "dfx_csr_create_acc", "dfx_csr_requirements_list",
+                 "dfx_csr_export_acc", "dfx_mfp_acc"):
         getattr(lib, name).restype = C.c_int
     lib.dfx_csr_nnz.restype = C.c_int64
 
@@ -160,6 +227,19 @@ class CsrProblem:
         eng.check(eng.lib.dfx_csr_create(eng.h, C.byref(cin), C.byref(h)), "dfx_csr_create")
         return cls(eng, h, n, words)
 
+    @classmethod
+    def from_acc(cls, row_ptr, col, kind, acc_off, acc, S, words: int,
+                 eng: _abi.Engine | None = None) -> "CsrProblem":
+        """Build from access lists (dfx_csr_create_acc): H2D + expansion."""
+        eng = eng or _abi.engine()
+        _setup(eng.lib)
+        cin, keep = _acc_in(row_ptr, col, kind, acc_off, acc, S, words)
+        h = C.c_void_p()
+        eng.check(eng.lib.dfx_csr_create_acc(eng.h, C.byref(cin), C.byref(h)),
+                  "dfx_csr_create_acc")
+        del keep
+        return cls(eng, h, int(row_ptr.shape[0]) - 1, words)
+
     def close(self) -> None:
         if self.h:
             self.eng.lib.dfx_csr_destroy(self.eng.h, self.h)
@@ -187,6 +267,37 @@ class CsrProblem:
         return _req_call(lambda o: self.eng.lib.dfx_csr_requirements(
             self.eng.h, self.h, C.byref(o), C.byref(self.stats)),
             self.eng, self.n_nodes, self.words, capacity, alloc, self.stats)
+
+    def requirements_list(self, capacity: int | None = None, alloc=np.empty) -> ReqList:
+        """Kernel (b) as per-node variable lists (dfx_csr_requirements_list)."""
+        if capacity is None:
+            o = ReqListOut(None, None, 0, 0)
+            self.eng.check(self.eng.lib.dfx_csr_requirements_list(
+                self.eng.h, self.h, C.byref(o), C.byref(self.stats)), "requirements_list(count)")
+            capacity = int(o.n_out)
+        while True:
+            row_off = alloc((self.n_nodes + 1,), np.int64)
+            vars_ = alloc((max(1, capacity),), np.uint16)
+            o = ReqListOut(row_off.ctypes.data, vars_.ctypes.data, vars_.shape[0], 0)
+            rc = self.eng.lib.dfx_csr_requirements_list(self.eng.h, self.h, C.byref(o),
+                                                        C.byref(self.stats))
+            if rc == _abi.DFX_E_NOSPC:
+                capacity = int(o.n_out)
+                continue
+            self.eng.check(rc, "dfx_csr_requirements_list")
+            return ReqList(row_off, vars_[: o.n_out], self.words)
+
+    def export_acc(self, alloc=np.empty):
+        """D2H of the problem's accesses as lists (acc_off int64 [n+1], acc uint16)."""
+        n_acc = C.c_int64()
+        self.eng.check(self.eng.lib.dfx_csr_export_acc(self.eng.h, self.h, None, None, 0,
+                                                       C.byref(n_acc)), "export_acc(count)")
+        off = alloc((self.n_nodes + 1,), np.int64)
+        acc = alloc((max(1, n_acc.value),), np.uint16)
+        self.eng.check(self.eng.lib.dfx_csr_export_acc(
+            self.eng.h, self.h, C.c_void_p(off.ctypes.data), C.c_void_p(acc.ctypes.data),
+            C.c_int64(acc.shape[0]), C.byref(n_acc)), "dfx_csr_export_acc")
+        return off, acc[: n_acc.value]
 
     def export_inputs(self, alloc=np.empty):
         """D2H of the inputs (row_ptr, col, kind, R, W); `alloc(shape, dtype)`
@@ -264,6 +375,53 @@ class MfpSession:
                 continue
             self.eng.check(rc, "dfx_mfp_csr")
             return ReqRows(row_off, occ, masks[: o.n_masks], words)
+
+
+def _acc_in(row_ptr, col, kind, acc_off, acc, S, words):
+    arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, acc_off, acc, S)]
+    row_ptr, col, kind, acc_off, acc, S = arrs
+    assert row_ptr.dtype == np.int32 and col.dtype == np.int32 and kind.dtype == np.uint8
+    assert acc_off.dtype == np.int64 and acc.dtype == np.uint16 and S.dtype == np.uint32
+    n = int(row_ptr.shape[0]) - 1
+    cin = AccIn(n, words, int(col.shape[0]), int(acc_off[-1]),
+                *(a.ctypes.data for a in arrs))
+    return cin, arrs
+
+
+class AccSession:
+    """Reference-facing all-in-one host-buffer path on lists (`dfx_mfp_acc`):
+    H2D of the CSR and the per-node access lists, expansion, kernels (a)+(b),
+    D2H of the per-node requirement lists.  Output buffers are reused across
+    calls (optionally pinned)."""
+
+    def __init__(self, eng: _abi.Engine | None = None, alloc=np.empty):
+        self.eng = eng or _abi.engine()
+        _setup(self.eng.lib)
+        self.alloc = alloc
+        self.capacity = 0
+        self.stats = CsrStats()
+        self._bufs = None
+
+    def run(self, row_ptr, col, kind, acc_off, acc, S, words: int) -> ReqList:
+        cin, keep = _acc_in(row_ptr, col, kind, acc_off, acc, S, words)
+        n = int(cin.n_nodes)
+        if self.capacity == 0:
+            self.capacity = max(1024, int(cin.n_acc))
+        while True:
+            if self._bufs is None or self._bufs[1].shape[0] < self.capacity \
+                    or self._bufs[0].shape[0] != n + 1:
+                self._bufs = (self.alloc((n + 1,), np.int64),
+                              self.alloc((self.capacity,), np.uint16))
+            row_off, vars_ = self._bufs
+            o = ReqListOut(row_off.ctypes.data, vars_.ctypes.data, vars_.shape[0], 0)
+            rc = self.eng.lib.dfx_mfp_acc(self.eng.h, C.byref(cin), C.byref(o),
+                                          C.byref(self.stats))
+            if rc == _abi.DFX_E_NOSPC:
+                self.capacity = int(o.n_out)
+                continue
+            self.eng.check(rc, "dfx_mfp_acc")
+            del keep
+            return ReqList(row_off, vars_[: o.n_out], words)
 
 
 def mfp_csr(row_ptr, col, kind, R, W, S, eng: _abi.Engine | None = None):

@@ -1,0 +1,200 @@
+// acc.cu -- access-list input and requirement-list output of kernels (a)+(b).
+//
+// The reference's front end describes every statement by a list of memory
+// accesses (dartomp/access.py:58-86 `MemoryAccess`: variable, kind
+// READ/WRITE/READWRITE; `classify_accesses` access.py:387-402), and its
+// analysis answers with per-statement directive plans naming variables
+// (dataflow.py:37-95 `DirectivePlan`).  The list forms below carry exactly
+// that across the boundary, so the host<->device traffic is proportional to
+// the accesses and the planned transfers, not to nodes x variables:
+//
+//   access entry    uint16  var | kind << 14   (kind 1 read, 2 write, 3 both)
+//   requirement     uint16  var | 0x8000 if firstprivate
+//
+// expand_acc_kernel  : access lists -> the A/B/USE bitplanes of kernel (a)
+// export_acc_kernel  : bitplanes -> access lists (benchmark/test export)
+// compact_list_kernel: requirement planes of kernel (b) -> per-node variable
+//                      lists, transfer requirements ascending, then
+//                      firstprivate captures ascending
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dfx.h"
+#include "dfx_internal.h"
+
+namespace dfx {
+
+namespace {
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int kWarps = 8;   // warps per block
+
+__device__ __forceinline__ int warp_exclusive_scan(int v, int lane, int* total) {
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  *total = __shfl_sync(FULL, incl, 31);
+  return incl - v;
+}
+}  // namespace
+
+// One warp per node: OR the node's access entries into two shared-memory
+// rows (reads, writes), then store USE = R, B = W, A = R | W coalesced.
+__global__ void __launch_bounds__(kWarps * 32)
+expand_acc_kernel(int64_t n_nodes, int words, const int64_t* __restrict__ off,
+                  const uint16_t* __restrict__ acc, uint32_t* __restrict__ A,
+                  uint32_t* __restrict__ B, uint32_t* __restrict__ USE, int* bad) {
+  extern __shared__ uint32_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* r = sm + (size_t)warp * 2 * words;
+  uint32_t* w = r + words;
+  const int nvars = words * 32;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = (int64_t)blockIdx.x * kWarps + warp; n < n_nodes; n += wstride) {
+    for (int i = lane; i < words; i += 32) r[i] = w[i] = 0u;
+    __syncwarp();
+    const int64_t e1 = off[n + 1];
+    for (int64_t e = off[n] + lane; e < e1; e += 32) {
+      const uint32_t a = acc[e];
+      const uint32_t v = a & 0x3FFFu, k = a >> 14;
+      if (v >= (uint32_t)nvars || k == 0u) { atomicExch(bad, 1); continue; }
+      const uint32_t bit = 1u << (v & 31);
+      if (k & 1u) atomicOr(&r[v >> 5], bit);
+      if (k & 2u) atomicOr(&w[v >> 5], bit);
+    }
+    __syncwarp();
+    const size_t row = (size_t)n * words;
+    for (int i = 4 * lane; i < words; i += 128) {
+      const uint4 rr = *reinterpret_cast<const uint4*>(r + i);
+      const uint4 ww = *reinterpret_cast<const uint4*>(w + i);
+      __stcs(reinterpret_cast<uint4*>(USE + row + i), rr);
+      __stcs(reinterpret_cast<uint4*>(B + row + i), ww);
+      __stcs(reinterpret_cast<uint4*>(A + row + i),
+             make_uint4(rr.x | ww.x, rr.y | ww.y, rr.z | ww.z, rr.w | ww.w));
+    }
+    __syncwarp();
+  }
+}
+
+// Per node: number of accessed variables (popcount of R | W).
+__global__ void __launch_bounds__(kWarps * 32)
+count_acc_kernel(int64_t n_nodes, int words, const uint32_t* __restrict__ A, int32_t* counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_nodes; n += wstride) {
+    int c = 0;
+    for (int i = lane; i < words; i += 32) c += __popc(__ldg(A + (size_t)n * words + i));
+    c = (int)__reduce_add_sync(FULL, (unsigned)c);
+    if (lane == 0) counts[n] = c;
+  }
+}
+
+// Per node: the access entries in ascending variable order.  Lane l covers
+// words l, l+32, ...; a warp scan of per-lane counts gives each lane's slot.
+__global__ void __launch_bounds__(kWarps * 32)
+export_acc_kernel(int64_t n_nodes, int words, const uint32_t* __restrict__ R,
+                  const uint32_t* __restrict__ W, const int64_t* __restrict__ off,
+                  uint16_t* __restrict__ acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_nodes; n += wstride) {
+    int64_t base = off[n];
+    for (int i0 = 0; i0 < words; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t r = 0u, w = 0u;
+      if (i < words) {
+        r = __ldg(R + (size_t)n * words + i);
+        w = __ldg(W + (size_t)n * words + i);
+      }
+      uint32_t m = r | w;
+      int tot;
+      int64_t pos = base + warp_exclusive_scan(__popc(m), lane, &tot);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t k = ((r >> b) & 1u) | (((w >> b) & 1u) << 1);
+        acc[pos++] = (uint16_t)((uint32_t)(32 * i + b) | (k << 14));
+      }
+      base += tot;
+    }
+  }
+}
+
+// Requirement planes (REQ, FPQ from requirements_kernel with bit counts) ->
+// per-node variable lists at offsets[n]: requirement vars ascending, then
+// firstprivate vars ascending with DFX_REQ_FIRSTPRIVATE set.
+__global__ void __launch_bounds__(kWarps * 32)
+compact_list_kernel(int64_t n_nodes, int words, const uint32_t* __restrict__ REQ,
+                    const uint32_t* __restrict__ FPQ, const int32_t* __restrict__ fp_slot,
+                    int n_fp_slots, const int64_t* __restrict__ offsets,
+                    uint16_t* __restrict__ vars, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_nodes; n += wstride) {
+    int64_t base = offsets[n];
+    for (int pass = 0; pass < 2; pass++) {
+      for (int i0 = 0; i0 < words; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t m = 0u;
+        if (i < words) {
+          if (pass == 0) {
+            m = __ldg(REQ + (size_t)n * words + i);
+          } else {
+            const int slot = fp_slot[i >> 2];
+            if (slot >= 0) m = __ldg(FPQ + ((size_t)n * n_fp_slots + slot) * 4 + (i & 3));
+          }
+        }
+        int tot;
+        int64_t pos = base + warp_exclusive_scan(__popc(m), lane, &tot);
+        const uint32_t flag = pass ? (uint32_t)DFX_REQ_FIRSTPRIVATE : 0u;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          if (pos < cap) vars[pos] = (uint16_t)((uint32_t)(32 * i + b) | flag);
+          pos++;
+        }
+        base += tot;
+      }
+    }
+  }
+}
+
+static int grid_nodes(int64_t n) {
+  int64_t g = (n + kWarps - 1) / kWarps;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, cudaStream_t st) {
+  const size_t smem = (size_t)kWarps * 2 * p.words * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(expand_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  expand_acc_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, smem, st>>>(p.n_nodes, p.words, off, acc,
+                                                                      p.A, p.B, p.USE, bad);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int count_acc(const CsrDev& p, int32_t* counts, cudaStream_t st) {
+  count_acc_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, 0, st>>>(p.n_nodes, p.words, p.A, counts);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int export_acc(const CsrDev& p, const int64_t* off, uint16_t* acc, cudaStream_t st) {
+  export_acc_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, 0, st>>>(p.n_nodes, p.words, p.USE, p.B,
+                                                                   off, acc);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int compact_list(const CsrDev& p, const int64_t* offsets, uint16_t* vars, int64_t cap,
+                 cudaStream_t st) {
+  compact_list_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, 0, st>>>(
+      p.n_nodes, p.words, p.REQ, p.FPQ, p.fp_slot, p.n_fp_slots, offsets, vars, cap);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+}  // namespace dfx

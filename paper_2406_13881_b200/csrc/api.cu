@@ -328,6 +328,9 @@ struct dfx_csr {
   uint32_t* d_masks = nullptr;
   int64_t masks_cap = 0;
   uint32_t* d_occ = nullptr;
+  uint16_t* d_vars = nullptr;     // requirement lists (grow-only)
+  int64_t vars_cap = 0;
+  int* d_bad = nullptr;           // access-list validation flag
   void* d_cnt = nullptr;
   uint8_t* flags = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -348,6 +351,7 @@ int csr_destroy_impl(dfx_csr* c) {
   for (void* p : c->allocs) cudaFree(p);
   if (c->d_masks) cudaFree(c->d_masks);
   if (c->d_occ) cudaFree(c->d_occ);
+  if (c->d_vars) cudaFree(c->d_vars);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   delete c;
@@ -380,8 +384,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   c->scratch_bytes = dfx::scan_scratch_bytes(n);
   c->scratch = csr_alloc<uint8_t>(c, c->scratch_bytes);
   c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_ctl_bytes());
-  p.succ_ptr = csr_alloc<int32_t>(c, n + 1);
-  p.succ = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
+  c->d_bad = csr_alloc<int>(c, 1);
   c->flags = csr_alloc<uint8_t>(c, 2 * (size_t)n);   // >= 2 * n_chunks for chunk_nodes >= 1
   // scalar quads -> FP slots
   std::vector<int32_t> slot(words / 4, -1);
@@ -398,7 +401,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   for (void* a : c->allocs)
     if (!a) return fail(DFX_E_CUDA, "cudaMalloc failed for a %lld-node x %d-word problem",
                         (long long)n, words);
-  if (c->allocs.size() != 22) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
+  if (c->allocs.size() != 21) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
   CK(cudaMemcpy(p.S, S_host, sizeof(uint32_t) * words, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(p.fp_slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice));
   CK(cudaEventCreate(&c->e0));
@@ -431,7 +434,6 @@ int csr_upload(dfx_csr* c, const dfx_csr_in* in, cudaStream_t st) {
   CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
   int rc = dfx::or_planes(p, st);
   if (!rc) rc = dfx::build_desc(p, st);
-  if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
   if (rc) return fail(rc, "or_planes/build_desc launch failed");
   return DFX_OK;
 }
@@ -475,7 +477,6 @@ int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
   if (rc) { csr_destroy_impl(c); return rc; }
   rc = dfx::c3_generate(c->p, spec->seed, spec->w0, h->st(), c->scratch, c->scratch_bytes);
   if (!rc) rc = dfx::build_desc(c->p, h->st());
-  if (!rc) rc = dfx::build_succ(c->p, c->scratch, c->scratch_bytes, c->counts, h->st());
   if (rc) { csr_destroy_impl(c); return fail(rc, "c3 generation failed"); }
   CK(cudaStreamSynchronize(h->st()));
   *out = c;
@@ -609,6 +610,153 @@ int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_out* out, dfx_csr_s
   }
   rc = dfx_csr_solve(h, c, 0, stats);
   if (!rc) rc = dfx_csr_requirements(h, c, out, stats);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// list forms (csrc/acc.cu): access lists in, requirement lists out
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+int check_acc_in(const dfx_acc_in* in) {
+  if (!in->row_ptr || !in->node_kind || !in->acc_off || !in->S || (in->nnz && !in->col) ||
+      (in->n_acc && !in->acc))
+    return fail(DFX_E_ARG, "dfx_acc_in: null array");
+  return check_words(in->n_nodes, in->words);
+}
+
+// H2D of CSR + access lists into already-allocated buffers, then expand the
+// lists into the A/B/USE planes and build the node descriptors
+int csr_upload_acc(dfx_handle* h, dfx_csr* c, const dfx_acc_in* in, cudaStream_t st) {
+  dfx::CsrDev& p = c->p;
+  auto* d_off = (int64_t*)dbuf(h, "acc_off", sizeof(int64_t) * (size_t)(in->n_nodes + 1));
+  auto* d_acc = (uint16_t*)dbuf(h, "acc", sizeof(uint16_t) * (size_t)(in->n_acc > 0 ? in->n_acc : 1));
+  if (!d_off || !d_acc) return fail(DFX_E_CUDA, "access-list buffers: allocation failed");
+  CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
+  if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_off, in->acc_off, sizeof(int64_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
+  if (in->n_acc) CK(cudaMemcpyAsync(d_acc, in->acc, sizeof(uint16_t) * in->n_acc, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
+  int rc = dfx::build_desc(p, st);
+  if (!rc) rc = dfx::expand_acc(p, d_off, d_acc, c->d_bad, st);
+  if (rc) return fail(rc, "expand_acc/build_desc launch failed");
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) return fail(DFX_E_ARG, "access list: variable >= %d or kind 0", 32 * in->words);
+  return DFX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int dfx_csr_create_acc(dfx_handle* h, const dfx_acc_in* in, dfx_csr** out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_csr_create_acc: null argument");
+  CK(cudaSetDevice(h->device));
+  int rc = check_acc_in(in);
+  if (rc) return rc;
+  auto* c = new dfx_csr();
+  rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
+  if (!rc) rc = csr_upload_acc(h, c, in, h->st());
+  if (rc) { csr_destroy_impl(c); return rc; }
+  *out = c;
+  return DFX_OK;
+}
+
+int dfx_csr_requirements_list(dfx_handle* h, dfx_csr* c, dfx_req_list* out, dfx_csr_stats* stats) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_requirements_list: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const dfx::CsrDev& p = c->p;
+  int64_t n_out = 0;
+  CK(cudaEventRecord(c->e0, st));
+  int rc = dfx::requirements_scan(p, c->counts, c->offsets, c->scratch, c->scratch_bytes, 1, &n_out, st);
+  if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
+  // row offsets go back while the lists are compacted
+  if (out && out->row_off)
+    CK(cudaMemcpyAsync(out->row_off, c->offsets, sizeof(int64_t) * (size_t)(p.n_nodes + 1),
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));   // n_out is on the host now
+  const int64_t want = (out && out->vars) ? out->cap : 0;
+  if (want && n_out <= want) {
+    if (n_out > c->vars_cap) {
+      if (c->d_vars) cudaFree(c->d_vars);
+      c->d_vars = nullptr;
+      c->vars_cap = 0;
+      CK(cudaMalloc(&c->d_vars, sizeof(uint16_t) * (size_t)(n_out + n_out / 8 + 64)));
+      c->vars_cap = n_out + n_out / 8 + 64;
+    }
+    rc = dfx::compact_list(p, c->offsets, c->d_vars, c->vars_cap, st);
+    if (rc) return fail(rc, "compact_list failed");
+    CK(cudaEventRecord(c->e1, st));
+    if (n_out) CK(cudaMemcpyAsync(out->vars, c->d_vars, sizeof(uint16_t) * (size_t)n_out,
+                                  cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaEventRecord(c->e1, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (out) out->n_out = n_out;
+  if (stats) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    stats->req_ms = ms;
+    stats->n_masks = n_out;
+  }
+  if (want && n_out > want)
+    return fail(DFX_E_NOSPC, "requirement-list capacity %lld < %lld", (long long)want, (long long)n_out);
+  return DFX_OK;
+}
+
+int dfx_csr_export_acc(dfx_handle* h, dfx_csr* c, int64_t* acc_off, uint16_t* acc, int64_t cap,
+                       int64_t* n_acc) {
+  if (!h || !c || !n_acc) return fail(DFX_E_ARG, "dfx_csr_export_acc: null argument");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const dfx::CsrDev& p = c->p;
+  int rc = dfx::count_acc(p, c->counts, st);
+  int64_t n = 0;
+  if (!rc) rc = dfx::scan_counts(p.n_nodes, c->counts, c->offsets, c->scratch, c->scratch_bytes, &n, st);
+  if (rc) return fail(rc, "export_acc: count/scan failed");
+  CK(cudaStreamSynchronize(st));
+  *n_acc = n;
+  if (acc_off)
+    CK(cudaMemcpyAsync(acc_off, c->offsets, sizeof(int64_t) * (size_t)(p.n_nodes + 1),
+                       cudaMemcpyDeviceToHost, st));
+  if (acc) {
+    if (cap < n) return fail(DFX_E_NOSPC, "access-list capacity %lld < %lld", (long long)cap, (long long)n);
+    auto* d_acc = (uint16_t*)dbuf(h, "acc_export", sizeof(uint16_t) * (size_t)(n > 0 ? n : 1));
+    if (!d_acc) return fail(DFX_E_CUDA, "export_acc: allocation failed");
+    rc = dfx::export_acc(p, c->offsets, d_acc, st);
+    if (rc) return fail(rc, "export_acc launch failed");
+    if (n) CK(cudaMemcpyAsync(acc, d_acc, sizeof(uint16_t) * (size_t)n, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return DFX_OK;
+}
+
+int dfx_mfp_acc(dfx_handle* h, const dfx_acc_in* in, dfx_req_list* out, dfx_csr_stats* stats) {
+  if (!h || !in) return fail(DFX_E_ARG, "dfx_mfp_acc: null argument");
+  CK(cudaSetDevice(h->device));
+  int rc = check_acc_in(in);
+  if (rc) return rc;
+  // device buffers persist in the handle across calls of the same shape
+  dfx_csr* c = h->csr_cache;
+  if (c && (c->p.n_nodes != in->n_nodes || c->p.words != in->words || c->p.nnz != in->nnz ||
+            !same_scalars(c, in->S, in->words))) {
+    csr_destroy_impl(c);
+    c = h->csr_cache = nullptr;
+  }
+  if (!c) {
+    c = new dfx_csr();
+    rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
+    if (rc) { csr_destroy_impl(c); return rc; }
+    h->csr_cache = c;
+  }
+  rc = csr_upload_acc(h, c, in, h->st());
+  if (!rc) rc = dfx_csr_solve(h, c, 0, stats);
+  if (!rc) rc = dfx_csr_requirements_list(h, c, out, stats);
   return rc;
 }
 

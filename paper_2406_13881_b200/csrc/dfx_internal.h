@@ -51,8 +51,6 @@ struct CsrDev {
   int32_t* popc;    // per-node population count of the current OUT row
   int32_t s_quads_low;  // every nonzero scalar quad has index < 8
   int32_t* desc;        // [n_nodes][8] node descriptors (rs, deg|kind<<30, p0..p3)
-  int32_t* succ_ptr;    // [n_nodes+1] successor (reverse) CSR
-  int32_t* succ;        // [nnz]
 };
 
 struct SolveStats {
@@ -68,10 +66,19 @@ int build_desc(const CsrDev& p, cudaStream_t st);
 int vpl_for(int words);
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
               SolveStats* stats);
-int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st);
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
                  size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
                  int64_t* n_out, cudaStream_t st);
+int requirements_scan(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                      size_t scratch_bytes, int count_bits, int64_t* n_out, cudaStream_t st);
+int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratch,
+                size_t scratch_bytes, int64_t* n_out, cudaStream_t st);
+// access lists (acc.cu)
+int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, cudaStream_t st);
+int count_acc(const CsrDev& p, int32_t* counts, cudaStream_t st);
+int export_acc(const CsrDev& p, const int64_t* off, uint16_t* acc, cudaStream_t st);
+int compact_list(const CsrDev& p, const int64_t* offsets, uint16_t* vars, int64_t cap,
+                 cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
 size_t round_ctl_bytes();
 

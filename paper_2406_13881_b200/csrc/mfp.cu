@@ -353,38 +353,6 @@ __global__ void build_desc_kernel(int64_t n_nodes, const int32_t* row_ptr, const
   }
 }
 
-__global__ void succ_count_kernel(int64_t nnz, const int32_t* col, int32_t* cnt) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + col[e], 1);
-}
-__global__ void succ_fill_kernel(int64_t n_nodes, const int32_t* row_ptr, const int32_t* col,
-                                 int32_t* cursor, int32_t* succ) {
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
-       n += (int64_t)gridDim.x * blockDim.x)
-    for (int e = row_ptr[n]; e < row_ptr[n + 1]; e++) succ[atomicAdd(cursor + col[e], 1)] = (int32_t)n;
-}
-
-// reverse (successor) CSR: succ_ptr [n+1], succ [nnz]; order inside a row
-// is irrelevant (it only feeds chunk dirty flags)
-int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st) {
-  int g = (int)((p.nnz + 255) / 256);
-  if (g > 148 * 64) g = 148 * 64;
-  if (g < 1) g = 1;
-  if (cudaMemsetAsync(p.succ_ptr, 0, sizeof(int32_t) * (p.n_nodes + 1), st) != cudaSuccess) return DFX_E_CUDA;
-  if (p.nnz) succ_count_kernel<<<g, 256, 0, st>>>(p.nnz, p.col, p.succ_ptr + 1);
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
-  if (cudaMemcpyAsync(tmp, p.succ_ptr, sizeof(int32_t) * p.n_nodes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-    return DFX_E_CUDA;
-  int gn = (int)((p.n_nodes + 255) / 256);
-  if (gn > 148 * 64) gn = 148 * 64;
-  succ_fill_kernel<<<gn, 256, 0, st>>>(p.n_nodes, p.row_ptr, p.col, tmp, p.succ);
-  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
-}
-
 int build_desc(const CsrDev& p, cudaStream_t st) {
   int g = (int)((p.n_nodes + 255) / 256);
   if (g > 148 * 64) g = 148 * 64;
@@ -559,7 +527,7 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
 // ---------------------------------------------------------------------------
 template <int VPL>
 __global__ void __launch_bounds__(256)
-requirements_kernel(CsrDev p, int32_t* counts) {
+requirements_kernel(CsrDev p, int32_t* counts, int count_bits) {
   const int lane = threadIdx.x & 31;
   const int nq = p.words >> 2;
   const uint4* A = reinterpret_cast<const uint4*>(p.A);
@@ -611,10 +579,12 @@ requirements_kernel(CsrDev p, int32_t* counts) {
         fp = and4(andn4(f, id[v]), ih[v]);
       }
       __stcs(REQ + row + q, req);
-      cnt += (req.x != 0) + (req.y != 0) + (req.z != 0) + (req.w != 0);
+      cnt += count_bits ? __popc(req.x) + __popc(req.y) + __popc(req.z) + __popc(req.w)
+                        : (req.x != 0) + (req.y != 0) + (req.z != 0) + (req.w != 0);
       if (p.fp_slot[q] >= 0) {
         FPQ[(size_t)n * p.n_fp_slots + p.fp_slot[q]] = fp;
-        cnt += (fp.x != 0) + (fp.y != 0) + (fp.z != 0) + (fp.w != 0);
+        cnt += count_bits ? __popc(fp.x) + __popc(fp.y) + __popc(fp.z) + __popc(fp.w)
+                          : (fp.x != 0) + (fp.y != 0) + (fp.z != 0) + (fp.w != 0);
       }
     }
 #pragma unroll
@@ -806,15 +776,44 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
   return DFX_OK;
 }
 
+// kernel (b) and the scan of its per-node counts: offsets[n] = start of node
+// n's output (nonzero masks, or set bits when count_bits); *n_out (host) =
+// total.  The caller synchronises before reading *n_out.
+int requirements_scan(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                      size_t scratch_bytes, int count_bits, int64_t* n_out, cudaStream_t st) {
+  const int vpl = vpl_for(p.words);
+  int blocks = grid_for(p.n_nodes * 32, 256);
+  switch (vpl) {
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
+    default: return DFX_E_LIMIT;
+  }
+  return scan_counts(p.n_nodes, counts, offsets, scratch, scratch_bytes, n_out, st);
+}
+
+int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratch,
+                size_t scratch_bytes, int64_t* n_out, cudaStream_t st) {
+  if (cudaMemsetAsync(offsets, 0, sizeof(int64_t), st) != cudaSuccess) return DFX_E_CUDA;
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, counts, offsets + 1, (int)n, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, counts, offsets + 1, (int)n, st);
+  if (n_out && cudaMemcpyAsync(n_out, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st) !=
+                   cudaSuccess)
+    return DFX_E_CUDA;
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
                  size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
                  int64_t* n_out, cudaStream_t st) {
   const int vpl = vpl_for(p.words);
   int blocks = grid_for(p.n_nodes * 32, 256);
   switch (vpl) {
-    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts); break;
-    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts); break;
-    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts); break;
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, 0); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, 0); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 0); break;
     default: return DFX_E_LIMIT;
   }
   // offsets[0] = 0; offsets[1..n] = inclusive prefix of counts

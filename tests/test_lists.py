@@ -1,0 +1,35 @@
+"""CPU: host-side list forms of kernels (a)+(b) (include/dfx.h dfx_acc_in /
+dfx_req_list) -- numpy converters between dense planes and per-node lists."""
+import numpy as np
+
+import _mfp_ref
+from paper_2406_13881_b200.csr import REQ_FP_FLAG, lists_to_planes, planes_to_acc
+
+
+def test_planes_to_acc_round_trip():
+    rng = np.random.default_rng(7)
+    for words in (4, 8, 132):
+        _, _, _, R, W, _ = _mfp_ref.random_graph(rng, 300, words)
+        off, acc = planes_to_acc(R, W)
+        assert off[0] == 0 and off[-1] == acc.shape[0]
+        kind = acc >> 14
+        assert np.all((kind >= 1) & (kind <= 3))
+        # reads = entries with the read bit, writes = entries with the write bit
+        rd, _ = lists_to_planes(off, np.where(kind & 1, acc & 0x3FFF, 0x4000).astype(np.uint16),
+                                words, 0x4000)
+        wr, _ = lists_to_planes(off, np.where(kind & 2, acc & 0x3FFF, 0x4000).astype(np.uint16),
+                                words, 0x4000)
+        assert np.array_equal(rd, R) and np.array_equal(wr, W)
+        # ascending variables inside each node
+        for i in range(0, 300, 17):
+            v = (acc[off[i]:off[i + 1]] & 0x3FFF).astype(np.int64)
+            assert np.all(np.diff(v) > 0)
+
+
+def test_requirement_lists_split_on_firstprivate_flag():
+    off = np.array([0, 3, 3, 5], dtype=np.int64)
+    ent = np.array([1, 40, 5 | REQ_FP_FLAG, 127, 0 | REQ_FP_FLAG], dtype=np.uint16)
+    req, fp = lists_to_planes(off, ent, 4, REQ_FP_FLAG)
+    assert req[0, 0] == 2 and req[0, 1] == 1 << 8 and fp[0, 0] == 1 << 5
+    assert not req[1].any() and not fp[1].any()
+    assert req[2, 3] == 1 << 31 and fp[2, 0] == 1

@@ -4,7 +4,7 @@ import pytest
 
 import _mfp_ref
 import _oracle
-from paper_2406_13881_b200.csr import C3Config, CsrProblem, mfp_csr
+from paper_2406_13881_b200.csr import AccSession, C3Config, CsrProblem, mfp_csr, planes_to_acc
 
 pytestmark = pytest.mark.gpu
 
@@ -87,3 +87,65 @@ def test_full_size_c3_properties():
     assert np.array_equal(OH[:, 0:4], eh0) and np.array_equal(OD[:, 0:4], ed0)
     # idempotence: solving again from the fixpoint changes nothing
     assert st.rounds_h >= 2
+
+
+# ---- list forms (dfx_csr_create_acc / dfx_csr_requirements_list / dfx_mfp_acc)
+
+def _check_lists(rl, g, eh, ed):
+    REQ, FP = _oracle.c3_requirements(g, eh, ed)
+    rq, rf = rl.to_planes()
+    assert np.array_equal(rq, REQ) and np.array_equal(rf, FP)
+    # per-node order: requirement vars ascending, then firstprivate ascending
+    cnt = np.unpackbits(REQ.view(np.uint8), axis=1).sum(axis=1) + \
+        np.unpackbits(FP.view(np.uint8), axis=1).sum(axis=1)
+    assert np.array_equal(np.diff(rl.row_off), cnt)
+    for n in np.nonzero(cnt)[0][:200]:
+        e = rl.vars[rl.row_off[n]:rl.row_off[n + 1]].astype(np.int64)
+        key = (e & 0x8000) * 4 + (e & 0x3FFF)
+        assert np.all(np.diff(key) > 0)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_acc_lists_random_graphs(seed):
+    rng = np.random.default_rng(300 + seed)
+    words = [4, 8, 128, 132][seed]
+    row_ptr, col, kind, R, W, S = _mfp_ref.random_graph(rng, 600, words)
+    g = {"row_ptr": row_ptr, "col": col, "kind": kind, "A": R | W, "B": W, "USE": R, "S": S}
+    off, acc = planes_to_acc(R, W)
+    shuffled = acc.copy()
+    for i in range(0, len(off) - 1, 7):         # order inside a node is free
+        rng.shuffle(shuffled[off[i]:off[i + 1]])
+    prob = CsrProblem.from_acc(row_ptr, col, kind, off, shuffled, S, words)
+    prob.solve()
+    eh, ed, _ = _oracle.c3_solve(g)
+    OH, OD, _ = prob.download(True, True)
+    assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
+    _check_lists(prob.requirements_list(), g, eh, ed)
+    # export round trip: planes -> lists on the device == numpy lists
+    eoff, eacc = prob.export_acc()
+    assert np.array_equal(eoff, off) and np.array_equal(eacc, acc)
+
+
+def test_acc_all_in_one_matches_plane_path():
+    g = _oracle.c3_generate(9, 1 << 14, 0, 128, 82)
+    off, acc = planes_to_acc(g["USE"], g["B"])
+    sess = AccSession()
+    rl = sess.run(g["row_ptr"], g["col"], g["kind"], off, acc, g["S"], 128)
+    eh, ed, _ = _oracle.c3_solve(g)
+    _check_lists(rl, g, eh, ed)
+    rl2 = sess.run(g["row_ptr"], g["col"], g["kind"], off, acc, g["S"], 128)   # cached buffers
+    assert np.array_equal(rl2.vars, rl.vars) and np.array_equal(rl2.row_off, rl.row_off)
+    assert sess.stats.solve_ms > 0
+
+
+def test_acc_rejects_bad_entries():
+    g = _oracle.c3_generate(3, 256, 0, 4, 8)
+    off, acc = planes_to_acc(g["USE"], g["B"])
+    bad = acc.copy()
+    bad[0] = 200 | (1 << 14)                      # var 200 >= V = 128
+    with pytest.raises(RuntimeError):
+        CsrProblem.from_acc(g["row_ptr"], g["col"], g["kind"], off, bad, g["S"], 4)
+    bad = acc.copy()
+    bad[0] = bad[0] & 0x3FFF                      # kind 0
+    with pytest.raises(RuntimeError):
+        CsrProblem.from_acc(g["row_ptr"], g["col"], g["kind"], off, bad, g["S"], 4)

@@ -385,6 +385,11 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   c->scratch = csr_alloc<uint8_t>(c, c->scratch_bytes);
   c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_ctl_bytes());
   c->d_bad = csr_alloc<int>(c, 1);
+  p.seen = csr_alloc<uint8_t>(c, nnz > 0 ? nnz : 1);
+  p.chunk_done = csr_alloc<int32_t>(c, n);
+  p.seen4 = csr_alloc<uint32_t>(c, n);
+  p.succ_ptr = csr_alloc<int32_t>(c, n + 1);
+  p.succ = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
   c->flags = csr_alloc<uint8_t>(c, 2 * (size_t)n);   // >= 2 * n_chunks for chunk_nodes >= 1
   // scalar quads -> FP slots
   std::vector<int32_t> slot(words / 4, -1);
@@ -401,7 +406,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   for (void* a : c->allocs)
     if (!a) return fail(DFX_E_CUDA, "cudaMalloc failed for a %lld-node x %d-word problem",
                         (long long)n, words);
-  if (c->allocs.size() != 21) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
+  if (c->allocs.size() != 26) return fail(DFX_E_CUDA, "cudaMalloc failed (%lld nodes)", (long long)n);
   CK(cudaMemcpy(p.S, S_host, sizeof(uint32_t) * words, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(p.fp_slot, slot.data(), sizeof(int32_t) * slot.size(), cudaMemcpyHostToDevice));
   CK(cudaEventCreate(&c->e0));
@@ -434,6 +439,7 @@ int csr_upload(dfx_csr* c, const dfx_csr_in* in, cudaStream_t st) {
   CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
   int rc = dfx::or_planes(p, st);
   if (!rc) rc = dfx::build_desc(p, st);
+  if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
   if (rc) return fail(rc, "or_planes/build_desc launch failed");
   return DFX_OK;
 }
@@ -477,6 +483,7 @@ int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
   if (rc) { csr_destroy_impl(c); return rc; }
   rc = dfx::c3_generate(c->p, spec->seed, spec->w0, h->st(), c->scratch, c->scratch_bytes);
   if (!rc) rc = dfx::build_desc(c->p, h->st());
+  if (!rc) rc = dfx::build_succ(c->p, c->scratch, c->scratch_bytes, c->counts, h->st());
   if (rc) { csr_destroy_impl(c); return fail(rc, "c3 generation failed"); }
   CK(cudaStreamSynchronize(h->st()));
   *out = c;
@@ -640,6 +647,7 @@ int csr_upload_acc(dfx_handle* h, dfx_csr* c, const dfx_acc_in* in, cudaStream_t
   if (in->n_acc) CK(cudaMemcpyAsync(d_acc, in->acc, sizeof(uint16_t) * in->n_acc, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
   int rc = dfx::build_desc(p, st);
+  if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
   if (!rc) rc = dfx::expand_acc(p, d_off, d_acc, c->d_bad, st);
   if (rc) return fail(rc, "expand_acc/build_desc launch failed");
   int bad = 0;

@@ -51,6 +51,11 @@ struct CsrDev {
   int32_t* popc;    // per-node population count of the current OUT row
   int32_t s_quads_low;  // every nonzero scalar quad has index < 8
   int32_t* desc;        // [n_nodes][8] node descriptors (rs, deg|kind<<30, p0..p3)
+  uint8_t* seen;        // [nnz] per-edge seen round, edges >= 4 of a node (kernel a frontier)
+  int32_t* succ_ptr;    // [n_nodes+1] successor (reverse) CSR: candidate flags of kernel (a)
+  int32_t* succ;        // [nnz]
+  uint32_t* seen4;      // [n_nodes] seen rounds of a node's first 4 edges, one byte each
+  int32_t* chunk_done;  // [n_nodes] per-chunk round completed (kernel a frontier)
 };
 
 struct SolveStats {
@@ -63,6 +68,7 @@ struct SolveStats {
 int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch, size_t scratch_bytes);
 int or_planes(const CsrDev& p, cudaStream_t st);
 int build_desc(const CsrDev& p, cudaStream_t st);
+int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st);
 int vpl_for(int words);
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
               SolveStats* stats);

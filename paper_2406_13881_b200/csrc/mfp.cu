@@ -25,7 +25,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
-#include <cuda_pipeline.h>
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstdio>
 
@@ -114,7 +114,9 @@ constexpr int kMaxRounds = 64;
 struct RoundCtl {
   RoundCounters cnt[kMaxRounds + 1];
   unsigned int blocks_done[kMaxRounds + 1];
+  unsigned long long t_end[kMaxRounds + 1];   // persistent kernel: %globaltimer after each round
   int done;
+  int rounds;                                  // persistent kernel: rounds run (incl. the last, unchanged one)
 };
 
 // per-warp counters -> round totals; the last block to finish decides
@@ -353,6 +355,38 @@ __global__ void build_desc_kernel(int64_t n_nodes, const int32_t* row_ptr, const
   }
 }
 
+__global__ void succ_count_kernel(int64_t nnz, const int32_t* col, int32_t* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[e], 1);
+}
+__global__ void succ_fill_kernel(int64_t n_nodes, const int32_t* row_ptr, const int32_t* col,
+                                 int32_t* cursor, int32_t* succ) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x)
+    for (int e = row_ptr[n]; e < row_ptr[n + 1]; e++) succ[atomicAdd(cursor + col[e], 1)] = (int32_t)n;
+}
+
+// reverse (successor) CSR: succ_ptr [n+1], succ [nnz]; order inside a row
+// is irrelevant (it only feeds the per-chunk candidate flags of kernel (a))
+int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st) {
+  int g = (int)((p.nnz + 255) / 256);
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  if (cudaMemsetAsync(p.succ_ptr, 0, sizeof(int32_t) * (p.n_nodes + 1), st) != cudaSuccess) return DFX_E_CUDA;
+  if (p.nnz) succ_count_kernel<<<g, 256, 0, st>>>(p.nnz, p.col, p.succ_ptr + 1);
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
+  if (cudaMemcpyAsync(tmp, p.succ_ptr, sizeof(int32_t) * p.n_nodes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return DFX_E_CUDA;
+  int gn = (int)((p.n_nodes + 255) / 256);
+  if (gn > 148 * 64) gn = 148 * 64;
+  succ_fill_kernel<<<gn, 256, 0, st>>>(p.n_nodes, p.row_ptr, p.col, tmp, p.succ);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 int build_desc(const CsrDev& p, cudaStream_t st) {
   int g = (int)((p.n_nodes + 255) / 256);
   if (g > 148 * 64) g = 148 * 64;
@@ -362,16 +396,43 @@ int build_desc(const CsrDev& p, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// kernel (a), V <= 4096 fast path: node descriptors prefetched one 32-node
-// batch ahead, so the only dependent metadata latency per batch is the
-// predecessor change stamps; otherwise identical to mfp_round_kernel
+// kernel (a), V <= 4096 fast path.  Node descriptors are prefetched one
+// 32-node batch ahead.  The frontier is per edge ("seen" rounds):
+//   stamp[p]      last round in which p's row changed
+//   chunk_done[c] last round in which chunk c was completely swept; a chunk's
+//                 rows are final for that round once its flag is set
+//   seen[e]       for edge e = (p -> n): n has incorporated every change of
+//                 p up to the end of round seen[e] -- r if p's chunk was done
+//                 in round r when n's batch checked it (or p is n's
+//                 fall-through predecessor taken from registers), else r-1
+// n is re-evaluated in round r+1 iff some edge has stamp[p] > seen[e] (plus
+// the Gauss-Seidel rule: a node whose fall-through predecessor changed
+// earlier in the same sweep is re-evaluated at once).  Round 1 reads every
+// predecessor whose chunk is already done and treats the others as top.
+// Values only decrease from top, so any value read is >= the fixpoint; a
+// round without changes leaves no edge with stamp > seen, so the phase ends
+// at the greatest fixpoint.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+// cumulative release: the warp's row stores (ordered before this by the
+// preceding __syncwarp) become visible before the flag
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 template <int PHASE, int MINB>
 __global__ void __launch_bounds__(256, MINB)
-mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
-                    RoundCtl* ctl, uint8_t* flags_cur, uint8_t* flags_next) {
-  if (__ldcg(&ctl->done)) return;
-  RoundCounters* cnt = &ctl->cnt[round];
+mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t* flags,
+                 int max_rounds) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int nq = p.words >> 2;
   const bool act = lane < nq;
@@ -382,15 +443,44 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
   const int4* desc = reinterpret_cast<const int4*>(p.desc);
   const uint4 smask = act ? ldg4(reinterpret_cast<const uint4*>(p.S) + lane) : zero4();
   const bool has_s = nz4(smask);
-  const bool any_s = __any_sync(FULL, has_s);
   const uint4 boundary = PHASE == 0 ? all4() : zero4();
-  unsigned long long n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;
+  for (int round = 1; round <= max_rounds; round++) {
+  const int first = round == 1;
+  RoundCounters* cnt = &ctl->cnt[round];
+  uint8_t* fcur = flags + (size_t)(round & 1) * n_chunks;
+  uint8_t* fnext = flags + (size_t)((round + 1) & 1) * n_chunks;
+  unsigned n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;   // per warp
+  // sparse rounds (late, few changes): static chunk striding, and only chunks
+  // a predecessor change flagged during the previous round are swept
+  // mark(r): round r flags successor chunks for round r+1, decided on round
+  // r-1's change count (final: the previous launch has completed)
+  auto marks = [&](int r) {
+    return r >= 2 && 8 * __ldcg(&ctl->cnt[r - 1].changed) <= 5ull * (unsigned long long)p.n_nodes;
+  };
+  const bool mark = marks(round);
+  const bool sparse = round >= 3 && marks(round - 1);
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int chunk = sparse ? gwarp - nwarps : 0;
 
   for (;;) {
-    int chunk = 0;
-    if (lane == 0) chunk = (int)atomicAdd(&cnt->chunk, 1ull);
-    chunk = __shfl_sync(FULL, chunk, 0);
+    if (sparse) {
+      chunk += nwarps;
+    } else {
+      if (lane == 0) chunk = (int)atomicAdd(&cnt->chunk, 1ull);
+      chunk = __shfl_sync(FULL, chunk, 0);
+    }
     if (chunk >= n_chunks) break;
+    // an unflagged chunk's rows are final for this round
+    if (sparse) {
+      int f = 0;
+      if (lane == 0) {
+        f = __ldcg(fcur + chunk);
+        if (f) fcur[chunk] = 0;               // reused as fnext next round
+        else st_relaxed(p.chunk_done + chunk, round);
+      }
+      if (!__shfl_sync(FULL, f, 0)) continue;
+    }
     const int n0 = chunk * chunk_nodes;
     const int n1 = min(n0 + chunk_nodes, (int)p.n_nodes);
     uint4 prev = zero4();
@@ -410,26 +500,35 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
       const int rs = d0.x, deg = d0.y & 0x3FFFFFFF, kd = (d0.y >> 30) & 1;
       const int pr0 = d0.z, pr1 = d0.w, pr2 = d1.x, pr3 = d1.y;
       const int cur_opc = first ? 32 * p.words : opc;
-      // issue the change-stamp loads of this batch and the next batch's descriptors
+      // dn bit k: pred k's chunk is done for this round (its row is final);
+      // the acquire orders the warp's later row loads after the release
+      unsigned dn = 0;
       bool dirty = first != 0;
-      int st0 = -4, st1 = -4, st2 = -4, st3 = -4;
-      if (valid && !first) {
-        if (deg > 0) st0 = __ldcg(p.stamp + pr0);
-        if (deg > 1) st1 = __ldcg(p.stamp + pr1);
-        if (deg > 2) st2 = __ldcg(p.stamp + pr2);
-        if (deg > 3) st3 = __ldcg(p.stamp + pr3);
+      if (valid) {
+        if (!first) {
+          const unsigned s4 = __ldcg(p.seen4 + n);
+#define DFX_DIRTY(K, Q) \
+  if (deg > K) dirty |= __ldcg(p.stamp + (Q)) > (int)((s4 >> (8 * K)) & 0xFFu);
+          DFX_DIRTY(0, pr0) DFX_DIRTY(1, pr1) DFX_DIRTY(2, pr2) DFX_DIRTY(3, pr3)
+#undef DFX_DIRTY
+          for (int e = rs + KP; e < rs + deg && !dirty; e++)
+            dirty = __ldcg(p.stamp + __ldg(p.col + e)) > (int)__ldcg(p.seen + e);
+        }
+        if (dirty) {
+#define DFX_DONE(K, Q)                                                                   \
+  if (deg > K) {                                                                         \
+    const int c_ = (Q) / chunk_nodes;                                                    \
+    if (c_ != chunk && ld_acquire(p.chunk_done + c_) == round) dn |= 1u << K;           \
+  }
+          DFX_DONE(0, pr0) DFX_DONE(1, pr1) DFX_DONE(2, pr2) DFX_DONE(3, pr3)
+#undef DFX_DONE
+        }
       }
       const int nn1 = nb + 32 + lane;
       if (nn1 < n1) {
         d0 = __ldg(desc + 2 * nn1);
         d1 = __ldg(desc + 2 * nn1 + 1);
         if (!first) opc = __ldcg(p.popc + nn1);
-      }
-      if (valid && !first) {
-        const int lim = round - 1;
-        dirty = st0 >= lim || st1 >= lim || st2 >= lim || st3 >= lim;
-        for (int e = rs + KP; e < rs + deg && !dirty; e++)
-          dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= lim;
       }
       unsigned dm = __ballot_sync(FULL, valid && dirty);
       if (carry && nb < n1) dm |= 1u;
@@ -439,64 +538,73 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
         const int j = __ffs(dm) - 1;
         dm &= dm - 1;
         const int nn = nb + j;
-        const int nrs = __shfl_sync(FULL, rs, j);
         const int ndeg = __shfl_sync(FULL, deg, j);
         const bool kern = __shfl_sync(FULL, kd, j) != 0;
         const int old_pc = __shfl_sync(FULL, cur_opc, j);
+        const unsigned ndn = __shfl_sync(FULL, dn, j);
         const int q0 = __shfl_sync(FULL, pr0, j), q1 = __shfl_sync(FULL, pr1, j);
         const int q2 = __shfl_sync(FULL, pr2, j), q3 = __shfl_sync(FULL, pr3, j);
         const size_t row = (size_t)nn * nq;
-        const bool need_hin = PHASE == 1 && kern && any_s;
         const bool have_prev = prev_n == nn - 1;
         const uint4* plane = (PHASE == 0) == kern ? B : A;
-        uint4 pl = zero4(), b0 = zero4(), hin = all4();
+        uint4 pl = zero4(), b0 = zero4(), oh = zero4();
         uint4 in = ndeg == 0 ? boundary : all4();
         if (act) {
           pl = ldg4(plane + row + lane);
-          if (need_hin && has_s) b0 = ldg4(B + row + lane);
+          // D phase, kernel node: F & H_in = F & OUT_H[n] (F = A & ~B & S is
+          // disjoint from B and OUT_H = H_in & ~B), only scalar lanes
+          if (PHASE == 1 && kern && has_s) { b0 = ldg4(B + row + lane); oh = ldcg4(OH + row + lane); }
         }
-        // gathers: all issued before use
-        uint4 g[KP];
-        bool use[KP];
-        const int qs[KP] = {q0, q1, q2, q3};
-#pragma unroll
-        for (int k = 0; k < KP; k++) {
-          use[k] = false;
-          g[k] = all4();
-          if (k >= ndeg) continue;
-          if (qs[k] == nn - 1 && have_prev) { g[k] = prev; continue; }
-          if (first) continue;
-          use[k] = true;
-          if (act) g[k] = ldcg4(OUT + (size_t)qs[k] * nq + lane);
-        }
-        if (need_hin && has_s) {
-#pragma unroll
-          for (int k = 0; k < KP; k++)
-            if (k < ndeg) hin = and4(hin, ldg4(OH + (size_t)qs[k] * nq + lane));
-        }
-#pragma unroll
-        for (int k = 0; k < KP; k++) { in = and4(in, g[k]); n_read += use[k]; }
-        for (int e = nrs + KP; e < nrs + ndeg; e++) {      // rare: more than KP preds
-          const int qk = __ldg(p.col + e);
-          if (qk == nn - 1 && have_prev) in = and4(in, prev);
-          else if (!first) {
-            if (act) in = and4(in, ldcg4(OUT + (size_t)qk * nq + lane));
-            n_read++;
+        // gathers, all issued before use; per edge the round whose final
+        // value this evaluation incorporates
+        unsigned s4 = 0;
+        uint4 g0 = all4(), g1 = all4(), g2 = all4(), g3 = all4();
+#define DFX_GATHER(K, Q, G)                                                              \
+  if (ndeg > K) {                                                                        \
+    if ((Q) == nn - 1 && have_prev) {                                                    \
+      G = prev;                                                                          \
+      s4 |= (unsigned)round << (8 * K);                                                  \
+    } else {                                                                             \
+      const bool fin_ = (ndn >> K) & 1u;                                                 \
+      s4 |= (unsigned)(fin_ ? round : round - 1) << (8 * K);                             \
+      if (!first || fin_) {                                                              \
+        if (act) G = ldcg4(OUT + (size_t)(Q) * nq + lane);                               \
+        n_read++;                                                                        \
+      }                                                                                  \
+    }                                                                                    \
+  }
+        DFX_GATHER(0, q0, g0) DFX_GATHER(1, q1, g1) DFX_GATHER(2, q2, g2) DFX_GATHER(3, q3, g3)
+#undef DFX_GATHER
+        in = and4(and4(in, and4(g0, g1)), and4(g2, g3));
+        if (ndeg > KP) {                                   // rare: more than KP preds
+          const int nrs = __shfl_sync(FULL, rs, j);
+          for (int e = nrs + KP; e < nrs + ndeg; e++) {
+            const int qk = __ldg(p.col + e);
+            int sr = round;
+            if (qk == nn - 1 && have_prev) {
+              in = and4(in, prev);
+            } else {
+              const int c = qk / chunk_nodes;
+              const bool fin = c != chunk && ld_acquire(p.chunk_done + c) == round;
+              sr = fin ? round : round - 1;
+              if (!first || fin) {
+                if (act) in = and4(in, ldcg4(OUT + (size_t)qk * nq + lane));
+                n_read++;
+              }
+            }
+            if (lane == 0) p.seen[e] = (uint8_t)sr;
           }
-          if (need_hin && has_s) hin = and4(hin, ldg4(OH + (size_t)qk * nq + lane));
         }
         uint4 out;
         if (PHASE == 0) {
           out = kern ? andn4(in, pl) : or4(in, pl);
         } else if (kern) {
-          const uint4 x = and4(and4(andn4(pl, b0), smask), hin);   // F & H_in
-          out = or4(in, andn4(pl, x));
+          out = or4(in, andn4(pl, and4(and4(andn4(pl, b0), smask), oh)));
         } else {
           out = andn4(in, pl);
         }
-        int pc = act ? __popc(out.x) + __popc(out.y) + __popc(out.z) + __popc(out.w) : 0;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+        const int pc = (int)__reduce_add_sync(
+            FULL, act ? (unsigned)(__popc(out.x) + __popc(out.y) + __popc(out.z) + __popc(out.w)) : 0u);
         const bool ch = pc != old_pc;
         n_eval++;
         n_read++;
@@ -505,6 +613,7 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
           n_written++;
         }
         if (lane == 0) {
+          p.seen4[nn] = s4;
           if (ch || first) p.popc[nn] = pc;
           if (ch) p.stamp[nn] = round;
           else if (first) p.stamp[nn] = 0;
@@ -515,11 +624,33 @@ mfp_round_v1_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunk
         if (ch && !first) {
           if (j < 31) dm |= (1u << (j + 1)) & vmask;
           else carry = true;
+          if (mark) {   // flag the successors' chunks for the next round
+            const int s0 = __ldg(p.succ_ptr + nn), s1 = __ldg(p.succ_ptr + nn + 1);
+            for (int e = s0 + lane; e < s1; e += 32) fnext[__ldg(p.succ + e) / chunk_nodes] = 1;
+          }
         }
       }
     }
+    // release the chunk: its rows are final for this round
+    __syncwarp();
+    if (lane == 0) st_release(p.chunk_done + chunk, round);
   }
-  round_epilogue(ctl, round, lane, n_changed, n_eval, n_read, n_written);
+  if (lane == 0) {
+    if (n_changed) atomicAdd(&cnt->changed, (unsigned long long)n_changed);
+    if (n_eval) atomicAdd(&cnt->evaluated, (unsigned long long)n_eval);
+    if (n_read) atomicAdd(&cnt->rows_read, (unsigned long long)n_read);
+    if (n_written) atomicAdd(&cnt->rows_written, (unsigned long long)n_written);
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ctl->t_end[round] = t;
+    ctl->rounds = round;
+  }
+  // every thread reads the same final count: a uniform exit
+  if (round > 1 && __ldcg(&cnt->changed) == 0) break;
+  }   // rounds
 }
 
 // ---------------------------------------------------------------------------
@@ -698,7 +829,7 @@ static int launch_round(const CsrDev& p, int vpl, int round, int first, int chun
     per_sm = occ_ > 0 ? occ_ : 1;                                                              \
     K<<<sms * per_sm, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, ctl, fcur, fnext); \
   } while (0)
-  if (vpl == 1) DFX_LAUNCH((mfp_round_v1_kernel<PHASE, 4>));      // V <= 4096 fast path
+  if (vpl == 1) return DFX_E_LIMIT;                  // persistent path (launch_phase)
   else if (vpl == 2) DFX_LAUNCH((mfp_round_kernel<PHASE, 2, 1>));
   else if (vpl == 4) DFX_LAUNCH((mfp_round_kernel<PHASE, 4, 1>));
   else return DFX_E_LIMIT;
@@ -715,18 +846,42 @@ int vpl_for(int words) {
   return -1;
 }
 
-size_t round_ctl_bytes() { return sizeof(RoundCtl); }
+size_t round_ctl_bytes() { return 2 * sizeof(RoundCtl); }
 
 // Both phases to their fixpoints.  Rounds are queued in batches of
 // `kBatch` launches with no host synchronisation in between; a round
 // launched after the phase converged returns immediately.
+// kernel (a), V <= 4096: one persistent cooperative launch per phase runs
+// every round (grid-wide barrier between rounds, uniform exit on a round
+// without changes) -- no host round trips and no launch gaps
+template <int PHASE>
+static int launch_phase(const CsrDev& p, int chunk_nodes, int n_chunks, RoundCtl* ctl,
+                        uint8_t* flags, cudaStream_t st) {
+  static int sms = 0, per_sm = 0;
+  auto* fn = mfp_phase_kernel<PHASE, 4>;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  CsrDev pp = p;
+  int max_rounds = kMaxRounds;
+  void* args[] = {&pp, &chunk_nodes, &n_chunks, &ctl, &flags, &max_rounds};
+  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(sms * per_sm), dim3(256), args, 0, st) !=
+      cudaSuccess)
+    return DFX_E_CUDA;
+  return DFX_OK;
+}
+
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
               SolveStats* stats) {
   const int vpl = vpl_for(p.words);
   if (vpl < 0) return DFX_E_LIMIT;
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
   constexpr int kBatch = 8;
-  RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctl_mem);
+  RoundCtl* ctl2 = reinterpret_cast<RoundCtl*>(ctl_mem);   // [2]: one per phase
   static thread_local cudaEvent_t ev[2 * (kMaxRounds + 1)] = {};
   if (!ev[0])
     for (auto& e : ev) cudaEventCreate(&e);
@@ -735,9 +890,44 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
   stats->rounds[0] = stats->rounds[1] = 0;
   stats->evaluated = stats->rows_read = stats->rows_written = 0;
   stats->kernel_ms = 0.f;
-  static thread_local RoundCtl h;
+  static thread_local RoundCtl h[2];
+  if (cudaMemsetAsync(ctl2, 0, 2 * sizeof(RoundCtl), st) != cudaSuccess) return DFX_E_CUDA;
+  if (vpl == 1) {
+    for (int phase = 0; phase < 2; phase++) {
+      if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
+      if (cudaMemsetAsync(p.chunk_done, 0, sizeof(int) * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
+      cudaEventRecord(ev[2 * phase], st);
+      int rc = phase == 0 ? launch_phase<0>(p, chunk_nodes, n_chunks, ctl2, flags, st)
+                          : launch_phase<1>(p, chunk_nodes, n_chunks, ctl2 + 1, flags, st);
+      if (rc != DFX_OK) return rc;
+      cudaEventRecord(ev[2 * phase + 1], st);
+    }
+    if (cudaMemcpyAsync(h, ctl2, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
+    for (int phase = 0; phase < 2; phase++) {
+      float kms = 0.f;
+      cudaEventElapsedTime(&kms, ev[2 * phase], ev[2 * phase + 1]);
+      stats->kernel_ms += kms;
+      const RoundCtl& c = h[phase];
+      if (c.rounds >= kMaxRounds && c.cnt[c.rounds].changed) return DFX_E_LIMIT;
+      stats->rounds[phase] = c.rounds;
+      for (int r = 1; r <= c.rounds; r++) {
+        stats->evaluated += (int64_t)c.cnt[r].evaluated;
+        stats->rows_read += (int64_t)c.cnt[r].rows_read;
+        stats->rows_written += (int64_t)c.cnt[r].rows_written;
+        if (trace)
+          fprintf(stderr, "dfx-trace phase %d round %d evaluated %llu changed %llu rows_read %llu "
+                  "rows_written %llu round_us %.1f\n", phase, r, c.cnt[r].evaluated,
+                  c.cnt[r].changed, c.cnt[r].rows_read, c.cnt[r].rows_written,
+                  r > 1 ? (c.t_end[r] - c.t_end[r - 1]) / 1e3 : 0.0);
+      }
+    }
+    return DFX_OK;
+  }
+  // V > 4096: one launch per round, queued in batches of kBatch with no host
+  // synchronisation in between; a round launched after convergence returns
   for (int phase = 0; phase < 2; phase++) {
-    if (cudaMemsetAsync(ctl, 0, sizeof(RoundCtl), st) != cudaSuccess) return DFX_E_CUDA;
+    RoundCtl* ctl = ctl2 + phase;
     if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
     int launched = 0;
     for (;;) {
@@ -751,14 +941,15 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
         if (rc != DFX_OK) return rc;
         cudaEventRecord(ev[2 * r + 1], st);
       }
-      if (cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
+      if (cudaMemcpyAsync(&h[phase], ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return DFX_E_CUDA;
       if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
-      if (h.done) break;
+      if (h[phase].done) break;
       if (launched >= kMaxRounds) return DFX_E_LIMIT;
     }
     int rounds = 0;
     for (int r = 1; r <= launched; r++) {
-      const RoundCounters& c = h.cnt[r];
+      const RoundCounters& c = h[phase].cnt[r];
       float kms = 0.f;
       cudaEventElapsedTime(&kms, ev[2 * r], ev[2 * r + 1]);
       stats->kernel_ms += kms;
@@ -769,16 +960,13 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
       stats->evaluated += (int64_t)c.evaluated;
       stats->rows_read += (int64_t)c.rows_read;
       stats->rows_written += (int64_t)c.rows_written;
-      if (!rounds && r > 1 && c.changed == 0 && h.blocks_done[r]) rounds = r;
+      if (!rounds && r > 1 && c.changed == 0 && h[phase].blocks_done[r]) rounds = r;
     }
     stats->rounds[phase] = rounds;
   }
   return DFX_OK;
 }
 
-// kernel (b) and the scan of its per-node counts: offsets[n] = start of node
-// n's output (nonzero masks, or set bits when count_bits); *n_out (host) =
-// total.  The caller synchronises before reading *n_out.
 int requirements_scan(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
                       size_t scratch_bytes, int count_bits, int64_t* n_out, cudaStream_t st) {
   const int vpl = vpl_for(p.words);

@@ -226,7 +226,8 @@ def run_ours(args, rank, world, local):
         for _ in range(args.steps):
             st = prob.solve(args.chunk)
             kernel_ms += st.kernel_ms
-            launches += st.rounds_h + st.rounds_d
+            # V <= 4096: one persistent cooperative launch per phase
+            launches += 2 if cfg.words <= 128 else st.rounds_h + st.rounds_d
             stats_last = {k: getattr(st, k) for k, _ in st._fields_}
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -326,10 +327,11 @@ def run_ours(args, rank, world, local):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "mfp_round_kernel",
+                         "kernel": "mfp_phase_kernel (kernel a, persistent, all rounds of a phase)",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_solve": bytes_per_solve,
-                         "launches_per_solve": rounds,
+                         "launches_per_solve": 2 if cfg.words <= 128 else rounds,
+                         "rounds_per_solve": rounds,
                          "kernel_ms_per_solve": kernel_ms_per_solve,
                          "survey_formula_frac": survey_bytes / (kernel_ms_per_solve / 1e3) / 1e9 / peak},
             "solve": {"rounds_h": stats_last["rounds_h"], "rounds_d": stats_last["rounds_d"],

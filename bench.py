@@ -358,7 +358,7 @@ def run_c4(args, rank, world, local):
     from paper_2406_13881_b200 import _abi
     from paper_2406_13881_b200.batch import (C4Config, ReplayBatch, c4_cost, c4_generate,
                                              c4_shapes, lpt_shards)
-    from paper_2406_13881_b200.dataflow import run_replay
+    from paper_2406_13881_b200.dataflow import ReplaySession, run_replay
 
     torch.cuda.set_device(local)
     eng = _abi.engine(local)
@@ -368,7 +368,12 @@ def run_c4(args, rank, world, local):
     N, V = c4_shapes(cfg)
     shards = lpt_shards(c4_cost(N, V), world)
     mine = shards[rank]
-    batch, facts_mine = c4_generate(cfg, mine)
+    def pinned(shape, dtype):
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        buf = torch.empty(max(1, n), dtype=torch.uint8, pin_memory=True)
+        return buf.numpy()[:n].view(dtype).reshape(shape)
+
+    batch, facts_mine = c4_generate(cfg, mine, alloc=pinned)
     facts_total = int((N.astype(np.int64) * V).sum())
     rb = ReplayBatch(batch, eng=eng)
     for _ in range(max(3, args.warmup)):
@@ -402,10 +407,13 @@ def run_c4(args, rank, world, local):
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         d2h = 0
+        sess = ReplaySession(eng, alloc=pinned, event_cap=rb.cap)
+        sess.run(batch)                                   # warm (allocates)
+        barrier()
+        e0.record(stream)
         for _ in range(args.e2e_steps):
-            raw = run_replay(batch, event_cap=rb.cap)
+            raw = sess.run(batch)
             d2h += raw.events.nbytes + raw.var_out.nbytes
         e1.record(stream)
         torch.cuda.synchronize()
@@ -417,7 +425,8 @@ def run_c4(args, rank, world, local):
         e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
                "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h // args.e2e_steps),
-               "path": "dfx_replay_batch (host buffers): H2D programs, E1 kernel, D2H events"}
+               "path": "dfx_replay_batch (pinned host buffers): H2D programs, E1 kernel, D2H "
+                       "events, pipelined over 8 function ranges (copy / compute / D2H streams)"}
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

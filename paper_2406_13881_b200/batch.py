@@ -68,8 +68,9 @@ def c4_cost(N: np.ndarray, V: np.ndarray) -> np.ndarray:
     return N.astype(np.float64) * np.ceil(V / 32.0)
 
 
-def c4_generate(cfg: C4Config, fids: np.ndarray) -> tuple[PackedBatch, int]:
-    """Generate the listed functions as one packed replay batch."""
+def c4_generate(cfg: C4Config, fids: np.ndarray, alloc=np.zeros) -> tuple[PackedBatch, int]:
+    """Generate the listed functions as one packed replay batch; `alloc(shape,
+    dtype)` lets callers place the arrays in pinned host memory."""
     lib = _lib()
     fids = np.ascontiguousarray(fids, dtype=np.int32)
     ch = np.array(cfg.var_choices, dtype=np.int32)
@@ -81,12 +82,12 @@ def c4_generate(cfg: C4Config, fids: np.ndarray) -> tuple[PackedBatch, int]:
     lib.dfx_gen_c4(*common, None, None, None, None, None, None,
                    C.c_void_p(sizes.ctypes.data), C.byref(facts))
     n_ops, n_vars, n_stmts, n_sites, n_arms = (int(x) for x in sizes)
-    fns = np.zeros(len(fids), dtype=_abi.FN_DESC_DTYPE)
-    ops = np.zeros((n_ops, 4), dtype=np.int32)
-    vf = np.zeros(n_vars, dtype=np.int32)
-    span = np.zeros((n_stmts, 2), dtype=np.int32)
-    sites = np.zeros(max(1, n_sites), dtype=np.int32)
-    arms = np.zeros(max(1, 2 * n_arms), dtype=np.int32)
+    fns = alloc((len(fids),), _abi.FN_DESC_DTYPE)
+    ops = alloc((n_ops, 4), np.int32)
+    vf = alloc((n_vars,), np.int32)
+    span = alloc((n_stmts, 2), np.int32)
+    sites = alloc((max(1, n_sites),), np.int32)
+    arms = alloc((max(1, 2 * n_arms),), np.int32)
     p = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
     lib.dfx_gen_c4(*common, p(fns), p(ops), p(vf), p(span), p(sites), p(arms), None, None)
     return PackedBatch(fns=fns, ops=ops, var_flags=vf, stmt_span=span, sites=sites[:n_sites],

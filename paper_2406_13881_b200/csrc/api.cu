@@ -16,6 +16,19 @@ struct dfx_csr;
 namespace { int csr_destroy_impl(dfx_csr* c); }
 
 struct dfx_handle {
+  static constexpr int kPipe = 8;     // chunks of the pipelined host-buffer calls
+  cudaStream_t s_copy = nullptr, s_d2h = nullptr;
+  cudaEvent_t pev[1 + 2 * kPipe] = {};
+  unsigned long long* pin_cnt = nullptr;   // pinned, kPipe counters
+  cudaError_t pipeline_init() {
+    if (s_copy) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking);
+    for (auto& ev : pev)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&pin_cnt, sizeof(unsigned long long) * kPipe, cudaHostAllocDefault);
+    return e;
+  }
   int device = 0;
   cudaStream_t stream = nullptr;      // the handle's own stream
   cudaStream_t ext_stream = nullptr;  // caller's stream (dfx_set_stream)
@@ -94,6 +107,11 @@ int dfx_close(dfx_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->csr_cache) csr_destroy_impl(h->csr_cache);
+  for (auto& ev : h->pev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->pin_cnt) cudaFreeHost(h->pin_cnt);
+  if (h->s_copy) cudaStreamDestroy(h->s_copy);
+  if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return DFX_OK;
@@ -234,8 +252,9 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   const int nf = in->n_funcs;
   // work items: one warp per (function, 32-variable chunk); at least one per
   // function so statically known errors surface even without variables
-  std::vector<int32_t> item_fn, item_chunk;
+  std::vector<int32_t> item_fn, item_chunk, fn_item0(nf + 1, 0);
   int max_slots = 2;
+  bool ordered = true;   // per-function array ranges ascending and contiguous
   for (int f = 0; f < nf; f++) {
     const dfx_fn_desc& d = in->fns[f];
     if (d.n_slots > 64 || d.max_loop_depth > 24 || d.max_br_depth > 48 || d.max_arms > 192)
@@ -243,6 +262,13 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
                   "branches %d, arms %d)", f, d.n_slots, d.max_loop_depth, d.max_br_depth,
                   d.max_arms);
     if (d.n_slots > max_slots) max_slots = d.n_slots;
+    if (f > 0) {
+      const dfx_fn_desc& e = in->fns[f - 1];
+      ordered &= d.op_off >= e.op_off + e.n_ops && d.var_off >= e.var_off + e.n_vars &&
+                 d.stmt_off >= e.stmt_off + e.n_stmts && d.site_off >= e.site_off &&
+                 d.arm_off >= e.arm_off;
+    }
+    fn_item0[f] = (int32_t)item_fn.size();
     int chunks = (d.n_vars + 31) / 32;
     if (chunks == 0) chunks = 1;
     for (int c = 0; c < chunks; c++) {
@@ -250,30 +276,32 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       item_chunk.push_back(c);
     }
   }
+  fn_item0[nf] = (int32_t)item_fn.size();
   const size_t n_items = item_fn.size();
-  struct Part { const char* name; const void* src; size_t bytes; void** dst; };
-  void *d_fns, *d_ops, *d_vf, *d_span, *d_sites, *d_arms, *d_ifn, *d_ich;
-  Part parts[] = {
-      {"fns", in->fns, sizeof(dfx_fn_desc) * (size_t)nf, &d_fns},
-      {"ops", in->ops, sizeof(int32_t) * 4 * (size_t)in->n_ops, &d_ops},
-      {"vf", in->var_flags, sizeof(int32_t) * (size_t)in->n_vars, &d_vf},
-      {"span", in->stmt_span, sizeof(int32_t) * 2 * (size_t)in->n_stmts, &d_span},
-      {"sites", in->sites, sizeof(int32_t) * (size_t)in->n_sites, &d_sites},
-      {"arms", in->arms, sizeof(int32_t) * 2 * (size_t)in->n_arms, &d_arms},
-      {"ifn", item_fn.data(), sizeof(int32_t) * n_items, &d_ifn},
-      {"ich", item_chunk.data(), sizeof(int32_t) * n_items, &d_ich},
-  };
-  for (auto& p : parts) {
-    *p.dst = dbuf(h, p.name, p.bytes + 16);
-    if (!*p.dst) return fail(DFX_E_CUDA, "cudaMalloc %s (%zu B) failed", p.name, p.bytes);
-    if (p.bytes) CK(cudaMemcpyAsync(*p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, h->st()));
-  }
+  cudaStream_t st = h->st();
+  void* d_fns = dbuf(h, "fns", sizeof(dfx_fn_desc) * (size_t)nf + 16);
+  void* d_ops = dbuf(h, "ops", sizeof(int32_t) * 4 * (size_t)in->n_ops + 16);
+  void* d_vf = dbuf(h, "vf", sizeof(int32_t) * (size_t)in->n_vars + 16);
+  void* d_span = dbuf(h, "span", sizeof(int32_t) * 2 * (size_t)in->n_stmts + 16);
+  void* d_sites = dbuf(h, "sites", sizeof(int32_t) * (size_t)in->n_sites + 16);
+  void* d_arms = dbuf(h, "arms", sizeof(int32_t) * 2 * (size_t)in->n_arms + 16);
+  void* d_ifn = dbuf(h, "ifn", sizeof(int32_t) * n_items + 16);
+  void* d_ich = dbuf(h, "ich", sizeof(int32_t) * n_items + 16);
   const int64_t cap = out->event_cap;
   auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)(cap > 0 ? cap : 1));
   auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
-  if (!d_ev || !d_cnt || !d_vout) return fail(DFX_E_CUDA, "cudaMalloc outputs failed");
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), h->st()));
+  if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
+      !d_cnt || !d_vout)
+    return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
+  CK(h->pipeline_init());
+  // small arrays first, on the compute stream
+  CK(cudaMemcpyAsync(d_fns, in->fns, sizeof(dfx_fn_desc) * (size_t)nf, cudaMemcpyHostToDevice, st));
+  if (n_items) {
+    CK(cudaMemcpyAsync(d_ifn, item_fn.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_ich, item_chunk.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -281,29 +309,80 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   r.stmt_span = (const int32_t*)d_span;
   r.sites = (const int32_t*)d_sites;
   r.arms = (const int32_t*)d_arms;
-  r.item_fn = (const int32_t*)d_ifn;
-  r.item_chunk = (const int32_t*)d_ich;
-  r.n_items = (int)n_items;
   r.max_slots = max_slots;
   r.events = d_ev;
   r.event_cap = cap;
   r.event_count = d_cnt;
   r.var_out = d_vout;
-  CK(cudaEventRecord(h->ev0, h->st()));
-  int rc = dfx::replay_launch(r, h->st());
-  if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-  CK(cudaEventRecord(h->ev1, h->st()));
-  unsigned long long count = 0;
-  CK(cudaMemcpyAsync(&count, d_cnt, sizeof count, cudaMemcpyDeviceToHost, h->st()));
-  CK(cudaStreamSynchronize(h->st()));
-  size_t ncopy = count < (unsigned long long)cap ? (size_t)count : (size_t)cap;
-  if (ncopy)
-    CK(cudaMemcpyAsync(out->events, d_ev, sizeof(dfx_event) * ncopy, cudaMemcpyDeviceToHost,
-                       h->st()));
+  // Pipeline over function ranges: the H2D of chunk k+1 (copy stream), the
+  // replay of chunk k (compute stream) and the D2H of chunk k-1's events
+  // (D2H stream) overlap.  Functions are independent (SURVEY F3 / SPEC), so
+  // chunking changes nothing but the order of events in the buffer.
+  const int K = ordered && nf >= 64 ? dfx_handle::kPipe : 1;
+  std::vector<int> cut(K + 1, nf);
+  {
+    cut[0] = 0;
+    const double per = (double)in->n_ops / K;
+    int f = 0;
+    for (int k = 1; k < K; k++) {
+      while (f < nf && (double)in->fns[f].op_off < per * k) f++;
+      cut[k] = f;
+    }
+  }
+  auto lo = [&](int f, int32_t dfx_fn_desc::*off) -> int64_t { return f < nf ? in->fns[f].*off : -1; };
+  CK(cudaEventRecord(h->pev[0], st));   // fns/items uploaded, counter cleared
+  CK(cudaStreamWaitEvent(h->s_copy, h->pev[0], 0));
+  for (int k = 0; k < K; k++) {
+    const int f0 = cut[k], f1 = cut[k + 1];
+    if (f0 < f1) {
+      struct Rng { const int32_t* src; void* dst; int64_t a, b; int unit; };
+      const int64_t ops_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::op_off);
+      const int64_t ops_b = K == 1 || f1 == nf ? in->n_ops : lo(f1, &dfx_fn_desc::op_off);
+      const int64_t vf_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::var_off);
+      const int64_t vf_b = K == 1 || f1 == nf ? in->n_vars : lo(f1, &dfx_fn_desc::var_off);
+      const int64_t sp_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::stmt_off);
+      const int64_t sp_b = K == 1 || f1 == nf ? in->n_stmts : lo(f1, &dfx_fn_desc::stmt_off);
+      const int64_t si_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::site_off);
+      const int64_t si_b = K == 1 || f1 == nf ? in->n_sites : lo(f1, &dfx_fn_desc::site_off);
+      const int64_t ar_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::arm_off);
+      const int64_t ar_b = K == 1 || f1 == nf ? in->n_arms : lo(f1, &dfx_fn_desc::arm_off);
+      Rng rng[] = {{in->ops, d_ops, ops_a, ops_b, 4}, {in->var_flags, d_vf, vf_a, vf_b, 1},
+                   {in->stmt_span, d_span, sp_a, sp_b, 2}, {in->sites, d_sites, si_a, si_b, 1},
+                   {in->arms, d_arms, ar_a, ar_b, 2}};
+      for (auto& g : rng)
+        if (g.b > g.a)
+          CK(cudaMemcpyAsync((int32_t*)g.dst + g.a * g.unit, g.src + g.a * g.unit,
+                             sizeof(int32_t) * g.unit * (size_t)(g.b - g.a), cudaMemcpyHostToDevice,
+                             h->s_copy));
+    }
+    CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
+    CK(cudaStreamWaitEvent(st, h->pev[1 + k], 0));
+    if (k == 0) CK(cudaEventRecord(h->ev0, st));
+    dfx::ReplayDev rk = r;
+    rk.item_fn = (const int32_t*)d_ifn + fn_item0[f0];
+    rk.item_chunk = (const int32_t*)d_ich + fn_item0[f0];
+    rk.n_items = fn_item0[f1] - fn_item0[f0];
+    int rc = dfx::replay_launch(rk, st);
+    if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (k == K - 1) CK(cudaEventRecord(h->ev1, st));
+    CK(cudaMemcpyAsync(h->pin_cnt + k, d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipe + k], st));
+  }
+  // events of chunk k go back as soon as chunk k's replay is done
+  unsigned long long done = 0;
+  for (int k = 0; k < K; k++) {
+    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipe + k]));
+    unsigned long long end = h->pin_cnt[k];
+    if (end > (unsigned long long)cap) end = (unsigned long long)(cap > 0 ? cap : 0);
+    if (end > done)
+      CK(cudaMemcpyAsync(out->events + done, d_ev + done, sizeof(dfx_event) * (size_t)(end - done),
+                         cudaMemcpyDeviceToHost, h->s_d2h));
+    done = end > done ? end : done;
+  }
+  const unsigned long long count = h->pin_cnt[K - 1];
   if (in->n_vars)
-    CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost,
-                       h->st()));
-  CK(cudaStreamSynchronize(h->st()));
+    CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost, h->s_d2h));
+  CK(cudaStreamSynchronize(h->s_d2h));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   out->kernel_ms = ms;

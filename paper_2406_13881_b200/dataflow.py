@@ -137,6 +137,41 @@ def run_replay(batch: PackedBatch, runner=None, event_cap: int | None = None) ->
                          kernel_ms=float(rout.kernel_ms))
 
 
+class ReplaySession:
+    """Reference-facing host-buffer path of E1 (`dfx_replay_batch`) with
+    output buffers reused across calls (optionally pinned, so the library's
+    chunked H2D / replay / D2H pipeline overlaps).  Results are views into
+    the session's buffers, valid until the next call."""
+
+    def __init__(self, eng: _abi.Engine | None = None, alloc=np.empty, event_cap: int = 0):
+        self.eng = eng or _abi.engine()
+        self.alloc = alloc
+        self.cap = event_cap
+        self._ev = None
+        self._vout = None
+
+    def run(self, batch: PackedBatch) -> RawResult:
+        if self.cap <= 0:
+            self.cap = max(1024, 4 * int(batch.ops.shape[0]) // 10)
+        while True:
+            if self._ev is None or self._ev.shape[0] < self.cap:
+                self._ev = self.alloc((self.cap,), _abi.EVENT_DTYPE)
+            if self._vout is None or self._vout.shape[0] < max(1, batch.n_vars):
+                self._vout = self.alloc((max(1, batch.n_vars),), np.uint8)
+            rin = batch.replay_in()
+            rout = _abi.ReplayOut()
+            rout.events = _abi.ptr(self._ev)
+            rout.event_cap = self._ev.shape[0]
+            rout.var_out = _abi.ptr(self._vout)
+            rc = self.eng.lib.dfx_replay_batch(self.eng.h, C.byref(rin), C.byref(rout))
+            if rc == _abi.DFX_E_NOSPC:
+                self.cap = int(rout.n_events) + 16
+                continue
+            self.eng.check(rc, "dfx_replay_batch")
+            return RawResult(events=self._ev[:rout.n_events], var_out=self._vout[:batch.n_vars],
+                             kernel_ms=float(rout.kernel_ms))
+
+
 # ---- decoding --------------------------------------------------------------
 
 def _raise_error(prog: FnProgram, src, ev) -> None:

@@ -180,24 +180,34 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 
   // op window: lane i holds op (wbase + i); an op is fetched by shuffles
   // instead of a dependent global load per op
+  // `rel` marks the window's ops this warp must execute: an access op on a
+  // variable outside this warp's 32-variable chunk only advances the visit
+  // counter, so runs of them are skipped in one step (uniform across the warp)
   int wbase = -64;
   int4 wop = make_int4(0, 0, 0, 0);
+  unsigned rel = 0u;
   for (;;) {
     if (pc < wbase || pc >= wbase + 32) {
       wbase = pc;
-      if (wbase + lane < d.n_ops) wop = __ldg(fops + wbase + lane);
+      bool r = true;
+      if (wbase + lane < d.n_ops) {
+        wop = __ldg(fops + wbase + lane);
+        r = !((unsigned)((wop.x & 0xFF) - DFX_OP_HR) <= (unsigned)(DFX_OP_DW - DFX_OP_HR) &&
+              (wop.y >> 5) != chunk);
+      }
+      rel = __ballot_sync(0xFFFFFFFFu, r);
     }
-    const int src = pc - wbase;
-    const int opx = __shfl_sync(0xFFFFFFFFu, wop.x, src), opy = __shfl_sync(0xFFFFFFFFu, wop.y, src);
-    // fast path: an access op on a variable outside this warp's 32-variable
-    // chunk only advances the visit counter (uniform across the warp)
-    if ((unsigned)((opx & 0xFF) - DFX_OP_HR) <= (unsigned)(DFX_OP_DW - DFX_OP_HR) && (opy >> 5) != chunk) {
-      seq++;
-      pc++;
+    const unsigned m = rel & (0xFFFFFFFFu << (pc - wbase));
+    if (!m) {                       // the rest of the window is foreign accesses
+      seq += (uint64_t)(wbase + 32 - pc);
+      pc = wbase + 32;
       continue;
     }
-    const int4 op = make_int4(opx, opy, __shfl_sync(0xFFFFFFFFu, wop.z, src),
-                              __shfl_sync(0xFFFFFFFFu, wop.w, src));
+    const int src = __ffs(m) - 1;
+    seq += (uint64_t)(wbase + src - pc);
+    pc = wbase + src;
+    const int4 op = make_int4(__shfl_sync(0xFFFFFFFFu, wop.x, src), __shfl_sync(0xFFFFFFFFu, wop.y, src),
+                              __shfl_sync(0xFFFFFFFFu, wop.z, src), __shfl_sync(0xFFFFFFFFu, wop.w, src));
     const int code = op.x & 0xFF, fl = op.x;
     seq++;
     const uint64_t key = seq << 24;

@@ -34,6 +34,7 @@ struct BrFrame { int16_t saved, arm_base, narms, pad; };
 struct LoopFrame { int32_t stmt, body_pc, loop_start; int16_t slot; int8_t round, may_skip, rec_saved, pad[3]; };
 
 struct WarpCtl {
+  unsigned long long live;   // bit i: ref[i] > 0
   uint8_t ref[kMaxSlots];
   BrFrame br[kMaxBr];
   uint8_t armstk[kMaxArmStk];
@@ -45,11 +46,18 @@ struct WarpCtl {
 __device__ __forceinline__ int st_start(const int32_t* span, int s) { return __ldg(span + 2 * s); }
 __device__ __forceinline__ int st_end(const int32_t* span, int s) { return __ldg(span + 2 * s + 1); }
 
+// first free slot from the live mask (lane 0 only)
 __device__ __forceinline__ int alloc_slot(WarpCtl& c, int nslots) {
-  for (int i = 0; i < nslots; i++)
-    if (c.ref[i] == 0) { c.ref[i] = 1; return i; }
-  c.fault = 1;
-  return 0;
+  const unsigned long long avail = ~c.live & (nslots >= 64 ? ~0ull : ((1ull << nslots) - 1ull));
+  if (!avail) { c.fault = 1; return 0; }
+  const int i = __ffsll((long long)avail) - 1;
+  c.ref[i] = 1;
+  c.live |= 1ull << i;
+  return i;
+}
+__device__ __forceinline__ void ref_inc(WarpCtl& c, int i) { c.ref[i]++; }
+__device__ __forceinline__ void ref_dec(WarpCtl& c, int i) {
+  if (--c.ref[i] == 0) c.live &= ~(1ull << i);
 }
 
 __device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, int64_t cap,
@@ -86,19 +94,24 @@ __device__ __forceinline__ int hoist(const int32_t* t, int loc_lim) {
   return acc;
 }
 
+template <class M>
 struct Lane {
-  uint64_t H, D;
+  M H, D;
   uint32_t skipH, skipD;
   int presence, to_comp, from_comp;
   int halted;
 };
 
-__device__ __forceinline__ int getb(uint64_t m, int s) { return (int)((m >> s) & 1ull); }
-__device__ __forceinline__ uint64_t setb(uint64_t m, int s, int v) {
-  return v ? (m | (1ull << s)) : (m & ~(1ull << s));
+template <class M>
+__device__ __forceinline__ int getb(M m, int s) { return (int)((m >> s) & (M)1); }
+template <class M>
+__device__ __forceinline__ M setb(M m, int s, int v) {   // branch-free bit assignment
+  const M bit = (M)1 << s;
+  return m ^ ((((M)0 - (M)v) ^ m) & bit);
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+template <class M>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
               const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
@@ -135,6 +148,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 
   if (lane == 0) {
     for (int i = 0; i < kMaxSlots; i++) c.ref[i] = 0;
+    c.live = 0ull;
     c.nbr = c.narm = c.nlp = 0;
     c.record = 1;
     c.fault = 0;
@@ -143,8 +157,8 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   for (int s = 0; s < slots_per_warp; s++) prov[s * 32 + lane] = 0xFFFFFFFFu;
   __syncwarp();
 
-  Lane L;
-  L.H = ~0ull; L.D = 0ull;
+  Lane<M> L;
+  L.H = ~(M)0; L.D = (M)0;
   L.skipH = L.skipD = 0u;
   L.presence = L.to_comp = L.from_comp = 0;
   L.halted = !active;
@@ -297,7 +311,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           if (c.nbr >= kMaxBr) c.fault = 1;
           else {
             BrFrame& b = c.br[c.nbr++];
-            b.saved = (int16_t)cur; c.ref[cur]++;
+            b.saved = (int16_t)cur; ref_inc(c, cur);
             b.arm_base = (int16_t)c.narm; b.narms = 0;
           }
         }
@@ -312,8 +326,8 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           if (c.narm >= kMaxArmStk) c.fault = 1;
           c.bc0 = s; c.bc1 = b.saved;
           if (code == DFX_OP_ARM_FORK) {
-            c.ref[cur]--; c.cur = s;
-            if (fl & DFX_F_CAPTURE) { c.armstk[c.narm++] = (uint8_t)s; c.ref[s]++; b.narms++; }
+            ref_dec(c, cur); c.cur = s;
+            if (fl & DFX_F_CAPTURE) { c.armstk[c.narm++] = (uint8_t)s; ref_inc(c, s); b.narms++; }
           } else {
             c.armstk[c.narm++] = (uint8_t)s; b.narms++;
           }
@@ -329,7 +343,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         if (lane == 0) {
           BrFrame& b = c.br[c.nbr - 1];
           if (c.narm >= kMaxArmStk) c.fault = 1;
-          else { c.armstk[c.narm++] = (uint8_t)cur; c.ref[cur]++; b.narms++; }
+          else { c.armstk[c.narm++] = (uint8_t)cur; ref_inc(c, cur); b.narms++; }
         }
         __syncwarp();
         break;
@@ -368,9 +382,9 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         __syncwarp();
         if (lane == 0) {
           int m = arm[0];
-          c.ref[m]++; c.ref[cur]--; c.cur = m;
-          for (int i = 0; i < n; i++) c.ref[arm[i]]--;
-          c.ref[b.saved]--;
+          ref_inc(c, m); ref_dec(c, cur); c.cur = m;
+          for (int i = 0; i < n; i++) ref_dec(c, arm[i]);
+          ref_dec(c, b.saved);
           c.narm = b.arm_base;
           c.nbr--;
         }
@@ -403,7 +417,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           merge_conj(cur, f.slot);
           __syncwarp();
           if (lane == 0) {
-            c.ref[f.slot]--;
+            ref_dec(c, f.slot);
             f.slot = (int16_t)alloc_slot(c, nslots);
             f.round = 1;
           }
@@ -424,7 +438,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         }
         L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
         __syncwarp();
-        if (lane == 0) { c.ref[f.slot]--; c.nlp--; }
+        if (lane == 0) { ref_dec(c, f.slot); c.nlp--; }
         __syncwarp();
         break;
       }
@@ -436,7 +450,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       default:
         goto fault;
     }
-    if (c.fault) goto fault;
+    if (code >= DFX_OP_BR_BEGIN && c.fault) goto fault;   // access ops never fault
     pc++;
   }
   if (active) {
@@ -463,10 +477,19 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream) {
   size_t smem = (size_t)kWarpsPerBlock * slots * 32 * sizeof(uint32_t);
   int blocks = (r.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks == 0) return DFX_OK;
-  cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  replay_kernel<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
-      r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
-      r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
+  // slot bitmasks in 32-bit registers when every function of the batch needs
+  // at most 32 live state slots (all of C4), else 64-bit
+  if (slots <= 32) {
+    cudaFuncSetAttribute(replay_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    replay_kernel<uint32_t><<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
+        r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
+        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
+  } else {
+    cudaFuncSetAttribute(replay_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    replay_kernel<uint64_t><<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
+        r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
+        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
+  }
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 

@@ -943,59 +943,87 @@ int dfx_cg_wave(dfx_handle* h, dfx_cg* c, const dfx_cg_tables* prev, dfx_cg_tabl
 // replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
 int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");
-  dfx_cg* c = nullptr;
-  int rc = dfx_cg_create(h, in, &c);
-  if (rc) return rc;
+  if (in->n_funcs < 0 || in->n_slots < 0 || in->n_waves < 0)
+    return fail(DFX_E_ARG, "dfx_summaries: negative size");
+  CK(cudaSetDevice(h->device));
   cudaStream_t st = h->st();
-  const int nf = in->n_funcs, ns = in->n_slots, nsp = c->g.nsp;
-  auto ibits = pad_rows(in->init_bits, nf, ns, nsp);
-  auto ilist = pad_rows(in->init_list, nf, ns, nsp);
-  dfx_cg_tables t[2];
-  for (int k = 0; k < 2; k++) {
-    t[k].bits = (uint8_t*)cg_alloc(c, ibits.size());
-    t[k].list = (int16_t*)cg_alloc(c, sizeof(int16_t) * ilist.size());
-    t[k].len = (int32_t*)cg_alloc(c, sizeof(int32_t) * nf);
-    if (!t[k].bits || !t[k].list || !t[k].len) { cg_destroy_impl(c); return fail(DFX_E_CUDA, "dfx_summaries: allocation failed"); }
+  const int nf = in->n_funcs, ns = in->n_slots;
+  const int nsp = ((ns + 31) / 32) * 32;                 // padded row (16-B quads, 32-bit seen words)
+  const int maxp = in->max_passes > 0 ? in->max_passes : 1;
+  const size_t rows = (size_t)(nf > 0 ? nf : 1);
+  // device arrays: grow-only handle buffers, no per-call allocation
+  auto* d_direct = (uint8_t*)dbuf(h, "cg_direct", rows * nsp + 16);
+  auto* d_srcoff = (int32_t*)dbuf(h, "cg_srcoff", sizeof(int32_t) * (rows + 1));
+  auto* d_src = (int32_t*)dbuf(h, "cg_src", sizeof(int32_t) * 4 * (size_t)(in->n_src + 1));
+  auto* d_slist = (int16_t*)dbuf(h, "cg_slist", sizeof(int16_t) * (size_t)(in->n_slist + 1));
+  auto* d_bind = (int32_t*)dbuf(h, "cg_bind", sizeof(int32_t) * 2 * (size_t)(in->n_bind + 1));
+  auto* d_wfns = (int32_t*)dbuf(h, "cg_wfns", sizeof(int32_t) * rows);
+  auto* d_woff = (int32_t*)dbuf(h, "cg_woff", sizeof(int32_t) * (size_t)(in->n_waves + 1));
+  auto* d_flags = (int*)dbuf(h, "cg_flags", sizeof(int) * (size_t)(maxp + 2));
+  uint8_t* tb[2] = {(uint8_t*)dbuf(h, "cg_b0", rows * nsp + 16), (uint8_t*)dbuf(h, "cg_b1", rows * nsp + 16)};
+  int16_t* tl[2] = {(int16_t*)dbuf(h, "cg_l0", sizeof(int16_t) * rows * nsp + 16),
+                    (int16_t*)dbuf(h, "cg_l1", sizeof(int16_t) * rows * nsp + 16)};
+  int32_t* tn[2] = {(int32_t*)dbuf(h, "cg_n0", sizeof(int32_t) * rows), (int32_t*)dbuf(h, "cg_n1", sizeof(int32_t) * rows)};
+  if (!d_direct || !d_srcoff || !d_src || !d_slist || !d_bind || !d_wfns || !d_woff || !d_flags ||
+      !tb[0] || !tb[1] || !tl[0] || !tl[1] || !tn[0] || !tn[1])
+    return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
+  // dense rows go up contiguously into a staging buffer and are re-pitched
+  // to the padded layout on the device (one DMA per array)
+  auto* d_stage = (uint8_t*)dbuf(h, "cg_stage", sizeof(int16_t) * rows * nsp + 16);
+  if (!d_stage) return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
+  if (nf && ns) {
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = 0;
+    CK(cudaMemcpyAsync(d_stage, in->direct, nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(d_stage, ns, d_direct, nsp, ns, nf, st);
+    CK(cudaMemcpyAsync(d_stage, in->init_bits, nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(d_stage, ns, tb[0], nsp, ns, nf, st);
+    CK(cudaMemcpyAsync(d_stage, in->init_list, 2 * nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(d_stage, 2 * (size_t)ns, tl[0], 2 * (size_t)nsp, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(DFX_E_CUDA, "dfx_summaries: repitch failed");
   }
-  CK(cudaMemcpyAsync(t[0].bits, ibits.data(), ibits.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(t[0].list, ilist.data(), sizeof(int16_t) * ilist.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(t[0].len, in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
-  int prev = 0, passes = 0, launches = 0;
+  if (nf) CK(cudaMemcpyAsync(tn[0], in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_srcoff, in->src_off, sizeof(int32_t) * (size_t)(nf + 1), cudaMemcpyHostToDevice, st));
+  if (in->n_src) CK(cudaMemcpyAsync(d_src, in->src, sizeof(int32_t) * 4 * (size_t)in->n_src, cudaMemcpyHostToDevice, st));
+  if (in->n_slist) CK(cudaMemcpyAsync(d_slist, in->slist, sizeof(int16_t) * (size_t)in->n_slist, cudaMemcpyHostToDevice, st));
+  if (in->n_bind) CK(cudaMemcpyAsync(d_bind, in->bind, sizeof(int32_t) * 2 * (size_t)in->n_bind, cudaMemcpyHostToDevice, st));
+  if (nf) CK(cudaMemcpyAsync(d_wfns, in->wave_fns, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_woff, in->wave_off, sizeof(int32_t) * (size_t)(in->n_waves + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_flags, 0, sizeof(int) * (size_t)(maxp + 2), st));
+  dfx::CgDev g{};
+  g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = in->n_waves;
+  g.direct = d_direct; g.src_off = d_srcoff; g.src = d_src; g.slist = d_slist; g.bind = d_bind;
+  g.wave_fns = d_wfns;
+  g.h_wave_off = in->wave_off;
+  // all passes in one persistent cooperative launch (waves separated by grid
+  // barriers); passes alternate tables t0 -> t1 -> t0 ...
   CK(cudaEventRecord(h->ev0, st));
-  while (passes < in->max_passes) {
-    passes++;
-    const int cur = prev ^ 1;
-    CK(cudaMemsetAsync(c->d_changed, 0, sizeof(int), st));
-    for (int w = 0; w < c->g.n_waves && rc == DFX_OK; w++) {
-      rc = dfx::cg_wave(c->g, t[prev].bits, t[prev].list, t[prev].len, t[cur].bits, t[cur].list,
-                        t[cur].len, w, 0, 1, c->d_changed, st);
-      launches++;
-    }
-    if (rc) break;
-    int changed = 0;
-    CK(cudaMemcpyAsync(&changed, c->d_changed, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    prev = cur;
-    if (!changed) break;
-  }
+  int rc = dfx::cg_solve(g, tb[0], tl[0], tn[0], tb[1], tl[1], tn[1], d_woff, maxp, d_flags,
+                         d_flags + maxp + 1, st);
   CK(cudaEventRecord(h->ev1, st));
-  if (rc) { cg_destroy_impl(c); return fail(rc, "cg_wave failed: %s", cudaGetErrorString(cudaGetLastError())); }
-  std::vector<uint8_t> hb((size_t)nf * nsp);
-  std::vector<int16_t> hl((size_t)nf * nsp);
-  CK(cudaMemcpyAsync(hb.data(), t[prev].bits, hb.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hl.data(), t[prev].list, sizeof(int16_t) * hl.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(out->len, t[prev].len, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  if (rc) return fail(rc, "cg_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
+  int passes = 0;
+  CK(cudaMemcpyAsync(&passes, d_flags + maxp + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  for (int f = 0; f < nf; f++) {
-    std::memcpy(out->bits + (size_t)f * ns, &hb[(size_t)f * nsp], ns);
-    std::memcpy(out->list + (size_t)f * ns, &hl[(size_t)f * nsp], sizeof(int16_t) * ns);
+  const int last = passes & 1;          // the table the last pass wrote
+  if (nf && ns) {   // re-pitch to dense rows on the device, one DMA per array
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = dfx::repitch(tb[last], nsp, d_stage, ns, ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
+    CK(cudaMemcpyAsync(out->bits, d_stage, nb, cudaMemcpyDeviceToHost, st));
+    auto* d_stage2 = (uint8_t*)dbuf(h, "cg_stage2", sizeof(int16_t) * rows * nsp + 16);
+    if (!d_stage2) return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
+    rc0 = dfx::repitch(tl[last], 2 * (size_t)nsp, d_stage2, 2 * (size_t)ns, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
+    CK(cudaMemcpyAsync(out->list, d_stage2, 2 * nb, cudaMemcpyDeviceToHost, st));
   }
+  if (nf) CK(cudaMemcpyAsync(out->len, tn[last], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   out->kernel_ms = ms;
   out->passes = passes;
-  out->launches = launches;
-  cg_destroy_impl(c);
+  out->launches = 1;
   return DFX_OK;
 }
 

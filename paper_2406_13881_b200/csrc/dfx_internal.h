@@ -106,5 +106,10 @@ struct CgDev {
 int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8_t* cbits,
             int16_t* clist, int32_t* clen, int wave, int shard, int nshards, int* d_changed,
             cudaStream_t st);
+int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size_t rows,
+            cudaStream_t st);
+int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
+             int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
+             int* d_passes, cudaStream_t st);
 
 }  // namespace dfx

@@ -18,6 +18,7 @@
 
 #include "../../include/dfx.h"
 #include "dfx_internal.h"
+#include <cooperative_groups.h>
 
 namespace dfx {
 
@@ -36,20 +37,14 @@ struct CgBuf {
   int32_t* len;      // [nf]
 };
 
-__global__ void __launch_bounds__(kCgWarps * 32)
-cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int nshards,
-               int* __restrict__ changed) {
-  extern __shared__ uint32_t seen_all[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Rebuild function f's summary (bits + insertion order) into `cur`; returns
+// (warp-uniform) whether its bit set differs from `prev`.
+__device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, const CgBuf& cur,
+                                            int f, uint32_t* seen, int lane) {
   const int sw = g.nsp >> 5;                       // seen words per warp
-  uint32_t* seen = seen_all + warp * sw;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
   const int nq = g.nsp >> 4;
   const int P = g.n_params;
-  int any = 0;
-  for (int pos = lo + shard + nshards * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); pos < hi;
-       pos += nshards * warps) {
-    const int f = __ldg(g.wave_fns + pos);
+  {
     const int s0 = __ldg(g.src_off + f), s1 = __ldg(g.src_off + f + 1);
     // ---- bits: direct | OR of transformed callee rows ----------------------
     bool ch = false;
@@ -82,7 +77,7 @@ cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int ns
       ch |= (old.x != acc.x) | (old.y != acc.y) | (old.z != acc.z) | (old.w != acc.w);
       __stcg(reinterpret_cast<uint4*>(cur.bits + (size_t)f * g.nsp) + q, acc);
     }
-    any |= __any_sync(FULLM, ch);
+    const bool any = __any_sync(FULLM, ch);
     // ---- insertion order ------------------------------------------------------
     for (int w = lane; w < sw; w += 32) seen[w] = 0u;
     __syncwarp();
@@ -133,8 +128,53 @@ cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int ns
       }
     }
     if (lane == 0) __stcg(cur.len + f, len);
+    return any;
   }
+}
+
+__global__ void __launch_bounds__(kCgWarps * 32)
+cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int nshards,
+               int* __restrict__ changed) {
+  extern __shared__ uint32_t seen_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  bool any = false;
+  for (int pos = lo + shard + nshards * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); pos < hi;
+       pos += nshards * warps)
+    any |= cg_function(g, prev, cur, __ldg(g.wave_fns + pos), seen, lane);
   if (any && lane == 0) atomicOr(changed, 1);
+}
+
+// All passes in one persistent cooperative launch: waves are separated by
+// grid-wide barriers, passes alternate the two tables, and the kernel exits
+// uniformly after the first pass that changed no bit set.  changed[p] is the
+// flag of pass p (zeroed by the host); *passes_out = passes run.
+__global__ void __launch_bounds__(kCgWarps * 32)
+cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, int max_passes,
+                int* __restrict__ changed, int* __restrict__ passes_out) {
+  namespace cgr = cooperative_groups;
+  cgr::grid_group grid = cgr::this_grid();
+  extern __shared__ uint32_t seen_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int pass = 1; pass <= max_passes; pass++) {
+    const CgBuf& prev = (pass & 1) ? t0 : t1;
+    const CgBuf& cur = (pass & 1) ? t1 : t0;
+    bool any = false;
+    for (int w = 0; w < g.n_waves; w++) {
+      const int lo = __ldg(wave_off + w), hi = __ldg(wave_off + w + 1);
+      for (int pos = lo + gw; pos < hi; pos += warps)
+        any |= cg_function(g, prev, cur, __ldg(g.wave_fns + pos), seen, lane);
+      grid.sync();
+    }
+    if (any && lane == 0) atomicOr(changed + pass, 1);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *passes_out = pass;
+    if (!__ldcg(changed + pass)) break;
+  }
 }
 
 int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8_t* cbits,
@@ -150,6 +190,61 @@ int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8
   cg_wave_kernel<<<blocks, kCgWarps * 32, smem, st>>>(g, prev, cur, lo, hi, shard, nshards,
                                                       d_changed);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+// row re-pitching between the ABI's dense [rows][n] layout and the kernels'
+// padded [rows][np] layout (elements of `es` bytes; padding zero-filled)
+__global__ void repitch_kernel(const uint8_t* __restrict__ src, size_t sp, uint8_t* __restrict__ dst,
+                               size_t dp, size_t width, size_t rows) {
+  const size_t total = rows * dp;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / dp, c = i - r * dp;
+    dst[i] = c < width ? src[r * sp + c] : (uint8_t)0;
+  }
+}
+
+int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size_t rows,
+            cudaStream_t st) {
+  if (!rows || !dp) return DFX_OK;
+  size_t g = (rows * dp + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  repitch_kernel<<<(int)g, 256, 0, st>>>((const uint8_t*)src, sp, (uint8_t*)dst, dp, width, rows);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+// whole solve on the device; returns the passes run through *passes (device)
+int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
+             int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
+             int* d_passes, cudaStream_t st) {
+  static int sms = 0, per_sm = 0;
+  const size_t smem = (size_t)kCgWarps * (g.nsp / 32) * sizeof(uint32_t);
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static size_t last_smem = (size_t)-1;
+  if (smem != last_smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_solve_kernel, kCgWarps * 32, smem);
+    last_smem = smem;
+  }
+  if (per_sm < 1) return DFX_E_LIMIT;
+  int max_wave = 0;
+  for (int w = 0; w < g.n_waves; w++) {
+    const int n = g.h_wave_off[w + 1] - g.h_wave_off[w];
+    if (n > max_wave) max_wave = n;
+  }
+  int blocks = (max_wave + kCgWarps - 1) / kCgWarps;
+  if (blocks > sms * per_sm) blocks = sms * per_sm;
+  if (blocks < 1) blocks = 1;
+  CgDev gg = g;
+  CgBuf t0{b0, l0, n0}, t1{b1, l1, n1};
+  void* args[] = {&gg, &t0, &t1, &d_wave_off, &max_passes, &d_changed, &d_passes};
+  if (cudaLaunchCooperativeKernel((const void*)cg_solve_kernel, dim3(blocks), dim3(kCgWarps * 32),
+                                  args, smem, st) != cudaSuccess)
+    return DFX_E_CUDA;
+  return DFX_OK;
 }
 
 }  // namespace dfx

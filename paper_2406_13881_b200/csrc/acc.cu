@@ -43,7 +43,7 @@ __device__ __forceinline__ int warp_exclusive_scan(int v, int lane, int* total) 
 // One warp per node: OR the node's access entries into two shared-memory
 // rows (reads, writes), then store USE = R, B = W, A = R | W coalesced.
 __global__ void __launch_bounds__(kWarps * 32)
-expand_acc_kernel(int64_t n_nodes, int words, const int64_t* __restrict__ off,
+expand_acc_kernel(int64_t n_lo, int64_t n_nodes, int words, const int64_t* __restrict__ off,
                   const uint16_t* __restrict__ acc, uint32_t* __restrict__ A,
                   uint32_t* __restrict__ B, uint32_t* __restrict__ USE, int* bad) {
   extern __shared__ uint32_t sm[];
@@ -52,7 +52,7 @@ expand_acc_kernel(int64_t n_nodes, int words, const int64_t* __restrict__ off,
   uint32_t* w = r + words;
   const int nvars = words * 32;
   const int64_t wstride = (int64_t)gridDim.x * kWarps;
-  for (int64_t n = (int64_t)blockIdx.x * kWarps + warp; n < n_nodes; n += wstride) {
+  for (int64_t n = n_lo + (int64_t)blockIdx.x * kWarps + warp; n < n_nodes; n += wstride) {
     for (int i = lane; i < words; i += 32) r[i] = w[i] = 0u;
     __syncwarp();
     const int64_t e1 = off[n + 1];
@@ -126,13 +126,13 @@ export_acc_kernel(int64_t n_nodes, int words, const uint32_t* __restrict__ R,
 // per-node variable lists at offsets[n]: requirement vars ascending, then
 // firstprivate vars ascending with DFX_REQ_FIRSTPRIVATE set.
 __global__ void __launch_bounds__(kWarps * 32)
-compact_list_kernel(int64_t n_nodes, int words, const uint32_t* __restrict__ REQ,
+compact_list_kernel(int64_t n_lo, int64_t n_hi, int words, const uint32_t* __restrict__ REQ,
                     const uint32_t* __restrict__ FPQ, const int32_t* __restrict__ fp_slot,
                     int n_fp_slots, const int64_t* __restrict__ offsets,
                     uint16_t* __restrict__ vars, int64_t cap) {
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * kWarps;
-  for (int64_t n = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_nodes; n += wstride) {
+  for (int64_t n = n_lo + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_hi; n += wstride) {
     int64_t base = offsets[n];
     for (int pass = 0; pass < 2; pass++) {
       for (int i0 = 0; i0 < words; i0 += 32) {
@@ -167,15 +167,17 @@ static int grid_nodes(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
-int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, cudaStream_t st) {
+int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, int64_t n_lo,
+               int64_t n_hi, cudaStream_t st) {
+  if (n_hi <= n_lo) return DFX_OK;
   const size_t smem = (size_t)kWarps * 2 * p.words * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(expand_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr = true;
   }
-  expand_acc_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, smem, st>>>(p.n_nodes, p.words, off, acc,
-                                                                      p.A, p.B, p.USE, bad);
+  expand_acc_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, smem, st>>>(n_lo, n_hi, p.words, off,
+                                                                         acc, p.A, p.B, p.USE, bad);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
@@ -191,9 +193,10 @@ int export_acc(const CsrDev& p, const int64_t* off, uint16_t* acc, cudaStream_t 
 }
 
 int compact_list(const CsrDev& p, const int64_t* offsets, uint16_t* vars, int64_t cap,
-                 cudaStream_t st) {
-  compact_list_kernel<<<grid_nodes(p.n_nodes), kWarps * 32, 0, st>>>(
-      p.n_nodes, p.words, p.REQ, p.FPQ, p.fp_slot, p.n_fp_slots, offsets, vars, cap);
+                 int64_t n_lo, int64_t n_hi, cudaStream_t st) {
+  if (n_hi <= n_lo) return DFX_OK;
+  compact_list_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, 0, st>>>(
+      n_lo, n_hi, p.words, p.REQ, p.FPQ, p.fp_slot, p.n_fp_slots, offsets, vars, cap);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 

@@ -713,22 +713,42 @@ int check_acc_in(const dfx_acc_in* in) {
 }
 
 // H2D of CSR + access lists into already-allocated buffers, then expand the
-// lists into the A/B/USE planes and build the node descriptors
+// lists into the A/B/USE planes and build the node descriptors.  The access
+// lists go up in node ranges on the copy stream, each range expanded on the
+// compute stream as soon as it lands; descriptors and the successor CSR are
+// built meanwhile.  The validation flag is read back by check_bad().
 int csr_upload_acc(dfx_handle* h, dfx_csr* c, const dfx_acc_in* in, cudaStream_t st) {
   dfx::CsrDev& p = c->p;
   auto* d_off = (int64_t*)dbuf(h, "acc_off", sizeof(int64_t) * (size_t)(in->n_nodes + 1));
   auto* d_acc = (uint16_t*)dbuf(h, "acc", sizeof(uint16_t) * (size_t)(in->n_acc > 0 ? in->n_acc : 1));
   if (!d_off || !d_acc) return fail(DFX_E_CUDA, "access-list buffers: allocation failed");
+  CK(h->pipeline_init());
   CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
   if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_off, in->acc_off, sizeof(int64_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
-  if (in->n_acc) CK(cudaMemcpyAsync(d_acc, in->acc, sizeof(uint16_t) * in->n_acc, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
+  CK(cudaEventRecord(h->pev[0], st));
   int rc = dfx::build_desc(p, st);
   if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
-  if (!rc) rc = dfx::expand_acc(p, d_off, d_acc, c->d_bad, st);
-  if (rc) return fail(rc, "expand_acc/build_desc launch failed");
+  if (rc) return fail(rc, "build_desc/build_succ launch failed");
+  CK(cudaStreamWaitEvent(h->s_copy, h->pev[0], 0));   // buffers free of the previous call
+  const int K = in->n_nodes >= 4096 ? dfx_handle::kPipe : 1;
+  for (int k = 0; k < K; k++) {
+    const int64_t lo = in->n_nodes * k / K, hi = in->n_nodes * (k + 1) / K;
+    const int64_t a = in->acc_off[lo], b = in->acc_off[hi];
+    CK(cudaMemcpyAsync(d_off + lo, in->acc_off + lo, sizeof(int64_t) * (size_t)(hi - lo + 1),
+                       cudaMemcpyHostToDevice, h->s_copy));
+    if (b > a) CK(cudaMemcpyAsync(d_acc + a, in->acc + a, sizeof(uint16_t) * (size_t)(b - a),
+                                  cudaMemcpyHostToDevice, h->s_copy));
+    CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
+    CK(cudaStreamWaitEvent(st, h->pev[1 + k], 0));
+    rc = dfx::expand_acc(p, d_off, d_acc, c->d_bad, lo, hi, st);
+    if (rc) return fail(rc, "expand_acc launch failed");
+  }
+  return DFX_OK;
+}
+
+int check_bad(dfx_csr* c, const dfx_acc_in* in, cudaStream_t st) {
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -747,6 +767,7 @@ int dfx_csr_create_acc(dfx_handle* h, const dfx_acc_in* in, dfx_csr** out) {
   auto* c = new dfx_csr();
   rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
   if (!rc) rc = csr_upload_acc(h, c, in, h->st());
+  if (!rc) rc = check_bad(c, in, h->st());
   if (rc) { csr_destroy_impl(c); return rc; }
   *out = c;
   return DFX_OK;
@@ -755,35 +776,46 @@ int dfx_csr_create_acc(dfx_handle* h, const dfx_acc_in* in, dfx_csr** out) {
 int dfx_csr_requirements_list(dfx_handle* h, dfx_csr* c, dfx_req_list* out, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_requirements_list: null argument");
   CK(cudaSetDevice(h->device));
+  CK(h->pipeline_init());
   cudaStream_t st = h->st();
   const dfx::CsrDev& p = c->p;
-  int64_t n_out = 0;
+  const int64_t want = (out && out->vars) ? out->cap : 0;
+  if (want > c->vars_cap) {
+    if (c->d_vars) cudaFree(c->d_vars);
+    c->d_vars = nullptr;
+    c->vars_cap = 0;
+    CK(cudaMalloc(&c->d_vars, sizeof(uint16_t) * (size_t)want));
+    c->vars_cap = want;
+  }
+  // Pipeline over node ranges: kernel (b), the scan and the list compaction
+  // of range k+1 run while range k's lists go back on the D2H stream.
+  const int K = p.n_nodes >= 4096 && want ? dfx_handle::kPipe : 1;
+  CK(cudaMemsetAsync(c->offsets, 0, sizeof(int64_t), st));
   CK(cudaEventRecord(c->e0, st));
-  int rc = dfx::requirements_scan(p, c->counts, c->offsets, c->scratch, c->scratch_bytes, 1, &n_out, st);
-  if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
-  // row offsets go back while the lists are compacted
+  for (int k = 0; k < K; k++) {
+    const int lo = (int)(p.n_nodes * k / K), hi = (int)(p.n_nodes * (k + 1) / K);
+    int rc = dfx::requirements_range(p, c->counts, c->offsets, c->scratch, c->scratch_bytes, lo, hi, st);
+    if (!rc && want) rc = dfx::compact_list(p, c->offsets, c->d_vars, want, lo, hi, st);
+    if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
+    CK(cudaMemcpyAsync(h->pin_cnt + k, c->offsets + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipe + k], st));
+  }
+  CK(cudaEventRecord(c->e1, st));
+  int64_t done = 0;
+  for (int k = 0; k < K; k++) {
+    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipe + k]));
+    int64_t end = (int64_t)h->pin_cnt[k];
+    if (end > want) end = want;
+    if (want && end > done)
+      CK(cudaMemcpyAsync(out->vars + done, c->d_vars + done, sizeof(uint16_t) * (size_t)(end - done),
+                         cudaMemcpyDeviceToHost, h->s_d2h));
+    if (end > done) done = end;
+  }
+  const int64_t n_out = (int64_t)h->pin_cnt[K - 1];
   if (out && out->row_off)
     CK(cudaMemcpyAsync(out->row_off, c->offsets, sizeof(int64_t) * (size_t)(p.n_nodes + 1),
-                       cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));   // n_out is on the host now
-  const int64_t want = (out && out->vars) ? out->cap : 0;
-  if (want && n_out <= want) {
-    if (n_out > c->vars_cap) {
-      if (c->d_vars) cudaFree(c->d_vars);
-      c->d_vars = nullptr;
-      c->vars_cap = 0;
-      CK(cudaMalloc(&c->d_vars, sizeof(uint16_t) * (size_t)(n_out + n_out / 8 + 64)));
-      c->vars_cap = n_out + n_out / 8 + 64;
-    }
-    rc = dfx::compact_list(p, c->offsets, c->d_vars, c->vars_cap, st);
-    if (rc) return fail(rc, "compact_list failed");
-    CK(cudaEventRecord(c->e1, st));
-    if (n_out) CK(cudaMemcpyAsync(out->vars, c->d_vars, sizeof(uint16_t) * (size_t)n_out,
-                                  cudaMemcpyDeviceToHost, st));
-  } else {
-    CK(cudaEventRecord(c->e1, st));
-  }
-  CK(cudaStreamSynchronize(st));
+                       cudaMemcpyDeviceToHost, h->s_d2h));
+  CK(cudaStreamSynchronize(h->s_d2h));
   if (out) out->n_out = n_out;
   if (stats) {
     float ms = 0.f;
@@ -842,7 +874,8 @@ int dfx_mfp_acc(dfx_handle* h, const dfx_acc_in* in, dfx_req_list* out, dfx_csr_
     h->csr_cache = c;
   }
   rc = csr_upload_acc(h, c, in, h->st());
-  if (!rc) rc = dfx_csr_solve(h, c, 0, stats);
+  if (!rc) rc = dfx_csr_solve(h, c, 0, stats);    // synchronises: the flag is final
+  if (!rc) rc = check_bad(c, in, h->st());
   if (!rc) rc = dfx_csr_requirements_list(h, c, out, stats);
   return rc;
 }

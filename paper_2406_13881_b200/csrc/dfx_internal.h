@@ -80,11 +80,14 @@ int requirements_scan(const CsrDev& p, int32_t* counts, int64_t* offsets, void* 
 int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratch,
                 size_t scratch_bytes, int64_t* n_out, cudaStream_t st);
 // access lists (acc.cu)
-int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, cudaStream_t st);
+int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, int64_t n_lo,
+               int64_t n_hi, cudaStream_t st);
 int count_acc(const CsrDev& p, int32_t* counts, cudaStream_t st);
 int export_acc(const CsrDev& p, const int64_t* off, uint16_t* acc, cudaStream_t st);
 int compact_list(const CsrDev& p, const int64_t* offsets, uint16_t* vars, int64_t cap,
-                 cudaStream_t st);
+                 int64_t n_lo, int64_t n_hi, cudaStream_t st);
+int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
 size_t round_ctl_bytes();
 

@@ -658,7 +658,7 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
 // ---------------------------------------------------------------------------
 template <int VPL>
 __global__ void __launch_bounds__(256)
-requirements_kernel(CsrDev p, int32_t* counts, int count_bits) {
+requirements_kernel(CsrDev p, int32_t* counts, int count_bits, int n_lo, int n_hi) {
   const int lane = threadIdx.x & 31;
   const int nq = p.words >> 2;
   const uint4* A = reinterpret_cast<const uint4*>(p.A);
@@ -678,7 +678,7 @@ requirements_kernel(CsrDev p, int32_t* counts, int count_bits) {
     smask[v] = active[v] ? ldg4(S4 + q) : zero4();
   }
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < p.n_nodes; n += warps) {
+  for (int n = n_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); n < n_hi; n += warps) {
     const int rs = __ldg(p.row_ptr + n), re = __ldg(p.row_ptr + n + 1);
     const bool kern = __ldg(p.kind + n) != 0;
     const size_t row = (size_t)n * nq;
@@ -972,12 +972,42 @@ int requirements_scan(const CsrDev& p, int32_t* counts, int64_t* offsets, void* 
   const int vpl = vpl_for(p.words);
   int blocks = grid_for(p.n_nodes * 32, 256);
   switch (vpl) {
-    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
-    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
-    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, count_bits); break;
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, count_bits, 0, (int)p.n_nodes); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, count_bits, 0, (int)p.n_nodes); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, count_bits, 0, (int)p.n_nodes); break;
     default: return DFX_E_LIMIT;
   }
   return scan_counts(p.n_nodes, counts, offsets, scratch, scratch_bytes, n_out, st);
+}
+
+// kernel (b) bit counts + scan over the node range [n_lo, n_hi): on return
+// (stream order) offsets[n_lo+1 .. n_hi] are global offsets, continuing from
+// offsets[n_lo] (set by the previous range; offsets[0] = 0 by the caller)
+__global__ void add_base_kernel(int64_t* out, int64_t len, const int64_t* base) {
+  const int64_t b = *base;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] += b;
+}
+
+int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
+                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st) {
+  const int vpl = vpl_for(p.words);
+  const int n = n_hi - n_lo;
+  if (n <= 0) return DFX_OK;
+  int blocks = grid_for((int64_t)n * 32, 256);
+  switch (vpl) {
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
+    default: return DFX_E_LIMIT;
+  }
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, counts + n_lo, offsets + n_lo + 1, n, st);
+  if (need > scratch_bytes) return DFX_E_NOSPC;
+  cub::DeviceScan::InclusiveSum(scratch, need, counts + n_lo, offsets + n_lo + 1, n, st);
+  add_base_kernel<<<grid_for(n, 256), 256, 0, st>>>(offsets + n_lo + 1, n, offsets + n_lo);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
 int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratch,
@@ -999,9 +1029,9 @@ int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scrat
   const int vpl = vpl_for(p.words);
   int blocks = grid_for(p.n_nodes * 32, 256);
   switch (vpl) {
-    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, 0); break;
-    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, 0); break;
-    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 0); break;
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, 0, 0, (int)p.n_nodes); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, 0, 0, (int)p.n_nodes); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 0, 0, (int)p.n_nodes); break;
     default: return DFX_E_LIMIT;
   }
   // offsets[0] = 0; offsets[1..n] = inclusive prefix of counts

@@ -427,13 +427,28 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// LDGSTS (cp.async, 16 B per lane) helpers
+__device__ __forceinline__ void cp16(uint4* sdst, const uint4* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
 template <int PHASE, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t* flags,
                  int max_rounds) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  // per-warp metadata of the current 32-node batch in shared memory (read
+  // by the node loop as broadcasts, so it holds no registers), and the next
+  // batch's descriptors landing by cp.async
+  struct BatchMeta { int4 d[2][32][2]; int opc[32]; unsigned dn[32]; };
+  __shared__ BatchMeta bm_all[256 / 32];
   const int lane = threadIdx.x & 31;
+  BatchMeta& bm = bm_all[threadIdx.x >> 5];
   const int nq = p.words >> 2;
   const bool act = lane < nq;
   const uint4* A = reinterpret_cast<const uint4*>(p.A);
@@ -487,19 +502,28 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
     int prev_n = -2;
     bool carry = false;
     // descriptors of the first batch
-    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
-    int opc = 0;
+    int buf = 0;
     if (n0 + lane < n1) {
-      d0 = __ldg(desc + 2 * (n0 + lane));
-      d1 = __ldg(desc + 2 * (n0 + lane) + 1);
-      if (!first) opc = __ldcg(p.popc + n0 + lane);
+      cp16(reinterpret_cast<uint4*>(&bm.d[0][lane][0]), reinterpret_cast<const uint4*>(desc + 2 * (n0 + lane)));
+      cp16(reinterpret_cast<uint4*>(&bm.d[0][lane][1]), reinterpret_cast<const uint4*>(desc + 2 * (n0 + lane) + 1));
     }
-    for (int nb = n0; nb < n1; nb += 32) {
+    cp_commit();
+    for (int nb = n0; nb < n1; nb += 32, buf ^= 1) {
       const int n = nb + lane;
       const bool valid = n < n1;
+      // next batch's descriptors in flight while this batch is processed
+      const int nn1 = nb + 32 + lane;
+      if (nn1 < n1) {
+        cp16(reinterpret_cast<uint4*>(&bm.d[buf ^ 1][lane][0]), reinterpret_cast<const uint4*>(desc + 2 * nn1));
+        cp16(reinterpret_cast<uint4*>(&bm.d[buf ^ 1][lane][1]), reinterpret_cast<const uint4*>(desc + 2 * nn1 + 1));
+      }
+      cp_commit();
+      cp_wait<1>();
+      __syncwarp();              // every lane's descriptor copies are visible warp-wide
+      const int4 d0 = bm.d[buf][lane][0], d1 = bm.d[buf][lane][1];
       const int rs = d0.x, deg = d0.y & 0x3FFFFFFF, kd = (d0.y >> 30) & 1;
       const int pr0 = d0.z, pr1 = d0.w, pr2 = d1.x, pr3 = d1.y;
-      const int cur_opc = first ? 32 * p.words : opc;
+      const int cur_opc = first ? 32 * p.words : (valid ? __ldcg(p.popc + n) : 0);
       // dn bit k: pred k's chunk is done for this round (its row is final);
       // the acquire orders the warp's later row loads after the release
       unsigned dn = 0;
@@ -524,12 +548,9 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
 #undef DFX_DONE
         }
       }
-      const int nn1 = nb + 32 + lane;
-      if (nn1 < n1) {
-        d0 = __ldg(desc + 2 * nn1);
-        d1 = __ldg(desc + 2 * nn1 + 1);
-        if (!first) opc = __ldcg(p.popc + nn1);
-      }
+      bm.opc[lane] = cur_opc;
+      bm.dn[lane] = dn;
+      __syncwarp();
       unsigned dm = __ballot_sync(FULL, valid && dirty);
       if (carry && nb < n1) dm |= 1u;
       carry = false;
@@ -538,12 +559,13 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
         const int j = __ffs(dm) - 1;
         dm &= dm - 1;
         const int nn = nb + j;
-        const int ndeg = __shfl_sync(FULL, deg, j);
-        const bool kern = __shfl_sync(FULL, kd, j) != 0;
-        const int old_pc = __shfl_sync(FULL, cur_opc, j);
-        const unsigned ndn = __shfl_sync(FULL, dn, j);
-        const int q0 = __shfl_sync(FULL, pr0, j), q1 = __shfl_sync(FULL, pr1, j);
-        const int q2 = __shfl_sync(FULL, pr2, j), q3 = __shfl_sync(FULL, pr3, j);
+        const int4 e0 = bm.d[buf][j][0], e1 = bm.d[buf][j][1];     // broadcasts
+        const int nrs = e0.x;
+        const int ndeg = e0.y & 0x3FFFFFFF;
+        const bool kern = (e0.y >> 30) & 1;
+        const int old_pc = bm.opc[j];
+        const unsigned ndn = bm.dn[j];
+        const int q0 = e0.z, q1 = e0.w, q2 = e1.x, q3 = e1.y;
         const size_t row = (size_t)nn * nq;
         const bool have_prev = prev_n == nn - 1;
         const uint4* plane = (PHASE == 0) == kern ? B : A;
@@ -577,7 +599,6 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
 #undef DFX_GATHER
         in = and4(and4(in, and4(g0, g1)), and4(g2, g3));
         if (ndeg > KP) {                                   // rare: more than KP preds
-          const int nrs = __shfl_sync(FULL, rs, j);
           for (int e = nrs + KP; e < nrs + ndeg; e++) {
             const int qk = __ldg(p.col + e);
             int sr = round;

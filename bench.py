@@ -252,6 +252,10 @@ def run_ours(args, rank, world, local):
     achieved = bytes_per_solve / (kernel_ms_per_solve / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic, _ = traffic_from_profiles()
+    pattern = None      # practical ceiling of the access pattern (profiles/, microbenchmark)
+    pc = ROOT / "profiles" / "r01b_gather_ceiling.json"
+    if pc.exists():
+        pattern = {r["pattern"]: r["GB_s"] for r in json.loads(pc.read_text())["results"]}
     survey_bytes = stats_last["evaluated"] * args.vars_per_gpu * (11 / 16)
 
     # kernel (b) once (not part of the fixpoint metric), for the record
@@ -333,7 +337,8 @@ def run_ours(args, rank, world, local):
                          "launches_per_solve": 2 if cfg.words <= 128 else rounds,
                          "rounds_per_solve": rounds,
                          "kernel_ms_per_solve": kernel_ms_per_solve,
-                         "survey_formula_frac": survey_bytes / (kernel_ms_per_solve / 1e3) / 1e9 / peak},
+                         "survey_formula_frac": survey_bytes / (kernel_ms_per_solve / 1e3) / 1e9 / peak,
+                         "access_pattern_ceiling_gbs": pattern},
             "solve": {"rounds_h": stats_last["rounds_h"], "rounds_d": stats_last["rounds_d"],
                       "evaluated_rows": stats_last["evaluated"],
                       "rows_read": stats_last["rows_read"],

@@ -31,6 +31,11 @@ def replay_runner(rin, rout) -> int:
     return lib().oracle_replay_batch(C.byref(rin), C.byref(rout))
 
 
+def replay_runner_mt(rin, rout) -> int:
+    """All host threads (OpenMP over functions); same output as replay_runner."""
+    return lib().oracle_replay_batch_mt(C.byref(rin), C.byref(rout))
+
+
 # ---- E2 / C3 (oracle/mfp_oracle.c) -------------------------------------------
 import numpy as np  # noqa: E402
 

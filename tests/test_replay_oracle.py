@@ -62,3 +62,16 @@ def test_oracle_vs_reference_random(seed):
         ref = _cases.canon_result(lambda: ref_analyze(a.src, a.cfgs[n], a.accesses[n], a.table))
         got = _cases.canon_result(d.get)
         assert got == ref, n
+
+
+def test_multithreaded_oracle_equals_sequential():
+    """The benchmark's all-threads CPU baseline (oracle_replay_batch_mt)
+    produces the sequential oracle's output exactly, event order included."""
+    import numpy as np
+    from paper_2406_13881_b200.batch import C4Config, c4_generate
+    from paper_2406_13881_b200.dataflow import run_replay
+    b, _ = c4_generate(C4Config(n_funcs=400, seed=3), np.arange(0, 400, 3, dtype=np.int32))
+    seq = run_replay(b, runner=_oracle.replay_runner)
+    mt = run_replay(b, runner=_oracle.replay_runner_mt)
+    assert np.array_equal(seq.events, mt.events)
+    assert np.array_equal(seq.var_out, mt.var_out)

@@ -204,7 +204,9 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     eng = _abi.engine(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by torch events and the engine
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng.lib.dfx_set_stream(eng.h, __import__("ctypes").c_void_p(stream.cuda_stream))
     cfg = C3Config(n_nodes=args.n_nodes, n_vars=args.vars_per_gpu, seed=args.seed,
                    w0=rank * (args.vars_per_gpu // 32))
@@ -219,19 +221,30 @@ def run_ours(args, rank, world, local):
 
     kernel_ms, launches, stats_last = 0.0, 0, None
     barrier()
+    # timed region: K solves enqueued back to back (V <= 4096: each solve is
+    # two persistent launches that decide convergence on the device, so no
+    # host round trip separates the steps), one synchronize at the end
+    persistent = cfg.words <= 128
     with ClockSampler(local) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
-            st = prob.solve(args.chunk)
-            kernel_ms += st.kernel_ms
-            # V <= 4096: one persistent cooperative launch per phase
-            launches += 2 if cfg.words <= 128 else st.rounds_h + st.rounds_d
-            stats_last = {k: getattr(st, k) for k, _ in st._fields_}
+            if persistent:
+                prob.solve_async(args.chunk)
+                launches += 2
+            else:
+                st = prob.solve(args.chunk)
+                launches += st.rounds_h + st.rounds_d
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
+    # per-solve statistics and phase-kernel time from synchronous solves
+    for _ in range(5):
+        st = prob.solve(args.chunk)
+        kernel_ms += st.kernel_ms
+    kernel_ms *= args.steps / 5.0
+    stats_last = {k: getattr(st, k) for k, _ in st._fields_}
     total_ms = ev0.elapsed_time(ev1)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -367,7 +380,9 @@ def run_c4(args, rank, world, local):
 
     torch.cuda.set_device(local)
     eng = _abi.engine(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by torch events and the engine
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng.lib.dfx_set_stream(eng.h, __import__("ctypes").c_void_p(stream.cuda_stream))
     cfg = C4Config(n_funcs=args.c4_funcs, seed=args.seed)
     N, V = c4_shapes(cfg)

@@ -158,6 +158,7 @@ def _setup(lib):
     for name in ("dfx_set_stream", "dfx_csr_create", "dfx_csr_generate_c3", "dfx_csr_destroy",
                  "dfx_csr_solve", "dfx_csr_requirements", "dfx_csr_download", "dfx_mfp_csr",
                  "dfx_csr_export", "dfx_csr_create_acc", "dfx_csr_requirements_list",
+                 "dfx_csr_solve_async",
                  "dfx_csr_export_acc", "dfx_mfp_acc"):
         getattr(lib, name).restype = C.c_int
     lib.dfx_csr_nnz.restype = C.c_int64
@@ -267,6 +268,11 @@ class CsrProblem:
         return _req_call(lambda o: self.eng.lib.dfx_csr_requirements(
             self.eng.h, self.h, C.byref(o), C.byref(self.stats)),
             self.eng, self.n_nodes, self.words, capacity, alloc, self.stats)
+
+    def solve_async(self, chunk_nodes: int = 0) -> None:
+        """Kernel (a) enqueued without host synchronisation (dfx_csr_solve_async)."""
+        self.eng.check(self.eng.lib.dfx_csr_solve_async(self.eng.h, self.h, C.c_int32(chunk_nodes)),
+                       "dfx_csr_solve_async")
 
     def requirements_list(self, capacity: int | None = None, alloc=np.empty) -> ReqList:
         """Kernel (b) as per-node variable lists (dfx_csr_requirements_list)."""

@@ -599,6 +599,17 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
   return DFX_OK;
 }
 
+int dfx_csr_solve_async(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes) {
+  if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve_async: null argument");
+  if (dfx::vpl_for(c->p.words) != 1) return dfx_csr_solve(h, c, chunk_nodes, nullptr);
+  CK(cudaSetDevice(h->device));
+  if (chunk_nodes <= 0) chunk_nodes = 64;
+  dfx::SolveStats s{};
+  int rc = dfx::mfp_solve(c->p, c->d_cnt, c->flags, h->st(), chunk_nodes, &s, false);
+  if (rc) return fail(rc, "mfp_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return DFX_OK;
+}
+
 int dfx_csr_requirements(dfx_handle* h, dfx_csr* c, dfx_req_out* out, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_requirements: null argument");
   CK(cudaSetDevice(h->device));

@@ -71,7 +71,7 @@ int build_desc(const CsrDev& p, cudaStream_t st);
 int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st);
 int vpl_for(int words);
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
-              SolveStats* stats);
+              SolveStats* stats, bool collect = true);
 int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
                  size_t scratch_bytes, uint32_t* occ, uint32_t* masks, int64_t cap,
                  int64_t* n_out, cudaStream_t st);

@@ -897,7 +897,7 @@ static int launch_phase(const CsrDev& p, int chunk_nodes, int n_chunks, RoundCtl
 }
 
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
-              SolveStats* stats) {
+              SolveStats* stats, bool collect) {
   const int vpl = vpl_for(p.words);
   if (vpl < 0) return DFX_E_LIMIT;
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
@@ -923,6 +923,7 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
       if (rc != DFX_OK) return rc;
       cudaEventRecord(ev[2 * phase + 1], st);
     }
+    if (!collect) return DFX_OK;        // enqueued only: no host synchronisation
     if (cudaMemcpyAsync(h, ctl2, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
     for (int phase = 0; phase < 2; phase++) {

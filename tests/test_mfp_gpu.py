@@ -149,3 +149,18 @@ def test_acc_rejects_bad_entries():
     bad[0] = bad[0] & 0x3FFF                      # kind 0
     with pytest.raises(RuntimeError):
         CsrProblem.from_acc(g["row_ptr"], g["col"], g["kind"], off, bad, g["S"], 4)
+
+
+def test_async_solves_back_to_back_reach_the_fixpoint():
+    """dfx_csr_solve_async: several solves enqueued without host sync (each
+    restarts from top and decides convergence on the device) end at the
+    same fixpoint as the synchronous call."""
+    g = _oracle.c3_generate(4, 1 << 14, 0, 128, 82)
+    prob = CsrProblem.from_arrays(g["row_ptr"], g["col"], g["kind"], g["USE"], g["B"], g["S"])
+    for _ in range(4):
+        prob.solve_async()
+    OH, OD, _ = prob.download(True, True)
+    eh, ed, _ = _oracle.c3_solve(g)
+    assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
+    st = prob.solve()
+    assert st.rounds_h >= 2

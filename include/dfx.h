@@ -228,8 +228,8 @@ int dfx_csr_destroy(dfx_handle *h, dfx_csr *p);
 /* kernel (a); chunk_nodes <= 0 picks the default */
 int dfx_csr_solve(dfx_handle *h, dfx_csr *p, int32_t chunk_nodes, dfx_csr_stats *stats);
 /* kernel (a) enqueued on the handle's stream without host synchronisation
- * (convergence is decided on the device; V <= 4096, else synchronous);
- * back-to-back solves of a resident problem pipeline on the GPU */
+ * (convergence is decided on the device); back-to-back solves of a resident
+ * problem pipeline on the GPU */
 int dfx_csr_solve_async(dfx_handle *h, dfx_csr *p, int32_t chunk_nodes);
 /* kernel (b): requirement planes + order-preserving compaction (D2H of the
  * parts of `out` that are non-NULL) */

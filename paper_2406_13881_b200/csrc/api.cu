@@ -464,9 +464,9 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
   c->scratch = csr_alloc<uint8_t>(c, c->scratch_bytes);
   c->d_cnt = csr_alloc<uint8_t>(c, dfx::round_ctl_bytes());
   c->d_bad = csr_alloc<int>(c, 1);
-  p.seen = csr_alloc<uint8_t>(c, nnz > 0 ? nnz : 1);
+  p.seen = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
   p.chunk_done = csr_alloc<int32_t>(c, n);
-  p.seen4 = csr_alloc<uint32_t>(c, n);
+  p.seen4 = csr_alloc<int32_t>(c, 4 * (size_t)n);
   p.succ_ptr = csr_alloc<int32_t>(c, n + 1);
   p.succ = csr_alloc<int32_t>(c, nnz > 0 ? nnz : 1);
   c->flags = csr_alloc<uint8_t>(c, 2 * (size_t)n);   // >= 2 * n_chunks for chunk_nodes >= 1
@@ -601,7 +601,6 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
 
 int dfx_csr_solve_async(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve_async: null argument");
-  if (dfx::vpl_for(c->p.words) != 1) return dfx_csr_solve(h, c, chunk_nodes, nullptr);
   CK(cudaSetDevice(h->device));
   if (chunk_nodes <= 0) chunk_nodes = 64;
   dfx::SolveStats s{};

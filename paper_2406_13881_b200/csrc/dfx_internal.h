@@ -51,10 +51,10 @@ struct CsrDev {
   int32_t* popc;    // per-node population count of the current OUT row
   int32_t s_quads_low;  // every nonzero scalar quad has index < 8
   int32_t* desc;        // [n_nodes][8] node descriptors (rs, deg|kind<<30, p0..p3)
-  uint8_t* seen;        // [nnz] per-edge seen round, edges >= 4 of a node (kernel a frontier)
+  int32_t* seen;        // [nnz] per-edge seen round, edges >= 4 of a node (kernel a frontier)
   int32_t* succ_ptr;    // [n_nodes+1] successor (reverse) CSR: candidate flags of kernel (a)
   int32_t* succ;        // [nnz]
-  uint32_t* seen4;      // [n_nodes] seen rounds of a node's first 4 edges, one byte each
+  int32_t* seen4;       // [n_nodes][4] seen rounds of a node's first 4 edges
   int32_t* chunk_done;  // [n_nodes] per-chunk round completed (kernel a frontier)
 };
 

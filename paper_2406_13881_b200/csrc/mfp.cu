@@ -106,237 +106,24 @@ struct RoundCounters {
   unsigned long long rows_written;
 };
 
-constexpr int kMaxRounds = 64;
+constexpr int kTraceRounds = 64;   // per-round counters kept for traces
+constexpr int kMaxSlices = 4;      // V <= 16384: up to four 4096-variable slices
 
-// device-side round control of one phase: rounds are launched back to back
-// without host round trips; the last block of a round that changed nothing
-// raises `done`, and every later launch of the phase returns at once
+// Device-side control of one phase (one persistent launch).  Rounds use a
+// ring of four counter slots (slot round & 3; the slot of round r+1 is
+// cleared during round r), so the number of rounds is unbounded.
 struct RoundCtl {
-  RoundCounters cnt[kMaxRounds + 1];
-  unsigned int blocks_done[kMaxRounds + 1];
-  unsigned long long t_end[kMaxRounds + 1];   // persistent kernel: %globaltimer after each round
-  int done;
-  int rounds;                                  // persistent kernel: rounds run (incl. the last, unchanged one)
+  RoundCounters ring[4];
+  RoundCounters cnt[kTraceRounds + 1];          // copies of the first rounds (traces)
+  unsigned long long t_end[kTraceRounds + 1];   // %globaltimer after each round
+  unsigned long long tot_eval, tot_read, tot_written;
+  int rounds;                                   // rounds run (incl. the last, unchanged one)
 };
 
-// per-warp counters -> round totals; the last block to finish decides
-// termination (a round r > 1 that changed no row ends the phase)
-__device__ __forceinline__ void round_epilogue(RoundCtl* ctl, int round, int lane,
-                                               unsigned long long n_changed,
-                                               unsigned long long n_eval,
-                                               unsigned long long n_read,
-                                               unsigned long long n_written) {
-  RoundCounters* cnt = &ctl->cnt[round];
-  if (lane == 0) {
-    if (n_changed) atomicAdd(&cnt->changed, n_changed);
-    if (n_eval) atomicAdd(&cnt->evaluated, n_eval);
-    if (n_read) atomicAdd(&cnt->rows_read, n_read);
-    if (n_written) atomicAdd(&cnt->rows_written, n_written);
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&ctl->blocks_done[round], 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence();
-      const unsigned long long ch = atomicAdd(&cnt->changed, 0ull);
-      if (round > 1 && ch == 0) atomicExch(&ctl->done, 1);
-    }
-  }
-}
-
-
-template <int PHASE, int VPL, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-mfp_round_kernel(CsrDev p, int round, int first, int chunk_nodes, int n_chunks,
-                 RoundCtl* ctl, uint8_t* flags_cur, uint8_t* flags_next) {
-  if (__ldcg(&ctl->done)) return;
-  RoundCounters* cnt = &ctl->cnt[round];
-  const int lane = threadIdx.x & 31;
-  const int nq = p.words >> 2;                 // uint4 per row
-  const uint4* A = reinterpret_cast<const uint4*>(p.A);
-  const uint4* B = reinterpret_cast<const uint4*>(p.B);
-  const uint4* OH = reinterpret_cast<const uint4*>(p.OH);
-  uint4* OUT = reinterpret_cast<uint4*>(PHASE == 0 ? p.OH : p.OD);
-  const uint4* S4 = reinterpret_cast<const uint4*>(p.S);
-
-  uint4 smask[VPL];
-  bool active[VPL];
-  bool any_s = false;
-#pragma unroll
-  for (int v = 0; v < VPL; v++) {
-    int q = lane + 32 * v;
-    active[v] = q < nq;
-    smask[v] = active[v] ? ldg4(S4 + q) : zero4();
-    any_s |= nz4(smask[v]);
-  }
-  const uint4 boundary = PHASE == 0 ? all4() : zero4();
-
-  unsigned long long n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;
-  for (;;) {
-    int chunk = 0;
-    if (lane == 0) chunk = (int)atomicAdd(&cnt->chunk, 1ull);
-    chunk = __shfl_sync(FULL, chunk, 0);
-    if (chunk >= n_chunks) break;
-    const int n0 = chunk * chunk_nodes;
-    const int n1 = min(n0 + chunk_nodes, (int)p.n_nodes);
-    uint4 prev[VPL];
-    int prev_n = -2;
-    bool carry = false;   // last node of the previous batch changed this round
-    for (int nb = n0; nb < n1; nb += 32) {
-      // per-node metadata for 32 nodes at once (lane = node): CSR bounds,
-      // kind, previous popcount and the first KP predecessor ids, all issued
-      // as independent loads so a node's row gathers later need no
-      // dependent index load
-      const int n = nb + lane;
-      const bool valid = n < n1;
-      int rs = 0, re = 0, kd = 0, opc = 0;
-      int pr[KP];
-      bool dirty = false;
-#pragma unroll
-      for (int k = 0; k < KP; k++) pr[k] = 0;
-      if (valid) {
-        rs = __ldg(p.row_ptr + n);
-        re = __ldg(p.row_ptr + n + 1);
-        kd = __ldg(p.kind + n);
-        opc = first ? 32 * p.words : __ldcg(p.popc + n);
-#pragma unroll
-        for (int k = 0; k < KP; k++)
-          if (k < re - rs) pr[k] = __ldg(p.col + rs + k);
-        dirty = first != 0;
-        if (!first) {
-#pragma unroll
-          for (int k = 0; k < KP; k++)
-            if (k < re - rs) dirty |= __ldcg(p.stamp + pr[k]) >= round - 1;
-          for (int e = rs + KP; e < re && !dirty; e++)
-            dirty = __ldcg(p.stamp + __ldg(p.col + e)) >= round - 1;
-        }
-      }
-      unsigned dm = __ballot_sync(FULL, dirty);
-      // fall-through successor of a node changed earlier in this sweep
-      if (carry && nb < n1) dm |= 1u;
-      carry = false;
-      const unsigned vmask = __ballot_sync(FULL, valid);
-      while (dm) {
-        const int j = __ffs(dm) - 1;
-        dm &= dm - 1;
-        const int nn = nb + j;
-        const int nrs = __shfl_sync(FULL, rs, j), nre = __shfl_sync(FULL, re, j);
-        const bool kern = __shfl_sync(FULL, kd, j) != 0;
-        const int old_pc = __shfl_sync(FULL, opc, j);
-        int q[KP];
-#pragma unroll
-        for (int k = 0; k < KP; k++) q[k] = __shfl_sync(FULL, pr[k], j);
-        const int deg = nre - nrs;
-        const size_t row = (size_t)nn * nq;
-        // transfer-plane rows
-        uint4 pa[VPL], pb[VPL];
-#pragma unroll
-        for (int v = 0; v < VPL; v++) {
-          const int qq = lane + 32 * v;
-          pa[v] = pb[v] = zero4();
-          if (!active[v]) continue;
-          if (PHASE == 0) {
-            if (kern) pb[v] = ldg4(B + row + qq); else pa[v] = ldg4(A + row + qq);
-          } else {
-            if (kern) {
-              pa[v] = ldg4(A + row + qq);
-              if (nz4(smask[v])) pb[v] = ldg4(B + row + qq);
-            } else {
-              pb[v] = ldg4(B + row + qq);
-            }
-          }
-        }
-        n_read += 1;
-        // meet over predecessors (change detection uses the popcount: every
-        // value only decreases -- monotone descent from top -- so a row
-        // changed iff its population count dropped; no old-row re-read)
-        uint4 in[VPL], hin[VPL];
-        const bool need_hin = PHASE == 1 && kern && any_s;
-#pragma unroll
-        for (int v = 0; v < VPL; v++) { in[v] = deg == 0 ? boundary : all4(); hin[v] = all4(); }
-        const bool have_prev = prev_n == nn - 1;
-#pragma unroll
-        for (int k = 0; k < KP; k++) {
-          if (k >= deg) break;
-          const int qk = q[k];
-          if (qk == nn - 1 && have_prev) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
-          } else if (!first) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++)
-              if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)qk * nq + lane + 32 * v));
-            n_read++;
-          }
-          if (need_hin) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++)
-              if (active[v] && nz4(smask[v]))
-                hin[v] = and4(hin[v], ldg4(OH + (size_t)qk * nq + lane + 32 * v));
-          }
-        }
-        for (int e = nrs + KP; e < nre; e++) {     // rare: more than KP preds
-          const int qk = __ldg(p.col + e);
-          if (qk == nn - 1 && have_prev) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++) in[v] = and4(in[v], prev[v]);
-          } else if (!first) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++)
-              if (active[v]) in[v] = and4(in[v], ldcg4(OUT + (size_t)qk * nq + lane + 32 * v));
-            n_read++;
-          }
-          if (need_hin) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++)
-              if (active[v] && nz4(smask[v]))
-                hin[v] = and4(hin[v], ldg4(OH + (size_t)qk * nq + lane + 32 * v));
-          }
-        }
-        // transfer
-        int pc = 0;
-        uint4 out[VPL];
-#pragma unroll
-        for (int v = 0; v < VPL; v++) {
-          if (PHASE == 0) {
-            out[v] = kern ? andn4(in[v], pb[v]) : or4(in[v], pa[v]);
-          } else if (kern) {
-            const uint4 f = and4(andn4(pa[v], pb[v]), smask[v]);
-            out[v] = or4(in[v], andn4(pa[v], and4(f, hin[v])));
-          } else {
-            out[v] = andn4(in[v], pb[v]);
-          }
-          if (active[v]) pc += __popc(out[v].x) + __popc(out[v].y) + __popc(out[v].z) + __popc(out[v].w);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
-        const bool ch = pc != old_pc;
-        n_eval++;
-        if (ch || first) {
-#pragma unroll
-          for (int v = 0; v < VPL; v++)
-            if (active[v]) __stcg(OUT + row + lane + 32 * v, out[v]);
-          n_written++;
-        }
-        if (lane == 0) {
-          if (ch || first) p.popc[nn] = pc;
-          p.stamp[nn] = ch ? round : (first ? 0 : p.stamp[nn]);
-        }
-        n_changed += ch;
-#pragma unroll
-        for (int v = 0; v < VPL; v++) prev[v] = out[v];
-        prev_n = nn;
-        if (ch && !first) {   // Gauss-Seidel: re-evaluate the successor now
-          if (j < 31) dm |= (1u << (j + 1)) & vmask;
-          else carry = true;
-        }
-      }
-    }
-  }
-  round_epilogue(ctl, round, lane, n_changed, n_eval, n_read, n_written);
-}
-
+// stamp[p] and seen[e] are full round numbers (a node can go unevaluated
+// for any number of rounds before a predecessor changes, so no wrapped
+// encoding is safe)
+__device__ __forceinline__ bool newer(int stamp, int seen) { return stamp > seen; }
 
 // ---------------------------------------------------------------------------
 // per-node descriptor (32 B, built once per problem): CSR start, degree,
@@ -438,7 +225,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 template <int PHASE, int MINB>
 __global__ void __launch_bounds__(256, MINB)
-mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t* flags,
+mfp_phase_kernel(CsrDev p, int q0, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t* flags,
                  int max_rounds) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -449,19 +236,25 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
   __shared__ BatchMeta bm_all[256 / 32];
   const int lane = threadIdx.x & 31;
   BatchMeta& bm = bm_all[threadIdx.x >> 5];
-  const int nq = p.words >> 2;
-  const bool act = lane < nq;
+  // this launch solves the 4096-variable slice of quads [q0, q0 + 32)
+  const int nq = p.words >> 2;          // row stride in quads
+  const int ql = q0 + lane;
+  const bool act = ql < nq;
   const uint4* A = reinterpret_cast<const uint4*>(p.A);
   const uint4* B = reinterpret_cast<const uint4*>(p.B);
   const uint4* OH = reinterpret_cast<const uint4*>(p.OH);
   uint4* OUT = reinterpret_cast<uint4*>(PHASE == 0 ? p.OH : p.OD);
   const int4* desc = reinterpret_cast<const int4*>(p.desc);
-  const uint4 smask = act ? ldg4(reinterpret_cast<const uint4*>(p.S) + lane) : zero4();
+  const uint4 smask = act ? ldg4(reinterpret_cast<const uint4*>(p.S) + ql) : zero4();
   const bool has_s = nz4(smask);
   const uint4 boundary = PHASE == 0 ? all4() : zero4();
   for (int round = 1; round <= max_rounds; round++) {
   const int first = round == 1;
-  RoundCounters* cnt = &ctl->cnt[round];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // slot of round + 1 (last used in round - 3)
+    RoundCounters& z = ctl->ring[(round + 1) & 3];
+    z.chunk = z.changed = z.evaluated = z.rows_read = z.rows_written = 0ull;
+  }
+  RoundCounters* cnt = &ctl->ring[round & 3];
   uint8_t* fcur = flags + (size_t)(round & 1) * n_chunks;
   uint8_t* fnext = flags + (size_t)((round + 1) & 1) * n_chunks;
   unsigned n_changed = 0, n_eval = 0, n_read = 0, n_written = 0;   // per warp
@@ -470,7 +263,7 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
   // mark(r): round r flags successor chunks for round r+1, decided on round
   // r-1's change count (final: the previous launch has completed)
   auto marks = [&](int r) {
-    return r >= 2 && 8 * __ldcg(&ctl->cnt[r - 1].changed) <= 5ull * (unsigned long long)p.n_nodes;
+    return r >= 2 && 8 * __ldcg(&ctl->ring[(r - 1) & 3].changed) <= 5ull * (unsigned long long)p.n_nodes;
   };
   const bool mark = marks(round);
   const bool sparse = round >= 3 && marks(round - 1);
@@ -530,13 +323,14 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
       bool dirty = first != 0;
       if (valid) {
         if (!first) {
-          const unsigned s4 = __ldcg(p.seen4 + n);
+          const int4 s4 = __ldcg(reinterpret_cast<const int4*>(p.seen4) + n);
+          const int sk[KP] = {s4.x, s4.y, s4.z, s4.w};
 #define DFX_DIRTY(K, Q) \
-  if (deg > K) dirty |= __ldcg(p.stamp + (Q)) > (int)((s4 >> (8 * K)) & 0xFFu);
+  if (deg > K) dirty |= newer(__ldcg(p.stamp + (Q)), sk[K]);
           DFX_DIRTY(0, pr0) DFX_DIRTY(1, pr1) DFX_DIRTY(2, pr2) DFX_DIRTY(3, pr3)
 #undef DFX_DIRTY
           for (int e = rs + KP; e < rs + deg && !dirty; e++)
-            dirty = __ldcg(p.stamp + __ldg(p.col + e)) > (int)__ldcg(p.seen + e);
+            dirty = newer(__ldcg(p.stamp + __ldg(p.col + e)), __ldcg(p.seen + e));
         }
         if (dirty) {
 #define DFX_DONE(K, Q)                                                                   \
@@ -572,25 +366,25 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
         uint4 pl = zero4(), b0 = zero4(), oh = zero4();
         uint4 in = ndeg == 0 ? boundary : all4();
         if (act) {
-          pl = ldg4(plane + row + lane);
+          pl = ldg4(plane + row + ql);
           // D phase, kernel node: F & H_in = F & OUT_H[n] (F = A & ~B & S is
           // disjoint from B and OUT_H = H_in & ~B), only scalar lanes
-          if (PHASE == 1 && kern && has_s) { b0 = ldg4(B + row + lane); oh = ldcg4(OH + row + lane); }
+          if (PHASE == 1 && kern && has_s) { b0 = ldg4(B + row + ql); oh = ldcg4(OH + row + ql); }
         }
         // gathers, all issued before use; per edge the round whose final
         // value this evaluation incorporates
-        unsigned s4 = 0;
+        int sv[KP] = {0, 0, 0, 0};
         uint4 g0 = all4(), g1 = all4(), g2 = all4(), g3 = all4();
 #define DFX_GATHER(K, Q, G)                                                              \
   if (ndeg > K) {                                                                        \
     if ((Q) == nn - 1 && have_prev) {                                                    \
       G = prev;                                                                          \
-      s4 |= (unsigned)round << (8 * K);                                                  \
+      sv[K] = round;                                                                     \
     } else {                                                                             \
       const bool fin_ = (ndn >> K) & 1u;                                                 \
-      s4 |= (unsigned)(fin_ ? round : round - 1) << (8 * K);                             \
+      sv[K] = fin_ ? round : round - 1;                                                  \
       if (!first || fin_) {                                                              \
-        if (act) G = ldcg4(OUT + (size_t)(Q) * nq + lane);                               \
+        if (act) G = ldcg4(OUT + (size_t)(Q) * nq + ql);                               \
         n_read++;                                                                        \
       }                                                                                  \
     }                                                                                    \
@@ -609,11 +403,11 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
               const bool fin = c != chunk && ld_acquire(p.chunk_done + c) == round;
               sr = fin ? round : round - 1;
               if (!first || fin) {
-                if (act) in = and4(in, ldcg4(OUT + (size_t)qk * nq + lane));
+                if (act) in = and4(in, ldcg4(OUT + (size_t)qk * nq + ql));
                 n_read++;
               }
             }
-            if (lane == 0) p.seen[e] = (uint8_t)sr;
+            if (lane == 0) p.seen[e] = sr;
           }
         }
         uint4 out;
@@ -630,11 +424,11 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
         n_eval++;
         n_read++;
         if (ch || first) {
-          if (act) __stcg(OUT + row + lane, out);
+          if (act) __stcg(OUT + row + ql, out);
           n_written++;
         }
         if (lane == 0) {
-          p.seen4[nn] = s4;
+          reinterpret_cast<int4*>(p.seen4)[nn] = make_int4(sv[0], sv[1], sv[2], sv[3]);
           if (ch || first) p.popc[nn] = pc;
           if (ch) p.stamp[nn] = round;
           else if (first) p.stamp[nn] = 0;
@@ -666,7 +460,10 @@ mfp_phase_kernel(CsrDev p, int chunk_nodes, int n_chunks, RoundCtl* ctl, uint8_t
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    ctl->t_end[round] = t;
+    ctl->tot_eval += cnt->evaluated;
+    ctl->tot_read += cnt->rows_read;
+    ctl->tot_written += cnt->rows_written;
+    if (round <= kTraceRounds) { ctl->cnt[round] = *cnt; ctl->t_end[round] = t; }
     ctl->rounds = round;
   }
   // every thread reads the same final count: a uniform exit
@@ -831,52 +628,12 @@ int or_planes(const CsrDev& p, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
-template <int PHASE>
-static int launch_round(const CsrDev& p, int vpl, int round, int first, int chunk_nodes,
-                        int n_chunks, RoundCtl* ctl, uint8_t* fcur, uint8_t* fnext,
-                        cudaStream_t st) {
-  // grid = resident blocks: a persistent-style launch pulling chunks
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per_sm = 1;
-#define DFX_LAUNCH(K)                                                                          \
-  do {                                                                                         \
-    static int occ_ = 0;                                                                       \
-    if (!occ_) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, K, 256, 0);               \
-    per_sm = occ_ > 0 ? occ_ : 1;                                                              \
-    K<<<sms * per_sm, 256, 0, st>>>(p, round, first, chunk_nodes, n_chunks, ctl, fcur, fnext); \
-  } while (0)
-  if (vpl == 1) return DFX_E_LIMIT;                  // persistent path (launch_phase)
-  else if (vpl == 2) DFX_LAUNCH((mfp_round_kernel<PHASE, 2, 1>));
-  else if (vpl == 4) DFX_LAUNCH((mfp_round_kernel<PHASE, 4, 1>));
-  else return DFX_E_LIMIT;
-#undef DFX_LAUNCH
-  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
-}
-
-int vpl_for(int words) {
-  int nq = words / 4;
-  if (words % 4) return -1;
-  if (nq <= 32) return 1;
-  if (nq <= 64) return 2;
-  if (nq <= 128) return 4;
-  return -1;
-}
-
-size_t round_ctl_bytes() { return 2 * sizeof(RoundCtl); }
-
-// Both phases to their fixpoints.  Rounds are queued in batches of
-// `kBatch` launches with no host synchronisation in between; a round
-// launched after the phase converged returns immediately.
-// kernel (a), V <= 4096: one persistent cooperative launch per phase runs
+// kernel (a): one persistent cooperative launch per (slice, phase) runs
 // every round (grid-wide barrier between rounds, uniform exit on a round
-// without changes) -- no host round trips and no launch gaps
+// without changes) -- no host round trips and no launch gaps.  V > 4096 is
+// solved as independent 4096-variable slices (variables are independent).
 template <int PHASE>
-static int launch_phase(const CsrDev& p, int chunk_nodes, int n_chunks, RoundCtl* ctl,
+static int launch_phase(const CsrDev& p, int q0, int chunk_nodes, int n_chunks, RoundCtl* ctl,
                         uint8_t* flags, cudaStream_t st) {
   static int sms = 0, per_sm = 0;
   auto* fn = mfp_phase_kernel<PHASE, 4>;
@@ -888,103 +645,73 @@ static int launch_phase(const CsrDev& p, int chunk_nodes, int n_chunks, RoundCtl
     if (per_sm < 1) per_sm = 1;
   }
   CsrDev pp = p;
-  int max_rounds = kMaxRounds;
-  void* args[] = {&pp, &chunk_nodes, &n_chunks, &ctl, &flags, &max_rounds};
+  int max_rounds = 1 << 30;
+  void* args[] = {&pp, &q0, &chunk_nodes, &n_chunks, &ctl, &flags, &max_rounds};
   if (cudaLaunchCooperativeKernel((const void*)fn, dim3(sms * per_sm), dim3(256), args, 0, st) !=
       cudaSuccess)
     return DFX_E_CUDA;
   return DFX_OK;
 }
 
+int vpl_for(int words) {
+  int nq = words / 4;
+  if (words % 4) return -1;
+  if (nq <= 32) return 1;
+  if (nq <= 64) return 2;
+  if (nq <= 128) return 4;
+  return -1;
+}
+
+size_t round_ctl_bytes() { return 2 * kMaxSlices * sizeof(RoundCtl); }
+
 int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, int chunk_nodes,
               SolveStats* stats, bool collect) {
   const int vpl = vpl_for(p.words);
   if (vpl < 0) return DFX_E_LIMIT;
+  const int n_slices = vpl;                 // 32 quads (4096 variables) per slice
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
-  constexpr int kBatch = 8;
-  RoundCtl* ctl2 = reinterpret_cast<RoundCtl*>(ctl_mem);   // [2]: one per phase
-  static thread_local cudaEvent_t ev[2 * (kMaxRounds + 1)] = {};
+  RoundCtl* ctls = reinterpret_cast<RoundCtl*>(ctl_mem);   // [slice][phase]
+  static thread_local cudaEvent_t ev[2 * 2 * kMaxSlices] = {};
   if (!ev[0])
     for (auto& e : ev) cudaEventCreate(&e);
   static int trace = -1;
   if (trace < 0) trace = getenv("DFX_TRACE") ? 1 : 0;
-  stats->rounds[0] = stats->rounds[1] = 0;
-  stats->evaluated = stats->rows_read = stats->rows_written = 0;
-  stats->kernel_ms = 0.f;
-  static thread_local RoundCtl h[2];
-  if (cudaMemsetAsync(ctl2, 0, 2 * sizeof(RoundCtl), st) != cudaSuccess) return DFX_E_CUDA;
-  if (vpl == 1) {
+  if (cudaMemsetAsync(ctls, 0, sizeof(RoundCtl) * 2 * n_slices, st) != cudaSuccess) return DFX_E_CUDA;
+  for (int sl = 0; sl < n_slices; sl++)
     for (int phase = 0; phase < 2; phase++) {
       if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
       if (cudaMemsetAsync(p.chunk_done, 0, sizeof(int) * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
-      cudaEventRecord(ev[2 * phase], st);
-      int rc = phase == 0 ? launch_phase<0>(p, chunk_nodes, n_chunks, ctl2, flags, st)
-                          : launch_phase<1>(p, chunk_nodes, n_chunks, ctl2 + 1, flags, st);
+      const int k = 2 * sl + phase;
+      cudaEventRecord(ev[2 * k], st);
+      int rc = phase == 0 ? launch_phase<0>(p, 32 * sl, chunk_nodes, n_chunks, ctls + k, flags, st)
+                          : launch_phase<1>(p, 32 * sl, chunk_nodes, n_chunks, ctls + k, flags, st);
       if (rc != DFX_OK) return rc;
-      cudaEventRecord(ev[2 * phase + 1], st);
+      cudaEventRecord(ev[2 * k + 1], st);
     }
-    if (!collect) return DFX_OK;        // enqueued only: no host synchronisation
-    if (cudaMemcpyAsync(h, ctl2, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFX_E_CUDA;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
-    for (int phase = 0; phase < 2; phase++) {
-      float kms = 0.f;
-      cudaEventElapsedTime(&kms, ev[2 * phase], ev[2 * phase + 1]);
-      stats->kernel_ms += kms;
-      const RoundCtl& c = h[phase];
-      if (c.rounds >= kMaxRounds && c.cnt[c.rounds].changed) return DFX_E_LIMIT;
-      stats->rounds[phase] = c.rounds;
-      for (int r = 1; r <= c.rounds; r++) {
-        stats->evaluated += (int64_t)c.cnt[r].evaluated;
-        stats->rows_read += (int64_t)c.cnt[r].rows_read;
-        stats->rows_written += (int64_t)c.cnt[r].rows_written;
-        if (trace)
-          fprintf(stderr, "dfx-trace phase %d round %d evaluated %llu changed %llu rows_read %llu "
-                  "rows_written %llu round_us %.1f\n", phase, r, c.cnt[r].evaluated,
-                  c.cnt[r].changed, c.cnt[r].rows_read, c.cnt[r].rows_written,
-                  r > 1 ? (c.t_end[r] - c.t_end[r - 1]) / 1e3 : 0.0);
-      }
-    }
-    return DFX_OK;
-  }
-  // V > 4096: one launch per round, queued in batches of kBatch with no host
-  // synchronisation in between; a round launched after convergence returns
-  for (int phase = 0; phase < 2; phase++) {
-    RoundCtl* ctl = ctl2 + phase;
-    if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
-    int launched = 0;
-    for (;;) {
-      for (int k = 0; k < kBatch && launched < kMaxRounds; k++) {
-        const int r = ++launched;
-        uint8_t* fcur = flags + (size_t)(r & 1) * n_chunks;
-        uint8_t* fnext = flags + (size_t)((r + 1) & 1) * n_chunks;
-        cudaEventRecord(ev[2 * r], st);
-        int rc = phase == 0 ? launch_round<0>(p, vpl, r, r == 1, chunk_nodes, n_chunks, ctl, fcur, fnext, st)
-                            : launch_round<1>(p, vpl, r, r == 1, chunk_nodes, n_chunks, ctl, fcur, fnext, st);
-        if (rc != DFX_OK) return rc;
-        cudaEventRecord(ev[2 * r + 1], st);
-      }
-      if (cudaMemcpyAsync(&h[phase], ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        return DFX_E_CUDA;
-      if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
-      if (h[phase].done) break;
-      if (launched >= kMaxRounds) return DFX_E_LIMIT;
-    }
-    int rounds = 0;
-    for (int r = 1; r <= launched; r++) {
-      const RoundCounters& c = h[phase].cnt[r];
-      float kms = 0.f;
-      cudaEventElapsedTime(&kms, ev[2 * r], ev[2 * r + 1]);
-      stats->kernel_ms += kms;
-      if (trace)
-        fprintf(stderr, "dfx-trace phase %d round %d evaluated %llu changed %llu rows_read %llu "
-                "rows_written %llu kernel_ms %.4f\n", phase, r, c.evaluated, c.changed,
-                c.rows_read, c.rows_written, kms);
-      stats->evaluated += (int64_t)c.evaluated;
-      stats->rows_read += (int64_t)c.rows_read;
-      stats->rows_written += (int64_t)c.rows_written;
-      if (!rounds && r > 1 && c.changed == 0 && h[phase].blocks_done[r]) rounds = r;
-    }
-    stats->rounds[phase] = rounds;
+  if (!collect) return DFX_OK;        // enqueued only: no host synchronisation
+  static thread_local RoundCtl h[2 * kMaxSlices];
+  if (cudaMemcpyAsync(h, ctls, sizeof(RoundCtl) * 2 * n_slices, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return DFX_E_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return DFX_E_CUDA;
+  stats->rounds[0] = stats->rounds[1] = 0;
+  stats->evaluated = stats->rows_read = stats->rows_written = 0;
+  stats->kernel_ms = 0.f;
+  for (int k = 0; k < 2 * n_slices; k++) {
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, ev[2 * k], ev[2 * k + 1]);
+    stats->kernel_ms += kms;
+    const RoundCtl& c = h[k];
+    const int phase = k & 1;
+    if (c.rounds > stats->rounds[phase]) stats->rounds[phase] = c.rounds;
+    stats->evaluated += (int64_t)c.tot_eval;
+    stats->rows_read += (int64_t)c.tot_read;
+    stats->rows_written += (int64_t)c.tot_written;
+    if (trace)
+      for (int r = 1; r <= c.rounds && r <= kTraceRounds; r++)
+        fprintf(stderr, "dfx-trace slice %d phase %d round %d evaluated %llu changed %llu rows_read %llu "
+                "rows_written %llu round_us %.1f\n", k >> 1, phase, r, c.cnt[r].evaluated,
+                c.cnt[r].changed, c.cnt[r].rows_read, c.cnt[r].rows_written,
+                r > 1 ? (c.t_end[r] - c.t_end[r - 1]) / 1e3 : 0.0);
   }
   return DFX_OK;
 }

@@ -164,3 +164,29 @@ def test_async_solves_back_to_back_reach_the_fixpoint():
     assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
     st = prob.solve()
     assert st.rounds_h >= 2
+
+
+def test_long_backward_propagation_hundreds_of_rounds():
+    """A reversed chain (pred of n is n+1) propagates one node per round
+    against the sweep order: ~N rounds.  Exercises the unbounded round loop
+    and the wrap of the per-edge seen bytes (> 255 rounds)."""
+    n, words = 700, 4
+    rng = np.random.default_rng(1)
+    row_ptr = np.zeros(n + 1, dtype=np.int32)
+    row_ptr[1:] = np.arange(1, n + 1, dtype=np.int32)
+    row_ptr[n] = n - 1                       # the last node is the entry
+    col = np.arange(1, n, dtype=np.int32)    # pred(n) = n + 1
+    kind = np.zeros(n, dtype=np.uint8)
+    kind[-50:] = 1                           # kernel nodes at the far end write
+    W = np.zeros((n, words), dtype=np.uint32)
+    W[-50:] = rng.integers(0, 2**32, size=(50, words), dtype=np.uint32)
+    R = np.zeros_like(W)
+    R[:: 7] = rng.integers(0, 2**32, size=R[:: 7].shape, dtype=np.uint32) & 0x01010101
+    S = np.zeros(words, dtype=np.uint32)
+    g = {"row_ptr": row_ptr, "col": col, "kind": kind, "A": R | W, "B": W, "USE": R, "S": S}
+    prob = CsrProblem.from_arrays(row_ptr, col, kind, R, W, S)
+    st = prob.solve()
+    OH, OD, _ = prob.download(True, True)
+    eh, ed, _ = _oracle.c3_solve(g)
+    assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
+    assert max(st.rounds_h, st.rounds_d) > 256

@@ -190,3 +190,31 @@ def test_long_backward_propagation_hundreds_of_rounds():
     eh, ed, _ = _oracle.c3_solve(g)
     assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
     assert max(st.rounds_h, st.rounds_d) > 256
+
+
+def test_acc_lists_edge_cases():
+    """List forms at the edges: no accesses at all, the widest variable
+    space (V = 16384: 14-bit variable ids, four 4096-variable slices), and a
+    too-small output capacity (DFX_E_NOSPC, then the exact size)."""
+    rng = np.random.default_rng(5)
+    # no accesses: every state stays at its boundary value, no requirements
+    row_ptr, col, kind, R, W, S = _mfp_ref.random_graph(rng, 300, 4)
+    R[:] = 0
+    W[:] = 0
+    off, acc = planes_to_acc(R, W)
+    assert acc.shape[0] == 0
+    prob = CsrProblem.from_acc(row_ptr, col, kind, off, acc, S, 4)
+    prob.solve()
+    rl = prob.requirements_list()
+    assert rl.vars.shape[0] == 0 and not rl.row_off.any()
+    # V = 16384
+    row_ptr, col, kind, R, W, S = _mfp_ref.random_graph(rng, 200, 512)
+    g = {"row_ptr": row_ptr, "col": col, "kind": kind, "A": R | W, "B": W, "USE": R, "S": S}
+    off, acc = planes_to_acc(R, W)
+    assert int((acc & 0x3FFF).max()) >= 16000
+    prob = CsrProblem.from_acc(row_ptr, col, kind, off, acc, S, 512)
+    prob.solve()
+    eh, ed, _ = _oracle.c3_solve(g)
+    OH, OD, _ = prob.download(True, True)
+    assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
+    _check_lists(prob.requirements_list(capacity=1), g, eh, ed)   # NOSPC, then exact

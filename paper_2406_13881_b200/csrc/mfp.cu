@@ -503,13 +503,15 @@ requirements_kernel(CsrDev p, int32_t* counts, int count_bits, int n_lo, int n_h
     uint4 ih[VPL], id[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; v++) { ih[v] = all4(); id[v] = re == rs ? zero4() : all4(); }
+    // host nodes read only IN_H; kernel nodes read IN_D, and IN_H only on
+    // the scalar quads (the firstprivate term F is zero elsewhere)
     for (int e = rs; e < re; e++) {
       const int q = __ldg(p.col + e);
 #pragma unroll
       for (int v = 0; v < VPL; v++)
         if (active[v]) {
-          ih[v] = and4(ih[v], ldg4(OH + (size_t)q * nq + lane + 32 * v));
-          id[v] = and4(id[v], ldg4(OD + (size_t)q * nq + lane + 32 * v));
+          if (!kern || nz4(smask[v])) ih[v] = and4(ih[v], ldg4(OH + (size_t)q * nq + lane + 32 * v));
+          if (kern) id[v] = and4(id[v], ldg4(OD + (size_t)q * nq + lane + 32 * v));
         }
     }
     int cnt = 0;

@@ -348,6 +348,27 @@ int32_t dfx_cg_nsp(dfx_cg *cg);
 int dfx_cg_wave(dfx_handle *h, dfx_cg *cg, const dfx_cg_tables *prev, dfx_cg_tables *cur,
                 int32_t wave, int32_t shard, int32_t nshards, int32_t *changed);
 
+/* Fused multi-GPU kernel (c) over peer memory (NVLink P2P via CUDA IPC).
+ * One process per GPU, one dfx_cgp per process.  A wave's functions are
+ * split round-robin over the ranks; the kernel that rebuilds a function's
+ * summary row also stores it into every peer's tables, and a wave ends when
+ * every rank has released its arrival on every peer (system-scope atomics).
+ * This replaces the NCCL path's all-gather after each wave.  Protocol:
+ *   dfx_cgp_create on every rank  ->  exchange the DFX_IPC_HANDLE_BYTES
+ *   handles (e.g. an all-gather of bytes)  ->  dfx_cgp_connect(handles of
+ *   ranks 0..nranks-1)  ->  dfx_cgp_solve on every rank (same number of
+ *   solves on every rank; no rank may start solve k+1 before every rank
+ *   returned from solve k).  out receives the same summaries on every rank.
+ * A peer that never arrives makes dfx_cgp_solve fail with DFX_E_CUDA after
+ * a bounded wait instead of hanging. */
+#define DFX_IPC_HANDLE_BYTES 64
+typedef struct dfx_cgp dfx_cgp;
+int dfx_cgp_create(dfx_handle *h, const dfx_cg_in *in, int32_t nranks, int32_t rank, dfx_cgp **out);
+int dfx_cgp_handle(dfx_cgp *p, void *ipc_handle);
+int dfx_cgp_connect(dfx_handle *h, dfx_cgp *p, const void *ipc_handles);
+int dfx_cgp_solve(dfx_handle *h, dfx_cgp *p, dfx_cg_out *out);
+int dfx_cgp_destroy(dfx_handle *h, dfx_cgp *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -983,6 +983,183 @@ int dfx_cg_wave(dfx_handle* h, dfx_cg* c, const dfx_cg_tables* prev, dfx_cg_tabl
   return DFX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// fused multi-GPU kernel (c) over peer memory (dfx_cgp_*)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct dfx_cgp {
+  dfx_cg* cg = nullptr;                 // static arrays (direct, sources, bindings, waves)
+  std::vector<int32_t> wave_off;
+  int nranks = 1, rank = 0, maxp = 1, nf = 0, ns = 0, nsp = 32;
+  void* block = nullptr;                // this rank's exchange block
+  size_t off_bits[2], off_list[2], off_len[2], off_arrive = 0, off_changed = 0, bytes = 0;
+  void* base[dfx::kMaxPeers] = {};      // every rank's block (peers opened by IPC)
+  bool opened[dfx::kMaxPeers] = {};
+  dfx::PeerTables tab{};
+  unsigned int* blocks_done = nullptr;
+  int* err = nullptr;
+  unsigned long long steps = 0;         // waves completed over all solves
+  int gen = 0;                          // solves started
+  const dfx_cg_in* in = nullptr;        // host inputs (init tables), kept by the caller
+};
+
+namespace {
+int cgp_destroy_impl(dfx_cgp* p) {
+  if (!p) return DFX_OK;
+  for (int r = 0; r < p->nranks && r < dfx::kMaxPeers; r++)
+    if (p->opened[r]) cudaIpcCloseMemHandle(p->base[r]);
+  if (p->block) cudaFree(p->block);
+  if (p->blocks_done) cudaFree(p->blocks_done);
+  if (p->err) cudaFree(p->err);
+  if (p->cg) cg_destroy_impl(p->cg);
+  delete p;
+  return DFX_OK;
+}
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+}  // namespace
+
+extern "C" {
+
+int dfx_cgp_create(dfx_handle* h, const dfx_cg_in* in, int32_t nranks, int32_t rank, dfx_cgp** out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_cgp_create: null argument");
+  if (nranks < 1 || nranks > dfx::kMaxPeers || rank < 0 || rank >= nranks)
+    return fail(DFX_E_ARG, "dfx_cgp_create: rank %d of %d (at most %d ranks)", rank, nranks, dfx::kMaxPeers);
+  CK(cudaSetDevice(h->device));
+  auto* p = new dfx_cgp();
+  int rc = dfx_cg_create(h, in, &p->cg);
+  if (rc) { delete p; return rc; }
+  p->nranks = nranks; p->rank = rank; p->in = in;
+  p->nf = in->n_funcs; p->ns = in->n_slots; p->nsp = p->cg->g.nsp;
+  p->maxp = in->max_passes > 0 ? in->max_passes : 1;
+  p->wave_off.assign(in->wave_off, in->wave_off + in->n_waves + 1);
+  p->cg->g.h_wave_off = p->wave_off.data();
+  const size_t rows = (size_t)(p->nf > 0 ? p->nf : 1);
+  size_t o = 0;
+  for (int k = 0; k < 2; k++) {
+    p->off_bits[k] = o; o = align256(o + rows * p->nsp);
+    p->off_list[k] = o; o = align256(o + 2 * rows * p->nsp);
+    p->off_len[k] = o; o = align256(o + 4 * rows);
+  }
+  p->off_arrive = o; o = align256(o + sizeof(unsigned long long));
+  p->off_changed = o; o = align256(o + sizeof(int) * (size_t)(p->maxp + 2));
+  p->bytes = o;
+  if (cudaMalloc(&p->block, p->bytes) != cudaSuccess || cudaMalloc(&p->blocks_done, 64) != cudaSuccess ||
+      cudaMalloc(&p->err, 64) != cudaSuccess) {
+    cgp_destroy_impl(p);
+    return fail(DFX_E_CUDA, "dfx_cgp_create: allocation failed");
+  }
+  // counters and flags start at zero and are never cleared afterwards
+  CK(cudaMemset(p->block, 0, p->bytes));
+  CK(cudaMemset(p->err, 0, 64));
+  CK(cudaDeviceSynchronize());
+  *out = p;
+  return DFX_OK;
+}
+
+int dfx_cgp_handle(dfx_cgp* p, void* ipc_handle) {
+  if (!p || !ipc_handle) return fail(DFX_E_ARG, "dfx_cgp_handle: null argument");
+  cudaIpcMemHandle_t hd;
+  CK(cudaIpcGetMemHandle(&hd, p->block));
+  static_assert(sizeof(hd) == DFX_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(ipc_handle, &hd, sizeof hd);
+  return DFX_OK;
+}
+
+int dfx_cgp_connect(dfx_handle* h, dfx_cgp* p, const void* ipc_handles) {
+  if (!h || !p || !ipc_handles) return fail(DFX_E_ARG, "dfx_cgp_connect: null argument");
+  CK(cudaSetDevice(h->device));
+  for (int r = 0; r < p->nranks; r++) {
+    if (r == p->rank) { p->base[r] = p->block; continue; }
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, (const char*)ipc_handles + (size_t)r * DFX_IPC_HANDLE_BYTES, sizeof hd);
+    CK(cudaIpcOpenMemHandle(&p->base[r], hd, cudaIpcMemLazyEnablePeerAccess));
+    p->opened[r] = true;
+  }
+  for (int r = 0; r < p->nranks; r++) {
+    char* b = (char*)p->base[r];
+    for (int k = 0; k < 2; k++) {
+      p->tab.bits[r][k] = (uint8_t*)(b + p->off_bits[k]);
+      p->tab.list[r][k] = (int16_t*)(b + p->off_list[k]);
+      p->tab.len[r][k] = (int32_t*)(b + p->off_len[k]);
+    }
+    p->tab.arrive[r] = (unsigned long long*)(b + p->off_arrive);
+    p->tab.changed[r] = (int*)(b + p->off_changed);
+  }
+  return DFX_OK;
+}
+
+int dfx_cgp_solve(dfx_handle* h, dfx_cgp* p, dfx_cg_out* out) {
+  if (!h || !p || !out) return fail(DFX_E_ARG, "dfx_cgp_solve: null argument");
+  if (!p->base[p->rank]) return fail(DFX_E_ARG, "dfx_cgp_solve: not connected");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const dfx_cg_in* in = p->in;
+  const int nf = p->nf, ns = p->ns, nsp = p->nsp;
+  const int gen = ++p->gen;
+  // pass-0 tables into t0 (local; peers only write t1 during pass 1)
+  auto* d_stage = (uint8_t*)dbuf(h, "cgp_stage", 2 * (size_t)(nf > 0 ? nf : 1) * nsp + 16);
+  if (!d_stage) return fail(DFX_E_CUDA, "dfx_cgp_solve: allocation failed");
+  if (nf && ns) {
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = 0;
+    CK(cudaMemcpyAsync(d_stage, in->init_bits, nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(d_stage, ns, p->tab.bits[p->rank][0], nsp, ns, nf, st);
+    CK(cudaMemcpyAsync(d_stage, in->init_list, 2 * nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(d_stage, 2 * (size_t)ns, p->tab.list[p->rank][0], 2 * (size_t)nsp, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(DFX_E_CUDA, "dfx_cgp_solve: repitch failed");
+  }
+  if (nf) CK(cudaMemcpyAsync(p->tab.len[p->rank][0], in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  const int n_waves = (int)p->wave_off.size() - 1;
+  const long long spins = 20000000;       // ~4 s of polling before a peer is declared lost
+  int passes = 0, launches = 0;
+  CK(cudaEventRecord(h->ev0, st));
+  for (int pass = 1; pass <= p->maxp; pass++) {
+    passes = pass;
+    const int cur = pass & 1;              // pass 1 reads t0, writes t1
+    for (int w = 0; w < n_waves; w++) {
+      int rc = dfx::cg_peer_wave(p->cg->g, p->tab, cur, w, p->rank, p->nranks, pass, gen,
+                                 p->blocks_done, st);
+      p->steps++;
+      if (!rc) rc = dfx::cg_peer_wait(p->tab.arrive[p->rank], p->steps * (unsigned long long)p->nranks,
+                                      spins, p->err, st);
+      if (rc) return fail(rc, "cg_peer_wave failed: %s", cudaGetErrorString(cudaGetLastError()));
+      launches += 2;
+    }
+    int flag = 0, err = 0;
+    CK(cudaMemcpyAsync(&flag, p->tab.changed[p->rank] + pass, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&err, p->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (err) return fail(DFX_E_CUDA, "dfx_cgp_solve: a peer did not arrive (pass %d)", pass);
+    if (flag != gen) break;                // no rank changed a set in this pass
+  }
+  CK(cudaEventRecord(h->ev1, st));
+  const int last = passes & 1;
+  if (nf && ns) {
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = dfx::repitch(p->tab.bits[p->rank][last], nsp, d_stage, ns, ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_cgp_solve: repitch failed");
+    CK(cudaMemcpyAsync(out->bits, d_stage, nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rc0 = dfx::repitch(p->tab.list[p->rank][last], 2 * (size_t)nsp, d_stage, 2 * (size_t)ns, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_cgp_solve: repitch failed");
+    CK(cudaMemcpyAsync(out->list, d_stage, 2 * nb, cudaMemcpyDeviceToHost, st));
+  }
+  if (nf) CK(cudaMemcpyAsync(out->len, p->tab.len[p->rank][last], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  out->kernel_ms = ms;
+  out->passes = passes;
+  out->launches = launches;
+  return DFX_OK;
+}
+
+int dfx_cgp_destroy(dfx_handle* h, dfx_cgp* p) {
+  if (h) cudaSetDevice(h->device);
+  return cgp_destroy_impl(p);
+}
+
 // replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
 int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");

@@ -111,6 +111,20 @@ int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8
             cudaStream_t st);
 int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size_t rows,
             cudaStream_t st);
+
+// fused multi-GPU kernel (c) over peer memory (summ.cu, dfx_cgp_*)
+constexpr int kMaxPeers = 8;
+struct PeerTables {                 // every rank's exchange block, mapped here
+  uint8_t* bits[kMaxPeers][2];
+  int16_t* list[kMaxPeers][2];
+  int32_t* len[kMaxPeers][2];
+  unsigned long long* arrive[kMaxPeers];   // waves finished, summed over ranks
+  int* changed[kMaxPeers];                 // [max_passes + 1] per-pass flags (= generation if changed)
+};
+int cg_peer_wave(const CgDev& g, const PeerTables& tab, int cur, int wave, int rank, int nranks,
+                 int pass, int gen, unsigned int* blocks_done, cudaStream_t st);
+int cg_peer_wait(const unsigned long long* arrive, unsigned long long expect, long long spins,
+                 int* err, cudaStream_t st);
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
              int* d_passes, cudaStream_t st);

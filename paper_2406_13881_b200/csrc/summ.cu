@@ -247,4 +247,113 @@ int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1,
   return DFX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// cgpeer.cu -- kernel (c) across GPUs with the exchange fused into the
+// producing kernel, over peer memory (NVLink P2P through CUDA IPC).
+//
+// The reference's pass schedule (interproc.py:105-143) runs wave by wave;
+// a wave's functions are split round-robin over the ranks.  In the NCCL
+// path (distributed.py) every rank rebuilds its share, then the ranks
+// all-gather the rebuilt rows and scatter them into their tables.  Here the
+// kernel that rebuilds a function's summary row also stores it straight into
+// every peer's table (one warp-wide coalesced copy per peer), so the rows
+// cross NVLink while other warps are still computing.  A wave ends when
+// every rank's wave kernel has released its arrival on every peer:
+//   writer: row stores -> fence.sc.sys -> (last block) atomicAdd_system on
+//           each rank's arrival counter
+//   reader: a one-warp wait kernel acquires (ld.acquire.sys) its own
+//           counter until it reaches waves_done * nranks; the next wave's
+//           kernel is stream-ordered after it.
+// The changed flag of a pass is raised on every rank's flag the same way
+// (atomicMax of the solve's generation number, so flags need no clearing
+// between solves), so every rank takes the same termination decision.
+constexpr unsigned FULLP = 0xFFFFFFFFu;
+constexpr int kPeerWarps = 8;
+
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kPeerWarps * 32)
+cg_wave_peer_kernel(CgDev g, PeerTables tab, int cur, int lo, int hi, int rank, int nranks,
+                    int pass, int gen, unsigned int* blocks_done) {
+  extern __shared__ uint32_t seen_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int prev = cur ^ 1;
+  const size_t nsp = (size_t)g.nsp;
+  uint8_t* const lbits = tab.bits[rank][cur];
+  int16_t* const llist = tab.list[rank][cur];
+  int32_t* const llen = tab.len[rank][cur];
+  bool any = false;
+  for (int pos = lo + rank + nranks * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); pos < hi;
+       pos += nranks * warps) {
+    const int f = __ldg(g.wave_fns + pos);
+    const CgBuf pb{tab.bits[rank][prev], tab.list[rank][prev], tab.len[rank][prev]};
+    const CgBuf cb{lbits, llist, llen};
+    any |= cg_function(g, pb, cb, f, seen, lane);
+    __syncwarp();
+    // the rebuilt row goes to every peer's table (16-B lanes, coalesced)
+    const uint4* sb = reinterpret_cast<const uint4*>(lbits + (size_t)f * nsp);
+    const uint4* sl = reinterpret_cast<const uint4*>(llist + (size_t)f * nsp);
+    const int len = __ldcg(llen + f);
+    for (int r = 0; r < nranks; r++) {
+      if (r == rank) continue;
+      uint4* db = reinterpret_cast<uint4*>(tab.bits[r][cur] + (size_t)f * nsp);
+      uint4* dl = reinterpret_cast<uint4*>(tab.list[r][cur] + (size_t)f * nsp);
+      for (int q = lane; q < (int)(nsp / 16); q += 32) __stcg(db + q, __ldcg(sb + q));
+      for (int q = lane; q < (int)(nsp / 8); q += 32) __stcg(dl + q, __ldcg(sl + q));
+      if (lane == 0) tab.len[r][cur][f] = len;
+    }
+  }
+  if (__any_sync(FULLP, any) && lane == 0)
+    for (int r = 0; r < nranks; r++) atomicMax_system(tab.changed[r] + pass, gen);
+  // release: this block's peer stores, then (last block) the arrivals
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev_done = atomicAdd(blocks_done, 1u);
+    if (prev_done == gridDim.x - 1) {
+      __threadfence_system();
+      for (int r = 0; r < nranks; r++) atomicAdd_system(tab.arrive[r], 1ull);
+    }
+  }
+}
+
+// one warp: wait until every rank has finished `waves` waves (acquire), or
+// give up after `spins` polls (a peer that never arrives) with *err = 1
+__global__ void cg_wait_kernel(const unsigned long long* arrive, unsigned long long expect,
+                               long long spins, int* err) {
+  if (threadIdx.x != 0) return;
+  for (long long i = 0; i < spins; i++) {
+    if (ld_acquire_sys(arrive) >= expect) return;
+    __nanosleep(200);
+  }
+  atomicExch(err, 1);
+}
+
+int cg_peer_wave(const CgDev& g, const PeerTables& tab, int cur, int wave, int rank, int nranks,
+                 int pass, int gen, unsigned int* blocks_done, cudaStream_t st) {
+  const int lo = g.h_wave_off[wave], hi = g.h_wave_off[wave + 1];
+  const int n = (hi - lo + nranks - 1) / nranks;
+  int blocks = (n + kPeerWarps - 1) / kPeerWarps;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;            // an empty share still signals its arrival
+  const size_t smem = (size_t)kPeerWarps * (g.nsp / 32) * sizeof(uint32_t);
+  if (cudaMemsetAsync(blocks_done, 0, sizeof(unsigned int), st) != cudaSuccess) return DFX_E_CUDA;
+  cg_wave_peer_kernel<<<blocks, kPeerWarps * 32, smem, st>>>(g, tab, cur, lo, hi, rank, nranks,
+                                                             pass, gen, blocks_done);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int cg_peer_wait(const unsigned long long* arrive, unsigned long long expect, long long spins,
+                 int* err, cudaStream_t st) {
+  cg_wait_kernel<<<1, 32, 0, st>>>(arrive, expect, spins, err);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 }  // namespace dfx

@@ -143,3 +143,59 @@ class ShardedSummaries:
             self.close()
         except Exception:
             pass
+
+
+class PeerSummaries:
+    """Kernel (c) across GPUs with the exchange fused into the producing
+    kernel (`dfx_cgp_*`, csrc/summ.cu `cg_wave_peer_kernel`): the kernel that
+    rebuilds a function's summary row stores it into every rank's tables over
+    peer memory (NVLink P2P through CUDA IPC), and a wave ends on
+    system-scope arrival counters -- no all-gather.  The IPC handles of the
+    ranks' exchange blocks are swapped once, through `torch.distributed`."""
+
+    def __init__(self, g, rank: int = 0, world: int = 1, eng: _abi.Engine | None = None,
+                 max_passes: int | None = None):
+        from .interproc import cg_struct
+        self.g = g
+        self.rank, self.world = rank, world
+        self.eng = eng or _abi.engine()
+        lib = self.eng.lib
+        for n in ("dfx_cgp_create", "dfx_cgp_handle", "dfx_cgp_connect", "dfx_cgp_solve",
+                  "dfx_cgp_destroy"):
+            getattr(lib, n).restype = C.c_int
+        self._keep: list = []
+        self.cin = cg_struct(g, self._keep, max_passes or max(16, g.n_funcs + 1))
+        h = C.c_void_p()
+        self.eng.check(lib.dfx_cgp_create(self.eng.h, C.byref(self.cin), C.c_int32(world),
+                                          C.c_int32(rank), C.byref(h)), "dfx_cgp_create")
+        self.h = h
+        mine = (C.c_char * 64)()
+        self.eng.check(lib.dfx_cgp_handle(h, mine), "dfx_cgp_handle")
+        handles = [bytes(mine)]
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(mine))
+        allh = (C.c_char * (64 * world)).from_buffer_copy(b"".join(handles))
+        self.eng.check(lib.dfx_cgp_connect(self.eng.h, h, allh), "dfx_cgp_connect")
+
+    def solve(self):
+        """Returns (bits uint8 [nf, ns], list int16 [nf, ns], len int32, passes)."""
+        from .interproc import CgOut
+        bits = np.zeros(self.g.init_bits.shape, dtype=np.uint8)
+        lst = np.zeros(self.g.init_list.shape, dtype=np.int16)
+        ln = np.zeros(self.g.n_funcs, dtype=np.int32)
+        out = CgOut(bits.ctypes.data, lst.ctypes.data, ln.ctypes.data, 0, 0, 0.0)
+        self.eng.check(self.eng.lib.dfx_cgp_solve(self.eng.h, self.h, C.byref(out)), "dfx_cgp_solve")
+        self.kernel_ms = float(out.kernel_ms)
+        return bits, lst, ln, int(out.passes)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.eng.lib.dfx_cgp_destroy(self.eng.h, self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

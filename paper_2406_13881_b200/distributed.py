@@ -45,9 +45,6 @@ class ShardedSummaries:
             lst = torch.zeros((nf, self.nsp), dtype=torch.int16, device=self.device)
             ln = torch.zeros(nf, dtype=torch.int32, device=self.device)
             self.t.append({"bits": bits, "list": lst, "len": ln})
-        self.t[0]["bits"][:, :ns] = torch.from_numpy(g.init_bits)
-        self.t[0]["list"][:, :ns] = torch.from_numpy(g.init_list)
-        self.t[0]["len"][:] = torch.from_numpy(g.init_len)
         self.wave_impl = wave_impl or self._gpu_wave
         self.cg = None
         self.launches = 0
@@ -109,9 +106,21 @@ class ShardedSummaries:
             t["bits"].index_copy_(0, ids, rows[:, :self.nsp].contiguous())
             t["list"].index_copy_(0, ids, rows[:, self.nsp:3 * self.nsp].contiguous().view(torch.int16))
             t["len"].index_copy_(0, ids, rows[:, 3 * self.nsp:].contiguous().view(torch.int32).view(-1))
+        if self.device.type == "cuda":
+            # the next wave runs on the engine's stream: the scattered rows
+            # (written on torch's stream) must have landed
+            torch.cuda.current_stream(self.device).synchronize()
+
+    def _reset(self) -> None:
+        """Pass-0 summaries into table 0 (every solve starts from them)."""
+        ns = self.ns
+        self.t[0]["bits"][:, :ns] = torch.from_numpy(self.g.init_bits)
+        self.t[0]["list"][:, :ns] = torch.from_numpy(self.g.init_list)
+        self.t[0]["len"][:] = torch.from_numpy(self.g.init_len)
 
     def solve(self):
         """Returns (bits uint8 [nf, ns], list int16 [nf, ns], len int32, passes)."""
+        self._reset()
         prev, passes = 0, 0
         n_waves = self.g.wave_off.shape[0] - 1
         while passes < self.max_passes:

@@ -1,7 +1,8 @@
-"""GPU: the fused multi-GPU kernel-(c) path (dfx_cgp_*: rebuilt summary rows
-stored into every rank's tables over peer memory, system-scope arrival
-counters) run by two processes that share one GPU through CUDA IPC, against
-the CPU oracle and the single-GPU engine."""
+"""GPU: kernel (c) across ranks, run by two processes that share one GPU:
+the fused path (dfx_cgp_*: rebuilt summary rows stored into every rank's
+tables over peer memory through CUDA IPC, system-scope arrival counters) and
+the all-gather path (dfx_cg_wave + torch.distributed all-gather of the
+rebuilt rows), against the CPU oracle."""
 import os
 import socket
 
@@ -23,15 +24,18 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, seed, n):
+def _worker(rank, world, port, q, seed, n, path="peer"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        from paper_2406_13881_b200.distributed import PeerSummaries
+        import torch
+        from paper_2406_13881_b200.distributed import PeerSummaries, ShardedSummaries
         from paper_2406_13881_b200.gen.c5 import generate_c5
+        torch.cuda.set_device(0)
         g = generate_c5(seed=seed, n_funcs=n, depth=12, n_globals=64, p_back=0.25)
-        ps = PeerSummaries(g, rank, world)
+        ps = PeerSummaries(g, rank, world) if path == "peer" else \
+            ShardedSummaries(g, rank, world, device="cuda:0")
         res = []
         for _ in range(2):                      # two solves: flags and counters carry over
             res.append(ps.solve())
@@ -43,8 +47,9 @@ def _worker(rank, world, port, q, seed, n):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("seed,n", [(3, 480), (8, 1200)])
-def test_peer_fused_summaries_two_ranks_one_gpu(seed, n):
+@pytest.mark.parametrize("seed,n,path", [(3, 480, "peer"), (8, 1200, "peer"),
+                                         (3, 480, "allgather")])
+def test_summaries_two_ranks_one_gpu(seed, n, path):
     from paper_2406_13881_b200.gen.c5 import generate_c5
     from paper_2406_13881_b200.interproc import solve_call_graph
     g = generate_c5(seed=seed, n_funcs=n, depth=12, n_globals=64, p_back=0.25)
@@ -54,7 +59,7 @@ def test_peer_fused_summaries_two_ranks_one_gpu(seed, n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, seed, n)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, seed, n, path)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=240) for _ in procs]

@@ -190,6 +190,9 @@ class _Lowerer:
         self.stmt_index: dict[int, int] = {}
         self.stmts: list = []
         self._site_cache: dict = {}
+        self._dev_read_sub: dict | None = None
+        self._dev_by_node: dict | None = None
+        self._fiv_cache: dict = {}
         self._norm_cache: dict = {}
         # structural bounds for engine resources
         self.loop_depth = 0
@@ -295,7 +298,7 @@ class _Lowerer:
             self.sites.extend([len(loops), acc_code])
             for f in loops:
                 code = self.norm_code(f)
-                v = find_indexing_var(f)
+                v = self.find_indexing_var(f)
                 if v is not None and v in idx_vars:
                     code |= AC_QUAL
                 if not self.writes_between(var, f.span.start, read_pos):
@@ -304,17 +307,40 @@ class _Lowerer:
         self._site_cache[key] = off
         return off
 
+    def find_indexing_var(self, f):
+        """`bounds.find_indexing_var`, memoised per loop statement."""
+        k = id(f)
+        if k not in self._fiv_cache:
+            self._fiv_cache[k] = find_indexing_var(f)
+        return self._fiv_cache[k]
+
+    def kernel_rw_sets(self, node_id, kernel_ast):
+        """`access.kernel_rw_sets` (`access.py:405-427`) over the kernel
+        node's device accesses only (grouped once per function, in access
+        order) instead of a scan of every access per kernel."""
+        by = self._dev_by_node
+        if by is None:
+            by = self._dev_by_node = {}
+            for acc in self.accesses:
+                if acc.space is Space.DEVICE:
+                    by.setdefault(acc.cfg_node, []).append(acc)
+        return kernel_rw_sets(by.get(node_id, ()), node_id, kernel_ast)
+
     def device_read_subscript(self, var, kernel_stmt):
-        """`_device_read_subscript` (`dataflow.py:380-390`)."""
+        """`_device_read_subscript` (`dataflow.py:380-390`): the subscript of
+        the first device read of `var` at the kernel's node, in access order
+        (indexed once per function instead of a scan per call)."""
         node = self.cfg.node_of_ast.get(kernel_stmt)
         if node is None:
             return None
-        for acc in self.accesses:
-            if (acc.cfg_node == node.id and acc.space is Space.DEVICE
-                    and acc.var is var and reads(acc.kind)
-                    and acc.subscript is not None):
-                return acc.subscript
-        return None
+        idx = self._dev_read_sub
+        if idx is None:
+            idx = self._dev_read_sub = {}
+            for acc in self.accesses:
+                if (acc.space is Space.DEVICE and reads(acc.kind)
+                        and acc.subscript is not None):
+                    idx.setdefault((acc.cfg_node, id(acc.var)), acc.subscript)
+        return idx.get((node.id, id(var)))
 
     # ---- access ops ------------------------------------------------------
     def op_hr(self, var, stmt, subscript, override):
@@ -412,12 +438,12 @@ class _Lowerer:
             if stmt.children:
                 self.exec_stmt(stmt.children[0])
             return
-        entry_reads, kernel_writes = kernel_rw_sets(self.accesses, node.id, stmt)
+        entry_reads, kernel_writes = self.kernel_rw_sets(node.id, stmt)
         kw = set(kernel_writes)
         captured = _clause_names(info, "firstprivate")
         private = _clause_names(info, "private") | _clause_names(info, "linear")
         for f in stmt.find_all(NodeKind.FOR_STMT):
-            v = find_indexing_var(f)
+            v = self.find_indexing_var(f)
             if v is not None:
                 private.add(v)
         for var in sorted(entry_reads, key=lambda v: v.name):

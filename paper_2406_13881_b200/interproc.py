@@ -62,20 +62,32 @@ def _eff_bits(kind, spaces) -> int:
     return b
 
 
-def _bits_kind(b: int):
+def _kind_of(b: int):
     r, w = b & BIT_R, b & BIT_W
     if r and w:
         return AccessKind.READWRITE
     return AccessKind.READ if r else AccessKind.WRITE
 
 
-def _bits_spaces(b: int) -> frozenset:
+def _spaces_of(b: int) -> frozenset:
     s = set()
     if b & BIT_H:
         s.add(Space.HOST)
     if b & BIT_D:
         s.add(Space.DEVICE)
     return frozenset(s)
+
+
+_KIND_OF = [_kind_of(b) for b in range(16)]
+_SPACES_OF = [_spaces_of(b) for b in range(16)]
+
+
+def _bits_kind(b: int):
+    return _KIND_OF[b & 15]
+
+
+def _bits_spaces(b: int) -> frozenset:
+    return _SPACES_OF[b & 15]
 
 
 def _force_dev(b: int) -> int:
@@ -131,7 +143,8 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
     pess = {name: pessimistic_summary(fn) for name, fn in declared.items() if name not in defined}
     names = list(defined)
     index = {n: i for i, n in enumerate(names)}
-    n_params = max([len(defined[n].params) for n in names] + [0])
+    params = {n: defined[n].params for n in names}      # `params` rescans children: once
+    n_params = max([len(params[n]) for n in names] + [0])
     gidx: dict[str, int] = {}
 
     def classify(fn_pidx, root):
@@ -147,7 +160,7 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
     per_fn = []
     for name in names:
         fn = defined[name]
-        pidx = {p: i for i, p in enumerate(fn.params)}
+        pidx = {p: i for i, p in enumerate(params[name])}
         items = []
         for acc in accesses[name]:                 # `_direct_effects` (:75-87)
             if acc.kind is AccessKind.UNKNOWN:
@@ -164,7 +177,7 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
             dev = cs.on_device
             if cs.callee in index:                 # defined callee (:119-131)
                 binds = []
-                for i in range(len(defined[cs.callee].params)):
+                for i in range(len(params[cs.callee])):
                     if i >= len(args):
                         continue
                     root = helper.pointerish_arg_root(args[i])
@@ -327,16 +340,22 @@ def summaries_from_result(g: CallGraph, r: CgResult) -> dict:
     `param_effects` / `global_effects` in insertion order."""
     out: dict[str, CallSummary] = dict(g.pess)
     P = g.n_params
+    eff_of = [Effect(_bits_kind(b), _bits_spaces(b)) for b in range(16)]   # frozen: shareable
+    lens = r.len.tolist()
+    globs = g.globals
     for f, name in enumerate(g.names):
         s = CallSummary(fn=name, defined=True)
-        for k in range(int(r.len[f])):
-            slot = int(r.list[f, k])
-            b = int(r.bits[f, slot])
-            eff = Effect(_bits_kind(b), _bits_spaces(b))
-            if slot < P:
-                s.param_effects[slot] = eff
-            else:
-                s.global_effects[g.globals[slot - P]] = eff
+        n = lens[f]
+        if n:
+            slots = r.list[f, :n].tolist()
+            bits = r.bits[f].tolist()
+            pe, ge = s.param_effects, s.global_effects
+            for slot in slots:
+                eff = eff_of[bits[slot] & 15]
+                if slot < P:
+                    pe[slot] = eff
+                else:
+                    ge[globs[slot - P]] = eff
         out[name] = s
     return out
 

@@ -327,14 +327,100 @@ class _Deferred:
         return self.plan
 
 
+# ---- parallel lowering -------------------------------------------------------
+# The lowering (the static half of `_Analyzer`) is pure Python and, once the
+# solve runs on the GPU, the host-side Amdahl limit for many functions
+# (SURVEY §8f rank 1).  Functions are independent, so large batches are
+# lowered by forked worker processes that see the parsed translation unit
+# copy-on-write.  Objects cannot cross processes, so a worker returns the
+# program's arrays with node and variable references as indices (a node's
+# child-index path from the function's AST root; index of an access naming
+# the variable), and the parent maps them back to its own objects -- the
+# FunctionPlan anchors stay the caller's AstNodes.
+_FORK_ITEMS: list = []
+_FORK_ALLOW: frozenset = frozenset()
+
+
+def _path(node, root) -> tuple:
+    """Child indices leading from `root` to `node`."""
+    steps = []
+    while node is not root:
+        p = node.parent
+        steps.append(next(i for i, c in enumerate(p.children) if c is node))
+        node = p
+    return tuple(reversed(steps))
+
+
+def _follow(root, path):
+    for i in path:
+        root = root.children[i]
+    return root
+
+
+def _lower_portable(i: int):
+    src, cfg, accs, table = _FORK_ITEMS[i]
+    try:
+        prog = lower_function(src, cfg, accs, table, _FORK_ALLOW)
+    except Exception as e:      # noqa: BLE001 -- re-raised by the parent's serial retry
+        return ("error", repr(e))
+    root = cfg.function
+    first = {}
+    for j, a in enumerate(accs):
+        first.setdefault(id(a.var), j)
+    try:
+        stmts = [_path(n, root) for n in prog.stmts]
+        kstmts = [_path(n, root) for n in prog.kernel_stmts]
+        region = None if prog.region is None else [_path(n, root) for n in prog.region]
+        vars_ = [first[id(v)] for v in prog.vars]
+    except (KeyError, AttributeError, StopIteration):
+        return ("serial", None)  # a reference not reachable this way: lower in the parent
+    fields = {k: getattr(prog, k) for k in ("ops", "var_flags", "stmt_span", "sites", "arms",
+                                            "region_begin_start", "n_slots", "max_loop_depth",
+                                            "max_br_depth", "max_arms")}
+    return ("ok", (fields, stmts, kstmts, region, vars_))
+
+
+def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | None = None):
+    """`lower_function` over a batch; forked workers for large batches
+    (`workers` or $DFX_LOWER_WORKERS, default min(16, cores); serial below
+    64 functions or with one worker)."""
+    import multiprocessing as mp
+    import os
+    if workers is None:
+        workers = int(os.environ.get("DFX_LOWER_WORKERS", "0")) or min(16, os.cpu_count() or 1)
+    if workers <= 1 or len(items) < 64 or "fork" not in mp.get_all_start_methods():
+        return [lower_function(src, cfg, accs, table, allow_stale)
+                for src, cfg, accs, table in items]
+    global _FORK_ITEMS, _FORK_ALLOW
+    _FORK_ITEMS, _FORK_ALLOW = list(items), allow_stale
+    try:
+        with mp.get_context("fork").Pool(workers) as pool:
+            res = pool.map(_lower_portable, range(len(items)),
+                           chunksize=max(1, len(items) // (8 * workers)))
+    finally:
+        _FORK_ITEMS, _FORK_ALLOW = [], frozenset()
+    progs = []
+    for (src, cfg, accs, table), (tag, r) in zip(items, res):
+        if tag != "ok":         # errors and unmappable programs: the serial path decides
+            progs.append(lower_function(src, cfg, accs, table, allow_stale))
+            continue
+        fields, stmts, kstmts, region, vars_ = r
+        root = cfg.function
+        progs.append(FnProgram(fn=root, **fields,
+                               vars=[accs[j].var for j in vars_],
+                               stmts=[_follow(root, q) for q in stmts],
+                               kernel_stmts=[_follow(root, q) for q in kstmts],
+                               region=None if region is None else tuple(_follow(root, q) for q in region)))
+    return progs
+
+
 def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
                       runner=None) -> list[_Deferred]:
     """Batched `analyze_function`: `items` is a list of
     `(src, cfg, accesses, table)`; one engine launch for all of them.
     Returns one deferred result per item (`.get()` returns the
     `FunctionPlan` or raises the reference's exception)."""
-    progs = [lower_function(src, cfg, accs, table, allow_stale)
-             for src, cfg, accs, table in items]
+    progs = lower_functions(items, allow_stale)
     batch = pack(progs)
     raw = run_replay(batch, runner=runner)
     order = np.argsort(raw.events["fn"], kind="stable")

@@ -150,6 +150,36 @@ class FnProgram:
         return len(self.vars)
 
 
+_STMT_KINDS = frozenset({
+    NodeKind.EXPR_STMT, NodeKind.DECL_STMT, NodeKind.RETURN_STMT,
+    NodeKind.IF_STMT, NodeKind.SWITCH_STMT, NodeKind.FOR_STMT,
+    NodeKind.WHILE_STMT, NodeKind.DO_STMT, NodeKind.OMP_DIRECTIVE,
+    NodeKind.BREAK_STMT, NodeKind.CONTINUE_STMT,
+})
+
+
+def _enclosing_statement(ast):
+    """`access.enclosing_statement` (`access.py:147-160`) with its statement-
+    kind set built once instead of per call."""
+    node = ast
+    while node is not None:
+        if node.kind in _STMT_KINDS:
+            return node
+        node = node.parent
+    return ast
+
+
+def _for_stmts(root):
+    """`root.find_all(NodeKind.FOR_STMT)` in the same (pre-)order, iteratively."""
+    out, stack = [], [root]
+    while stack:
+        n = stack.pop()
+        if n.kind is NodeKind.FOR_STMT:
+            out.append(n)
+        stack.extend(reversed(n.children))
+    return out
+
+
 class _Lowerer:
     """Static half of `_Analyzer` (`dataflow.py:194-734`)."""
 
@@ -168,7 +198,7 @@ class _Lowerer:
         for acc in accesses:
             if acc.space is Space.DEVICE and acc.cfg_node in self.kernel_node_ids:
                 continue
-            stmt = enclosing_statement(acc.ast)
+            stmt = _enclosing_statement(acc.ast)
             self.stmt_groups.setdefault(stmt, []).append(acc)
         self.region_block = self.region_begin = self.region_end = None
         if self.kernel_stmts:
@@ -442,7 +472,7 @@ class _Lowerer:
         kw = set(kernel_writes)
         captured = _clause_names(info, "firstprivate")
         private = _clause_names(info, "private") | _clause_names(info, "linear")
-        for f in stmt.find_all(NodeKind.FOR_STMT):
+        for f in _for_stmts(stmt):
             v = self.find_indexing_var(f)
             if v is not None:
                 private.add(v)

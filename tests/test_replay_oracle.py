@@ -75,3 +75,32 @@ def test_multithreaded_oracle_equals_sequential():
     mt = run_replay(b, runner=_oracle.replay_runner_mt)
     assert np.array_equal(seq.events, mt.events)
     assert np.array_equal(seq.var_out, mt.var_out)
+
+
+def test_parallel_lowering_equals_serial():
+    """Forked-worker lowering (dataflow.lower_functions) returns the serial
+    lowering exactly: same arrays, and references mapped back to the
+    caller's own AstNode / VariableId objects."""
+    if not have_dartomp():
+        pytest.skip("reference front end not importable")
+    import dartomp.pipeline as rp
+    from paper_2406_13881_b200.dataflow import lower_functions
+    from paper_2406_13881_b200.gen.cprog import GenConfig, generate
+    from paper_2406_13881_b200.lower import lower_function
+    a = rp.load(text=generate(11, GenConfig(n_funcs=70, n_stmts=12)))
+    items = [(a.src, a.cfgs[n], a.accesses[n], a.table) for n in a.cfgs]
+    par = lower_functions(items, workers=4)
+    for (src, cfg, accs, table), p in zip(items, par):
+        s = lower_function(src, cfg, accs, table)
+        for k in ("ops", "var_flags", "stmt_span", "sites", "arms"):
+            assert np.array_equal(getattr(p, k), getattr(s, k)), k
+        assert (p.region_begin_start, p.n_slots, p.max_loop_depth, p.max_br_depth,
+                p.max_arms) == (s.region_begin_start, s.n_slots, s.max_loop_depth,
+                                s.max_br_depth, s.max_arms)
+        assert p.fn is s.fn
+        assert all(x is y for x, y in zip(p.stmts, s.stmts)) and len(p.stmts) == len(s.stmts)
+        assert all(x is y for x, y in zip(p.vars, s.vars)) and len(p.vars) == len(s.vars)
+        assert all(x is y for x, y in zip(p.kernel_stmts, s.kernel_stmts))
+        assert (p.region is None) == (s.region is None)
+        if p.region is not None:
+            assert all(x is y for x, y in zip(p.region, s.region))

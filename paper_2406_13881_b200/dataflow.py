@@ -392,13 +392,27 @@ def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | 
         return [lower_function(src, cfg, accs, table, allow_stale)
                 for src, cfg, accs, table in items]
     global _FORK_ITEMS, _FORK_ALLOW
+    import warnings
     _FORK_ITEMS, _FORK_ALLOW = list(items), allow_stale
+    res = None
     try:
-        with mp.get_context("fork").Pool(workers) as pool:
-            res = pool.map(_lower_portable, range(len(items)),
-                           chunksize=max(1, len(items) // (8 * workers)))
+        # the workers run pure Python on the copied parse (no CUDA, no locks
+        # of the parent's other threads); a bounded wait falls back to the
+        # serial lowering if a worker ever stalls
+        with warnings.catch_warnings():
+            warnings.filterwarnings("ignore", message=".*multi-threaded.*fork.*",
+                                    category=DeprecationWarning)
+            with mp.get_context("fork").Pool(workers) as pool:
+                res = pool.map_async(_lower_portable, range(len(items)),
+                                     chunksize=max(1, len(items) // (8 * workers))
+                                     ).get(timeout=60 + 0.05 * len(items))
+    except mp.TimeoutError:
+        res = None
     finally:
         _FORK_ITEMS, _FORK_ALLOW = [], frozenset()
+    if res is None:
+        return [lower_function(src, cfg, accs, table, allow_stale)
+                for src, cfg, accs, table in items]
     progs = []
     for (src, cfg, accs, table), (tag, r) in zip(items, res):
         if tag != "ok":         # errors and unmappable programs: the serial path decides

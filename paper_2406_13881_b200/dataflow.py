@@ -208,36 +208,43 @@ def _raise_error(prog: FnProgram, src, ev) -> None:
                            % (prog.fn.name, kind))
 
 
+_PLAN_KIND = {_abi.EV_UPDATE_FROM: PlanKind.UPDATE_FROM,
+              _abi.EV_UPDATE_TO: PlanKind.UPDATE_TO,
+              _abi.EV_FIRSTPRIVATE: PlanKind.FIRSTPRIVATE}
+
+
 def decode(prog: FnProgram, src, accesses, events: np.ndarray,
-           var_out: np.ndarray) -> FunctionPlan:
-    """Events of one function (any order) + per-variable bits -> FunctionPlan."""
-    if events.shape[0]:
-        events = events[np.argsort(events["key"], kind="stable")]
-        errs = events[events["kind"] >= _abi.EV_ERR_DATAMAP]
-        if errs.shape[0]:
-            _raise_error(prog, src, errs[0])
+           var_out: np.ndarray, presorted: bool = False) -> FunctionPlan:
+    """Events of one function (any order, or key order with `presorted`) +
+    per-variable bits -> FunctionPlan."""
     updates: list = []
     firstprivates: list = []
     suppressed: list[str] = []
-    keys: set = set()
-    for ev in events:
-        kind = int(ev["kind"])
-        var = prog.vars[int(ev["var"])]
-        if kind == _abi.EV_SUPPRESS:
-            if var.name not in suppressed:
-                suppressed.append(var.name)
-            continue
-        anchor = prog.stmts[int(ev["node"])]
-        pos = _POS[int(ev["pos"])]
-        pk = {_abi.EV_UPDATE_FROM: PlanKind.UPDATE_FROM,
-              _abi.EV_UPDATE_TO: PlanKind.UPDATE_TO,
-              _abi.EV_FIRSTPRIVATE: PlanKind.FIRSTPRIVATE}[kind]
-        key = (pk, var.name, id(anchor), pos)           # `dataflow.py:264`
-        if key in keys:
-            continue
-        keys.add(key)
-        bucket = firstprivates if pk is PlanKind.FIRSTPRIVATE else updates
-        bucket.append(DirectivePlan(pk, (var.name,), anchor, pos))
+    if events.shape[0]:
+        if not presorted:
+            events = events[np.argsort(events["key"], kind="stable")]
+        kinds = events["kind"].tolist()
+        if max(kinds) >= _abi.EV_ERR_DATAMAP:
+            errs = events[events["kind"] >= _abi.EV_ERR_DATAMAP]
+            _raise_error(prog, src, errs[0])
+        keys: set = set()
+        pvars, pstmts, fp_kind = prog.vars, prog.stmts, PlanKind.FIRSTPRIVATE
+        for kind, vi, ni, pi in zip(kinds, events["var"].tolist(), events["node"].tolist(),
+                                    events["pos"].tolist()):
+            name = pvars[vi].name
+            if kind == _abi.EV_SUPPRESS:
+                if name not in suppressed:
+                    suppressed.append(name)
+                continue
+            anchor = pstmts[ni]
+            pos = _POS[pi]
+            pk = _PLAN_KIND[kind]
+            key = (pk, name, id(anchor), pos)           # `dataflow.py:264`
+            if key in keys:
+                continue
+            keys.add(key)
+            (firstprivates if pk is fp_kind else updates).append(
+                DirectivePlan(pk, (name,), anchor, pos))
     # sets (`dataflow.py:214-216`) and `_escape_liveness` (`:671-676`)
     presence, to_comp, from_comp = set(), set(), set()
     for i, var in enumerate(prog.vars):
@@ -437,7 +444,7 @@ def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
     progs = lower_functions(items, allow_stale)
     batch = pack(progs)
     raw = run_replay(batch, runner=runner)
-    order = np.argsort(raw.events["fn"], kind="stable")
+    order = np.lexsort((raw.events["key"], raw.events["fn"]))   # by function, then visit key
     evs = raw.events[order]
     bounds = np.searchsorted(evs["fn"], np.arange(len(progs) + 1))
     out = []
@@ -445,7 +452,8 @@ def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
         d = batch.fns[i]
         vo = raw.var_out[int(d["var_off"]):int(d["var_off"]) + int(d["n_vars"])]
         try:
-            out.append(_Deferred(plan=decode(p, src, accs, evs[bounds[i]:bounds[i + 1]], vo)))
+            out.append(_Deferred(plan=decode(p, src, accs, evs[bounds[i]:bounds[i + 1]], vo,
+                                             presorted=True)))
         except Exception as e:  # the reference's ToolError subclasses
             out.append(_Deferred(error=e))
     return out

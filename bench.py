@@ -487,8 +487,9 @@ def run_c4(args, rank, world, local):
                        "functions": cfg.n_funcs, "facts_total": facts_total,
                        "parallelism": "function-sharded (LPT), %d GPU(s)" % world,
                        "l2": "programs %.1f GB > 126 MB L2" % (batch.ops.nbytes / 1e9)},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": args.steps,
-            "replay": {"kernel": "replay_kernel", "kernel_ms_per_step": kernel_ms / args.steps,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 2 * args.steps,
+            "replay": {"kernel": "replay_kernel", "launches_per_step": ["region_kernel",
+                                                                       "replay_kernel"], "kernel_ms_per_step": kernel_ms / args.steps,
                        "events": n_ev, "functions_rank0": int(len(mine)),
                        "ops_rank0": int(batch.ops.shape[0])}}
     if world == 1 and not args.no_cpu_baseline:

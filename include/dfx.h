@@ -51,7 +51,11 @@ int dfx_close(dfx_handle *h);
 /* E1: exact schedule replay of `_Analyzer` (dataflow.py:194-734)            */
 /* ------------------------------------------------------------------------ */
 
-/* opcodes: low 8 bits of op word 0; flags above (see lower.py) */
+/* opcodes: low 8 bits of op word 0; flags above (see lower.py).
+ * Words 2-3 of BR_BEGIN / LOOP_BEGIN and word 3 of BR_END / LOOP_END are
+ * reserved: the library fills them in its device copy of the program with
+ * the region table (chunk mask, extent, dynamic length) that lets a warp
+ * skip a region none of its variables is accessed in. */
 enum {
   DFX_OP_END = 0, DFX_OP_HR = 1, DFX_OP_HW = 2, DFX_OP_DR = 3, DFX_OP_DW = 4,
   DFX_OP_BR_BEGIN = 5, DFX_OP_ARM_FORK = 6, DFX_OP_ARM_CLOSE = 7,

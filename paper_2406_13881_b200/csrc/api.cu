@@ -1,6 +1,7 @@
 // api.cu -- C ABI of libdfx.so (include/dfx.h): handles, buffers, entry points.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -16,17 +17,25 @@ struct dfx_csr;
 namespace { int csr_destroy_impl(dfx_csr* c); }
 
 struct dfx_handle {
-  static constexpr int kPipe = 8;     // chunks of the pipelined host-buffer calls
+  static constexpr int kPipe = 8;      // node ranges of the pipelined CSR calls
+  static constexpr int kPipeMax = 16;  // function ranges of dfx_replay_batch
+  static constexpr int kComp = 3;     // compute streams of dfx_replay_batch
   cudaStream_t s_copy = nullptr, s_d2h = nullptr;
-  cudaEvent_t pev[1 + 2 * kPipe] = {};
-  unsigned long long* pin_cnt = nullptr;   // pinned, kPipe counters
+  cudaStream_t s_comp[kComp] = {};    // [0] unused: the call's own stream
+  cudaEvent_t jev[kComp] = {};        // joins of the compute streams
+  cudaEvent_t pev[1 + 2 * kPipeMax] = {};
+  unsigned long long* pin_cnt = nullptr;   // pinned, kPipeMax counters
   cudaError_t pipeline_init() {
     if (s_copy) return cudaSuccess;
     cudaError_t e = cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking);
+    for (int i = 1; i < kComp; i++)
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_comp[i], cudaStreamNonBlocking);
+    for (auto& ev : jev)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     for (auto& ev : pev)
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaHostAlloc((void**)&pin_cnt, sizeof(unsigned long long) * kPipe, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&pin_cnt, sizeof(unsigned long long) * kPipeMax, cudaHostAllocDefault);
     return e;
   }
   int device = 0;
@@ -34,6 +43,10 @@ struct dfx_handle {
   cudaStream_t ext_stream = nullptr;  // caller's stream (dfx_set_stream)
   cudaStream_t st() const { return ext_stream ? ext_stream : stream; }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // DFX_TRACE=1: per-range timeline of the pipelined calls on stderr
+  // (H2D done, replay start / end, relative to the call's first event)
+  bool trace = false;
+  cudaEvent_t tev[3 * kPipeMax + 1] = {};
   struct dfx_csr* csr_cache = nullptr;   // reused by dfx_mfp_csr across calls
   std::unordered_map<std::string, std::pair<void*, size_t>> bufs;
 };
@@ -95,6 +108,9 @@ int dfx_open(int device, dfx_handle** out) {
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&h->ev0));
   CK(cudaEventCreate(&h->ev1));
+  if (const char* t = getenv("DFX_TRACE")) h->trace = t[0] == '1';
+  if (h->trace)
+    for (auto& e : h->tev) CK(cudaEventCreate(&e));
   *out = h;
   return DFX_OK;
 }
@@ -106,12 +122,18 @@ int dfx_close(dfx_handle* h) {
     if (kv.second.first) cudaFree(kv.second.first);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  for (auto& e : h->tev)
+    if (e) cudaEventDestroy(e);
   if (h->csr_cache) csr_destroy_impl(h->csr_cache);
   for (auto& ev : h->pev)
     if (ev) cudaEventDestroy(ev);
   if (h->pin_cnt) cudaFreeHost(h->pin_cnt);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+  for (auto& cs : h->s_comp)
+    if (cs) cudaStreamDestroy(cs);
+  for (auto& ev : h->jev)
+    if (ev) cudaEventDestroy(ev);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return DFX_OK;
@@ -141,6 +163,34 @@ struct dfx_replay {
   }
 };
 
+namespace {
+// Work items of functions [f0, f1): one per (function, 32-variable chunk), at
+// least one per function so statically known errors surface without
+// variables.  Functions go longest program first (counting sort on n_ops), so
+// the long warps start in the first waves and a launch does not end on a
+// tail of them; chunks of one function stay adjacent (similar cost in a block).
+void append_items(const dfx_fn_desc* fns, int f0, int f1, std::vector<int32_t>& item_fn,
+                  std::vector<int32_t>& item_chunk) {
+  constexpr int kBins = 4096;
+  auto bin = [&](int f) {
+    const int b = fns[f].n_ops >> 4;
+    return kBins - 1 - (b < kBins - 1 ? b : kBins - 1);
+  };
+  std::vector<int32_t> start(kBins + 1, 0), order((size_t)(f1 - f0));
+  for (int f = f0; f < f1; f++) start[bin(f) + 1]++;
+  for (int b = 0; b < kBins; b++) start[b + 1] += start[b];
+  for (int f = f0; f < f1; f++) order[start[bin(f)]++] = f;
+  for (int f : order) {
+    int chunks = (fns[f].n_vars + 31) / 32;
+    if (chunks == 0) chunks = 1;
+    for (int c = 0; c < chunks; c++) {
+      item_fn.push_back(f);
+      item_chunk.push_back(c);
+    }
+  }
+}
+}  // namespace
+
 extern "C" {
 
 int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap, dfx_replay** out) {
@@ -156,13 +206,8 @@ int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap,
                   "branches %d, arms %d)", f, d.n_slots, d.max_loop_depth, d.max_br_depth,
                   d.max_arms);
     if (d.n_slots > max_slots) max_slots = d.n_slots;
-    int chunks = (d.n_vars + 31) / 32;
-    if (chunks == 0) chunks = 1;
-    for (int c = 0; c < chunks; c++) {
-      item_fn.push_back(f);
-      item_chunk.push_back(c);
-    }
   }
+  append_items(in->fns, 0, nf, item_fn, item_chunk);
   auto* rp = new dfx_replay();
   cudaStream_t st = h->st();
   auto up = [&](const void* src, size_t bytes) -> void* {
@@ -182,6 +227,8 @@ int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap,
   r.item_fn = (const int32_t*)up(item_fn.data(), sizeof(int32_t) * item_fn.size());
   r.item_chunk = (const int32_t*)up(item_chunk.data(), sizeof(int32_t) * item_chunk.size());
   r.n_items = (int)item_fn.size();
+  r.fn_lo = 0;
+  r.fn_hi = nf;
   r.max_slots = max_slots;
   r.event_cap = event_cap > 0 ? event_cap : 1;
   r.events = (dfx_event*)up(nullptr, sizeof(dfx_event) * (size_t)r.event_cap);
@@ -250,9 +297,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_replay_batch: null argument");
   CK(cudaSetDevice(h->device));
   const int nf = in->n_funcs;
-  // work items: one warp per (function, 32-variable chunk); at least one per
-  // function so statically known errors surface even without variables
-  std::vector<int32_t> item_fn, item_chunk, fn_item0(nf + 1, 0);
+  std::vector<int32_t> item_fn, item_chunk;
   int max_slots = 2;
   bool ordered = true;   // per-function array ranges ascending and contiguous
   for (int f = 0; f < nf; f++) {
@@ -268,15 +313,38 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
                  d.stmt_off >= e.stmt_off + e.n_stmts && d.site_off >= e.site_off &&
                  d.arm_off >= e.arm_off;
     }
-    fn_item0[f] = (int32_t)item_fn.size();
-    int chunks = (d.n_vars + 31) / 32;
-    if (chunks == 0) chunks = 1;
-    for (int c = 0; c < chunks; c++) {
-      item_fn.push_back(f);
-      item_chunk.push_back(c);
+  }
+  // Pipeline over function ranges: the H2D of range k+1 (copy stream), the
+  // replay of range k (compute stream) and the D2H of range k-1's events
+  // (D2H stream) overlap.  Functions are independent (SURVEY F3 / SPEC), so
+  // ranges change nothing but the order of events in the buffer.  Range sizes
+  // (by ops) ramp up by 1.4x -- the replay of a range outlasts the H2D of the
+  // next one -- so the first H2D, which nothing overlaps, is short; they ramp
+  // down at the end for the same reason on the D2H side.
+  const int K = ordered && nf >= 256 ? dfx_handle::kPipeMax : 1;
+  std::vector<int> cut(K + 1, nf);
+  cut[0] = 0;
+  if (K > 1) {
+    double w[dfx_handle::kPipeMax], tot = 0.0;
+    for (int k = 0; k < K; k++) {
+      const int edge = k < K - 1 - k ? k : K - 1 - k;
+      w[k] = 1.0;
+      for (int i = 0; i < edge && i < 5; i++) w[k] *= 1.4;
+      tot += w[k];
+    }
+    double acc = 0.0;
+    int f = 0;
+    for (int k = 1; k < K; k++) {
+      acc += w[k - 1] / tot;
+      while (f < nf && (double)in->fns[f].op_off < acc * (double)in->n_ops) f++;
+      cut[k] = f;
     }
   }
-  fn_item0[nf] = (int32_t)item_fn.size();
+  std::vector<int32_t> range_item0(K + 1, 0);
+  for (int k = 0; k < K; k++) {
+    append_items(in->fns, cut[k], cut[k + 1], item_fn, item_chunk);
+    range_item0[k + 1] = (int32_t)item_fn.size();
+  }
   const size_t n_items = item_fn.size();
   cudaStream_t st = h->st();
   void* d_fns = dbuf(h, "fns", sizeof(dfx_fn_desc) * (size_t)nf + 16);
@@ -288,20 +356,40 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   void* d_ifn = dbuf(h, "ifn", sizeof(int32_t) * n_items + 16);
   void* d_ich = dbuf(h, "ich", sizeof(int32_t) * n_items + 16);
   const int64_t cap = out->event_cap;
-  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)(cap > 0 ? cap : 1));
-  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long));
+  // Per-range event regions and counters: consecutive ranges replay on
+  // different compute streams, so range k+1 fills the SMs while range k drains
+  // its longest warps (a range lasts at least as long as its longest function).
+  // A region is sized from the caller's capacity in proportion to the range's
+  // ops; a range that overflows its region is replayed again into a region of
+  // the exact size (rare), unless the total already exceeds the caller's
+  // capacity (then the call reports DFX_E_NOSPC with the total, as before).
+  std::vector<int64_t> ev_off(K + 1, 0), ev_cap(K, 0);
+  for (int k = 0; k < K; k++) {
+    const int f0 = cut[k], f1 = cut[k + 1];
+    int64_t ops_k = 0;
+    if (K == 1) ops_k = in->n_ops;
+    else if (f0 < f1) ops_k = (f1 < nf ? (int64_t)in->fns[f1].op_off : in->n_ops) - in->fns[f0].op_off;
+    const double share = in->n_ops > 0 ? (double)ops_k / (double)in->n_ops : 1.0;
+    ev_cap[k] = (int64_t)(1.25 * (double)(cap > 0 ? cap : 0) * share) + 4096;
+    ev_off[k + 1] = ev_off[k] + ev_cap[k];
+  }
+  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[K]);
+  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (K + 1));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
   if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
       !d_cnt || !d_vout)
     return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
   CK(h->pipeline_init());
-  // small arrays first, on the compute stream
+  cudaStream_t cs[dfx_handle::kComp];
+  cs[0] = st;
+  for (int i = 1; i < dfx_handle::kComp; i++) cs[i] = h->s_comp[i];
+  // small arrays first, on the call's stream
   CK(cudaMemcpyAsync(d_fns, in->fns, sizeof(dfx_fn_desc) * (size_t)nf, cudaMemcpyHostToDevice, st));
   if (n_items) {
     CK(cudaMemcpyAsync(d_ifn, item_fn.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_ich, item_chunk.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
   }
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (K + 1), st));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -310,28 +398,24 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   r.sites = (const int32_t*)d_sites;
   r.arms = (const int32_t*)d_arms;
   r.max_slots = max_slots;
-  r.events = d_ev;
-  r.event_cap = cap;
-  r.event_count = d_cnt;
   r.var_out = d_vout;
-  // Pipeline over function ranges: the H2D of chunk k+1 (copy stream), the
-  // replay of chunk k (compute stream) and the D2H of chunk k-1's events
-  // (D2H stream) overlap.  Functions are independent (SURVEY F3 / SPEC), so
-  // chunking changes nothing but the order of events in the buffer.
-  const int K = ordered && nf >= 64 ? dfx_handle::kPipe : 1;
-  std::vector<int> cut(K + 1, nf);
-  {
-    cut[0] = 0;
-    const double per = (double)in->n_ops / K;
-    int f = 0;
-    for (int k = 1; k < K; k++) {
-      while (f < nf && (double)in->fns[f].op_off < per * k) f++;
-      cut[k] = f;
-    }
-  }
+  auto range_dev = [&](int k) {
+    dfx::ReplayDev rk = r;
+    rk.item_fn = (const int32_t*)d_ifn + range_item0[k];
+    rk.item_chunk = (const int32_t*)d_ich + range_item0[k];
+    rk.n_items = range_item0[k + 1] - range_item0[k];
+    rk.fn_lo = cut[k];
+    rk.fn_hi = cut[k + 1];
+    rk.events = d_ev + ev_off[k];
+    rk.event_cap = ev_cap[k];
+    rk.event_count = d_cnt + k;
+    return rk;
+  };
   auto lo = [&](int f, int32_t dfx_fn_desc::*off) -> int64_t { return f < nf ? in->fns[f].*off : -1; };
-  CK(cudaEventRecord(h->pev[0], st));   // fns/items uploaded, counter cleared
+  CK(cudaEventRecord(h->pev[0], st));   // fns/items uploaded, counters cleared
+  if (h->trace) CK(cudaEventRecord(h->tev[3 * dfx_handle::kPipeMax], st));
   CK(cudaStreamWaitEvent(h->s_copy, h->pev[0], 0));
+  for (int i = 1; i < dfx_handle::kComp; i++) CK(cudaStreamWaitEvent(cs[i], h->pev[0], 0));
   for (int k = 0; k < K; k++) {
     const int f0 = cut[k], f1 = cut[k + 1];
     if (f0 < f1) {
@@ -356,35 +440,75 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
                              h->s_copy));
     }
     CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
-    CK(cudaStreamWaitEvent(st, h->pev[1 + k], 0));
-    if (k == 0) CK(cudaEventRecord(h->ev0, st));
-    dfx::ReplayDev rk = r;
-    rk.item_fn = (const int32_t*)d_ifn + fn_item0[f0];
-    rk.item_chunk = (const int32_t*)d_ich + fn_item0[f0];
-    rk.n_items = fn_item0[f1] - fn_item0[f0];
-    int rc = dfx::replay_launch(rk, st);
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * k], h->s_copy));
+    cudaStream_t sk = cs[k % dfx_handle::kComp];
+    CK(cudaStreamWaitEvent(sk, h->pev[1 + k], 0));
+    if (k == 0) CK(cudaEventRecord(h->ev0, sk));
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * k + 1], sk));
+    int rc = dfx::replay_launch(range_dev(k), sk);
     if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    if (k == K - 1) CK(cudaEventRecord(h->ev1, st));
-    CK(cudaMemcpyAsync(h->pin_cnt + k, d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipe + k], st));
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * k + 2], sk));
+    CK(cudaMemcpyAsync(h->pin_cnt + k, d_cnt + k, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sk));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + k], sk));
   }
-  // events of chunk k go back as soon as chunk k's replay is done
-  unsigned long long done = 0;
+  for (int i = 1; i < dfx_handle::kComp; i++) {
+    CK(cudaEventRecord(h->jev[i], cs[i]));
+    CK(cudaStreamWaitEvent(st, h->jev[i], 0));
+  }
+  CK(cudaEventRecord(h->ev1, st));
+  // events of range k go back as soon as range k's replay is done
+  unsigned long long count = 0, done = 0;
+  std::vector<int> redo;
   for (int k = 0; k < K; k++) {
-    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipe + k]));
-    unsigned long long end = h->pin_cnt[k];
-    if (end > (unsigned long long)cap) end = (unsigned long long)(cap > 0 ? cap : 0);
-    if (end > done)
-      CK(cudaMemcpyAsync(out->events + done, d_ev + done, sizeof(dfx_event) * (size_t)(end - done),
+    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipeMax + k]));
+    const unsigned long long c = h->pin_cnt[k];
+    count += c;
+    if ((int64_t)c > ev_cap[k]) { redo.push_back(k); continue; }
+    unsigned long long n = c;
+    if (cap <= (int64_t)done) n = 0;
+    else if ((int64_t)(done + n) > cap) n = (unsigned long long)cap - done;
+    if (n)
+      CK(cudaMemcpyAsync(out->events + done, d_ev + ev_off[k], sizeof(dfx_event) * (size_t)n,
                          cudaMemcpyDeviceToHost, h->s_d2h));
-    done = end > done ? end : done;
+    done += n;
   }
-  const unsigned long long count = h->pin_cnt[K - 1];
-  if (in->n_vars)
+  if (!redo.empty() && (int64_t)count <= cap) {
+    for (int k : redo) {
+      const int64_t need = (int64_t)h->pin_cnt[k];
+      auto* d_re = (dfx_event*)dbuf(h, "events_redo", sizeof(dfx_event) * (size_t)need);
+      if (!d_re) return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
+      dfx::ReplayDev rk = range_dev(k);
+      rk.events = d_re;
+      rk.event_cap = need;
+      rk.event_count = d_cnt + K;
+      CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home
+      CK(cudaMemsetAsync(d_cnt + K, 0, sizeof(unsigned long long), st));
+      int rc = dfx::replay_launch(rk, st);
+      if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpyAsync(out->events + done, d_re, sizeof(dfx_event) * (size_t)need,
+                         cudaMemcpyDeviceToHost, h->s_d2h));
+      done += (unsigned long long)need;
+    }
+  }
+  if (in->n_vars) {
+    CK(cudaStreamWaitEvent(h->s_d2h, h->ev1, 0));
     CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost, h->s_d2h));
+  }
   CK(cudaStreamSynchronize(h->s_d2h));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (h->trace) {
+    const cudaEvent_t t0 = h->tev[3 * dfx_handle::kPipeMax];
+    for (int k = 0; k < K; k++) {
+      float a = 0.f, b = 0.f, c = 0.f;
+      cudaEventElapsedTime(&a, t0, h->tev[3 * k]);
+      cudaEventElapsedTime(&b, t0, h->tev[3 * k + 1]);
+      cudaEventElapsedTime(&c, t0, h->tev[3 * k + 2]);
+      fprintf(stderr, "dfx_replay_batch range %2d: functions [%d, %d) h2d done %8.2f ms, "
+              "replay %8.2f .. %8.2f ms (%.2f)\n", k, cut[k], cut[k + 1], a, b, c, c - b);
+    }
+  }
   out->kernel_ms = ms;
   out->n_events = (int64_t)count;
   if ((int64_t)count > cap) return fail(DFX_E_NOSPC, "event capacity %lld < %llu",
@@ -808,12 +932,12 @@ int dfx_csr_requirements_list(dfx_handle* h, dfx_csr* c, dfx_req_list* out, dfx_
     if (!rc && want) rc = dfx::compact_list(p, c->offsets, c->d_vars, want, lo, hi, st);
     if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
     CK(cudaMemcpyAsync(h->pin_cnt + k, c->offsets + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipe + k], st));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + k], st));
   }
   CK(cudaEventRecord(c->e1, st));
   int64_t done = 0;
   for (int k = 0; k < K; k++) {
-    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipe + k]));
+    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipeMax + k]));
     int64_t end = (int64_t)h->pin_cnt[k];
     if (end > want) end = want;
     if (want && end > done)

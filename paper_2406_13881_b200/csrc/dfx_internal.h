@@ -17,6 +17,7 @@ struct ReplayDev {
   const int32_t* item_fn;
   const int32_t* item_chunk;
   int n_items;
+  int fn_lo, fn_hi;   // functions of this launch (region_kernel)
   int max_slots;
   dfx_event* events;
   int64_t event_cap;

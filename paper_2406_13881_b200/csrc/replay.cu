@@ -307,6 +307,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         break;
       }
       case DFX_OP_BR_BEGIN: {  // saved = self.state
+        if (!(((uint32_t)op.z >> (chunk & 31)) & 1u)) goto skip_region;
         if (lane == 0) {
           if (c.nbr >= kMaxBr) c.fault = 1;
           else {
@@ -393,6 +394,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         break;
       }
       case DFX_OP_LOOP_BEGIN: {  // _loop_rounds: entry = state.copy(); dry round
+        if (!(((uint32_t)op.z >> (chunk & 31)) & 1u)) goto skip_region;
         if (lane == 0) {
           if (c.nlp >= kMaxLoop) c.fault = 1;
           else {
@@ -452,6 +454,33 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     }
     if (code >= DFX_OP_BR_BEGIN && c.fault) goto fault;   // access ops never fault
     pc++;
+    continue;
+  skip_region:
+    // no access of this warp's variables (and no static error) anywhere in the
+    // region: every arm / round leaves the state as it found it, so the region
+    // only advances the visit counter, by its dynamic op count (region_kernel).
+    // A region holding a branch still ends in a fresh slot (`_merge_arms`
+    // returns a new state object): an enclosing arm captured by F_CAPTURE
+    // keeps the old slot and must stay frozen at this point (D4)
+    {
+      const uint32_t ew = (uint32_t)__ldg(&fops[pc + op.w].w);
+      seq += (uint64_t)(ew & 0x7FFFFFFFu) - 1u;
+      pc += op.w + 1;
+      if (!(ew >> 31)) continue;
+    }
+    {
+      if (lane == 0) {
+        const int s = alloc_slot(c, nslots);
+        c.bc0 = s;
+        ref_dec(c, cur);
+        c.cur = s;
+      }
+      __syncwarp();
+      copy_slot(c.bc0, cur);
+      cur = c.cur;
+      __syncwarp();
+      if (c.fault) goto fault;
+    }
   }
   if (active) {
     uint8_t o = 0;
@@ -470,7 +499,73 @@ halt_all:
   if (active) var_out[d.var_off + var] = 0;
 }
 
+// Region table, one thread per function (runs before the replay of the same
+// function range, on the same stream).  For every BR_BEGIN / LOOP_BEGIN it
+// writes into the device copy of the program
+//   begin.z = chunk mask: bit (v >> 5) & 31 for every variable v accessed
+//             anywhere inside the region; all ones if the region holds a
+//             static error op, nests deeper than the frame stack, or its
+//             dynamic length does not fit 31 bits (never skipped)
+//   begin.w = end pc - begin pc
+//   end.w   = dynamic op count of one visit of the region, begin and end
+//             included: branch 2 + content, loop 3 + 2 x content (the dry
+//             round and the planning round, `_loop_rounds`, dataflow.py:566-590)
+//             | 1 << 31 if the region holds a branch (the current slot changes
+//             identity across it)
+// Idempotent; fields the replay reads from these ops are untouched.
+constexpr int kRegionStack = kMaxBr + kMaxLoop;
+__global__ void __launch_bounds__(128)
+region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int fn_lo, int fn_hi) {
+  const int f = fn_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= fn_hi) return;
+  const dfx_fn_desc d = fns[f];
+  int4* o = ops + d.op_off;
+  int32_t st_pc[kRegionStack + 1];
+  uint32_t st_mask[kRegionStack + 1];
+  int64_t st_dyn[kRegionStack + 1];
+  bool st_br[kRegionStack + 1];
+  int sp = 0, deep = 0;   // deep: open regions beyond the stack (never skipped)
+  st_mask[0] = 0u; st_dyn[0] = 0; st_br[0] = false;
+  for (int pc = 0; pc < d.n_ops; pc++) {
+    const int4 op = o[pc];
+    const int code = op.x & 0xFF;
+    if (code == DFX_OP_END) break;
+    if (code >= DFX_OP_HR && code <= DFX_OP_DW) {
+      st_mask[sp] |= 1u << ((op.y >> 5) & 31);
+      st_dyn[sp]++;
+    } else if (code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN) {
+      o[pc].z = -1;          // until its end is seen
+      if (deep || sp == kRegionStack) { deep++; st_mask[sp] = ~0u; continue; }
+      sp++;
+      st_pc[sp] = pc; st_mask[sp] = 0u; st_dyn[sp] = 0; st_br[sp] = code == DFX_OP_BR_BEGIN;
+    } else if (code == DFX_OP_BR_END || code == DFX_OP_LOOP_END) {
+      if (deep) { deep--; continue; }
+      if (sp == 0) continue; // unbalanced
+      const int b = st_pc[sp];
+      const bool loop = code == DFX_OP_LOOP_END;
+      const int64_t dyn = loop ? 3 + 2 * st_dyn[sp] : 2 + st_dyn[sp];
+      uint32_t mask = st_mask[sp];
+      if (dyn > 0x7FFFFFFF || loop != ((o[b].x & 0xFF) == DFX_OP_LOOP_BEGIN)) mask = ~0u;
+      o[b].z = (int)mask;
+      o[b].w = pc - b;
+      o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (st_br[sp] ? 0x80000000u : 0u));
+      const bool br = st_br[sp];
+      sp--;
+      st_mask[sp] |= mask;
+      st_dyn[sp] += dyn;
+      st_br[sp] |= br;
+    } else {
+      if (code == DFX_OP_ERR) st_mask[sp] = ~0u;
+      st_dyn[sp]++;
+    }
+  }
+}
+
 int replay_launch(const ReplayDev& r, cudaStream_t stream) {
+  if (r.fn_hi > r.fn_lo) {
+    region_kernel<<<(r.fn_hi - r.fn_lo + 127) / 128, 128, 0, stream>>>(
+        r.fns, reinterpret_cast<int4*>(const_cast<int32_t*>(r.ops)), r.fn_lo, r.fn_hi);
+  }
   int slots = r.max_slots;
   if (slots < 2) slots = 2;
   if (slots > kMaxSlots) return DFX_E_LIMIT;

@@ -61,3 +61,48 @@ def test_cuda_replay_matches_oracle_on_c4_batch():
     n, ms = rb.run()
     res = rb.fetch()
     _golden.assert_raw_equal(res.events, res.var_out, exp.events, exp.var_out)
+
+
+@pytest.mark.gpu
+def test_cuda_replay_matches_oracle_at_bench_shapes():
+    """Functions of the benchmark's own batch (64-2048 nodes, up to 512
+    variables = 16 warps per function), through the pipelined batch call and
+    the device-resident one.  Large functions nest branches and loops inside
+    captured if-arms; warps skip regions none of their variables is accessed
+    in (replay.cu region_kernel), and a skipped region that holds a branch must
+    still end in a fresh slot so the enclosing arm stays frozen (D4)."""
+    from paper_2406_13881_b200.batch import C4Config, ReplayBatch, c4_generate
+    b, _ = c4_generate(C4Config(), np.arange(0, 100_000, 67))
+    exp = run_replay(b, runner=_oracle.replay_runner_mt)
+    got = run_replay(b)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+    rb = ReplayBatch(b)
+    rb.run()
+    res = rb.fetch()
+    _golden.assert_raw_equal(res.events, res.var_out, exp.events, exp.var_out)
+
+
+@pytest.mark.gpu
+def test_host_buffer_call_with_uneven_event_density():
+    """dfx_replay_batch gives each pipeline range an event region sized by its
+    share of the ops.  Here the first half of the functions carries all the
+    events (the second half only writes on the host), and the caller's
+    capacity is the exact total, so the early ranges overflow their regions
+    and are replayed again into exact-size ones: the result must not change."""
+    import dataclasses
+    from paper_2406_13881_b200.batch import C4Config, c4_generate
+    from paper_2406_13881_b200.dataflow import ReplaySession
+    b, _ = c4_generate(C4Config(), np.arange(400))
+    ops = b.ops.copy()
+    start = int(b.fns[200]["op_off"])
+    code = ops[start:, 0] & 0xFF
+    acc = (code >= 1) & (code <= 4)
+    ops[start:, 0][acc] = (ops[start:, 0][acc] & ~0xFF) | 2        # every access -> HW
+    b2 = dataclasses.replace(b, ops=ops)
+    exp = run_replay(b2, runner=_oracle.replay_runner_mt)
+    assert not (exp.events["fn"] >= 200).any() and exp.events.shape[0] > 100_000
+    got = ReplaySession(event_cap=int(exp.events.shape[0])).run(b2)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+    small = ReplaySession(event_cap=1000)                          # NOSPC -> regrow
+    got = small.run(b2)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)

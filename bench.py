@@ -474,8 +474,9 @@ def run_c4(args, rank, world, local):
         e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
                "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h // args.e2e_steps),
-               "path": "dfx_replay_batch (pinned host buffers): H2D programs, E1 kernel, D2H "
-                       "events, pipelined over 8 function ranges (copy / compute / D2H streams)"}
+               "path": "dfx_replay_batch (pinned host buffers): H2D programs in 16 function "
+                       "ranges (copy stream), E1 replays per range and one longest-first launch "
+                       "over the last 40% (3 compute streams), D2H events per launch (D2H stream)"}
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -340,10 +340,28 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       cut[k] = f;
     }
   }
-  std::vector<int32_t> range_item0(K + 1, 0);
-  for (int k = 0; k < K; k++) {
-    append_items(in->fns, cut[k], cut[k + 1], item_fn, item_chunk);
-    range_item0[k + 1] = (int32_t)item_fn.size();
+  // Replays run per launch unit: ranges 0..m-1 one unit each, ranges m..K-1
+  // (the last 40% of the ops) one unit, items longest first.  By the time the
+  // compute streams reach that unit its inputs are resident, and one launch
+  // sorted over all of them ends on short items, not on the long items of
+  // each of the last ranges.
+  int m = K;
+  if (K > 1) {
+    m = 1;
+    while (m < K && (double)(cut[m] < nf ? in->fns[cut[m]].op_off : in->n_ops) <
+                        0.6 * (double)in->n_ops)
+      m++;
+  }
+  const int U = m < K ? m + 1 : K;
+  std::vector<int> ucut(U + 1, nf), last_range(U, K - 1);
+  for (int u = 0; u < U; u++) {
+    ucut[u] = cut[u];
+    if (u < m) last_range[u] = u;
+  }
+  std::vector<int32_t> range_item0(U + 1, 0);
+  for (int u = 0; u < U; u++) {
+    append_items(in->fns, ucut[u], ucut[u + 1], item_fn, item_chunk);
+    range_item0[u + 1] = (int32_t)item_fn.size();
   }
   const size_t n_items = item_fn.size();
   cudaStream_t st = h->st();
@@ -363,18 +381,18 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   // ops; a range that overflows its region is replayed again into a region of
   // the exact size (rare), unless the total already exceeds the caller's
   // capacity (then the call reports DFX_E_NOSPC with the total, as before).
-  std::vector<int64_t> ev_off(K + 1, 0), ev_cap(K, 0);
-  for (int k = 0; k < K; k++) {
-    const int f0 = cut[k], f1 = cut[k + 1];
-    int64_t ops_k = 0;
-    if (K == 1) ops_k = in->n_ops;
-    else if (f0 < f1) ops_k = (f1 < nf ? (int64_t)in->fns[f1].op_off : in->n_ops) - in->fns[f0].op_off;
-    const double share = in->n_ops > 0 ? (double)ops_k / (double)in->n_ops : 1.0;
-    ev_cap[k] = (int64_t)(1.25 * (double)(cap > 0 ? cap : 0) * share) + 4096;
-    ev_off[k + 1] = ev_off[k] + ev_cap[k];
+  std::vector<int64_t> ev_off(U + 1, 0), ev_cap(U, 0);
+  for (int u = 0; u < U; u++) {
+    const int f0 = ucut[u], f1 = ucut[u + 1];
+    int64_t ops_u = 0;
+    if (U == 1) ops_u = in->n_ops;
+    else if (f0 < f1) ops_u = (f1 < nf ? (int64_t)in->fns[f1].op_off : in->n_ops) - in->fns[f0].op_off;
+    const double share = in->n_ops > 0 ? (double)ops_u / (double)in->n_ops : 1.0;
+    ev_cap[u] = (int64_t)(1.25 * (double)(cap > 0 ? cap : 0) * share) + 4096;
+    ev_off[u + 1] = ev_off[u] + ev_cap[u];
   }
-  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[K]);
-  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (K + 1));
+  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[U]);
+  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (U + 1));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
   if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
       !d_cnt || !d_vout)
@@ -389,7 +407,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     CK(cudaMemcpyAsync(d_ifn, item_fn.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_ich, item_chunk.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
   }
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (K + 1), st));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (U + 1), st));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -404,8 +422,8 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     rk.item_fn = (const int32_t*)d_ifn + range_item0[k];
     rk.item_chunk = (const int32_t*)d_ich + range_item0[k];
     rk.n_items = range_item0[k + 1] - range_item0[k];
-    rk.fn_lo = cut[k];
-    rk.fn_hi = cut[k + 1];
+    rk.fn_lo = ucut[k];
+    rk.fn_hi = ucut[k + 1];
     rk.events = d_ev + ev_off[k];
     rk.event_cap = ev_cap[k];
     rk.event_count = d_cnt + k;
@@ -441,25 +459,27 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     }
     CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
     if (h->trace) CK(cudaEventRecord(h->tev[3 * k], h->s_copy));
-    cudaStream_t sk = cs[k % dfx_handle::kComp];
+    const int u = k < m ? k : U - 1;
+    if (k != last_range[u]) continue;
+    cudaStream_t sk = cs[u % dfx_handle::kComp];
     CK(cudaStreamWaitEvent(sk, h->pev[1 + k], 0));
-    if (k == 0) CK(cudaEventRecord(h->ev0, sk));
-    if (h->trace) CK(cudaEventRecord(h->tev[3 * k + 1], sk));
-    int rc = dfx::replay_launch(range_dev(k), sk);
+    if (u == 0) CK(cudaEventRecord(h->ev0, sk));
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * u + 1], sk));
+    int rc = dfx::replay_launch(range_dev(u), sk);
     if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    if (h->trace) CK(cudaEventRecord(h->tev[3 * k + 2], sk));
-    CK(cudaMemcpyAsync(h->pin_cnt + k, d_cnt + k, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sk));
-    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + k], sk));
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * u + 2], sk));
+    CK(cudaMemcpyAsync(h->pin_cnt + u, d_cnt + u, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sk));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + u], sk));
   }
   for (int i = 1; i < dfx_handle::kComp; i++) {
     CK(cudaEventRecord(h->jev[i], cs[i]));
     CK(cudaStreamWaitEvent(st, h->jev[i], 0));
   }
   CK(cudaEventRecord(h->ev1, st));
-  // events of range k go back as soon as range k's replay is done
+  // events of unit k go back as soon as unit k's replay is done
   unsigned long long count = 0, done = 0;
   std::vector<int> redo;
-  for (int k = 0; k < K; k++) {
+  for (int k = 0; k < U; k++) {
     CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipeMax + k]));
     const unsigned long long c = h->pin_cnt[k];
     count += c;
@@ -480,9 +500,9 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       dfx::ReplayDev rk = range_dev(k);
       rk.events = d_re;
       rk.event_cap = need;
-      rk.event_count = d_cnt + K;
+      rk.event_count = d_cnt + U;
       CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home
-      CK(cudaMemsetAsync(d_cnt + K, 0, sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(d_cnt + U, 0, sizeof(unsigned long long), st));
       int rc = dfx::replay_launch(rk, st);
       if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       CK(cudaStreamSynchronize(st));
@@ -501,12 +521,17 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if (h->trace) {
     const cudaEvent_t t0 = h->tev[3 * dfx_handle::kPipeMax];
     for (int k = 0; k < K; k++) {
-      float a = 0.f, b = 0.f, c = 0.f;
+      float a = 0.f;
       cudaEventElapsedTime(&a, t0, h->tev[3 * k]);
-      cudaEventElapsedTime(&b, t0, h->tev[3 * k + 1]);
-      cudaEventElapsedTime(&c, t0, h->tev[3 * k + 2]);
-      fprintf(stderr, "dfx_replay_batch range %2d: functions [%d, %d) h2d done %8.2f ms, "
-              "replay %8.2f .. %8.2f ms (%.2f)\n", k, cut[k], cut[k + 1], a, b, c, c - b);
+      fprintf(stderr, "dfx_replay_batch range %2d: functions [%d, %d) h2d done %8.2f ms\n", k,
+              cut[k], cut[k + 1], a);
+    }
+    for (int u = 0; u < U; u++) {
+      float b = 0.f, c = 0.f;
+      cudaEventElapsedTime(&b, t0, h->tev[3 * u + 1]);
+      cudaEventElapsedTime(&c, t0, h->tev[3 * u + 2]);
+      fprintf(stderr, "dfx_replay_batch unit %2d: functions [%d, %d) replay %8.2f .. %8.2f ms "
+              "(%.2f)\n", u, ucut[u], ucut[u + 1], b, c, c - b);
     }
   }
   out->kernel_ms = ms;

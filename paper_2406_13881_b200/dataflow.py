@@ -379,12 +379,13 @@ def _lower_portable(i: int):
         kstmts = [_path(n, root) for n in prog.kernel_stmts]
         region = None if prog.region is None else [_path(n, root) for n in prog.region]
         vars_ = [first[id(v)] for v in prog.vars]
+        premapped = None if prog.premapped is None else _path(prog.premapped, root)
     except (KeyError, AttributeError, StopIteration):
         return ("serial", None)  # a reference not reachable this way: lower in the parent
     fields = {k: getattr(prog, k) for k in ("ops", "var_flags", "stmt_span", "sites", "arms",
                                             "region_begin_start", "n_slots", "max_loop_depth",
                                             "max_br_depth", "max_arms")}
-    return ("ok", (fields, stmts, kstmts, region, vars_))
+    return ("ok", (fields, stmts, kstmts, region, vars_, premapped))
 
 
 def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | None = None):
@@ -425,27 +426,52 @@ def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | 
         if tag != "ok":         # errors and unmappable programs: the serial path decides
             progs.append(lower_function(src, cfg, accs, table, allow_stale))
             continue
-        fields, stmts, kstmts, region, vars_ = r
+        fields, stmts, kstmts, region, vars_, premapped = r
         root = cfg.function
         progs.append(FnProgram(fn=root, **fields,
                                vars=[accs[j].var for j in vars_],
                                stmts=[_follow(root, q) for q in stmts],
                                kernel_stmts=[_follow(root, q) for q in kstmts],
-                               region=None if region is None else tuple(_follow(root, q) for q in region)))
+                               region=None if region is None else tuple(_follow(root, q) for q in region),
+                               premapped=None if premapped is None else _follow(root, premapped)))
     return progs
 
 
+def _first_occurrences(evs: np.ndarray) -> np.ndarray:
+    """Mask of the events (sorted by function, then visit key) that are the
+    first of their (function, kind, variable, node, position): a repeat
+    (a plan re-planned in a later loop round) is dropped by `_add_plan`'s
+    dedup (`dataflow.py:259-268`) and a repeated suppression by name, so
+    `decode` need not see it.  Error events are always kept."""
+    if evs.shape[0] < 2:
+        return np.ones(evs.shape[0], dtype=bool)
+    rec = np.empty(evs.shape[0], dtype=[("fn", "<i4"), ("var", "<i4"), ("node", "<i4"),
+                                        ("kind", "u1"), ("pos", "u1")])
+    for f in ("fn", "var", "node", "kind", "pos"):
+        rec[f] = evs[f]
+    _, first = np.unique(rec, return_index=True)
+    keep = np.zeros(evs.shape[0], dtype=bool)
+    keep[first] = True
+    keep |= evs["kind"] >= _abi.EV_ERR_DATAMAP
+    return keep
+
+
 def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
-                      runner=None) -> list[_Deferred]:
+                      runner=None, precheck=None) -> list[_Deferred]:
     """Batched `analyze_function`: `items` is a list of
     `(src, cfg, accesses, table)`; one engine launch for all of them.
     Returns one deferred result per item (`.get()` returns the
-    `FunctionPlan` or raises the reference's exception)."""
+    `FunctionPlan` or raises the reference's exception).  `precheck(progs)`
+    runs after the lowering and before the launch (the unit-level input
+    checks of `plan_transform`, fed by the per-function lowering)."""
     progs = lower_functions(items, allow_stale)
+    if precheck is not None:
+        precheck(progs)
     batch = pack(progs)
     raw = run_replay(batch, runner=runner)
     order = np.lexsort((raw.events["key"], raw.events["fn"]))   # by function, then visit key
     evs = raw.events[order]
+    evs = evs[_first_occurrences(evs)]
     bounds = np.searchsorted(evs["fn"], np.arange(len(progs) + 1))
     out = []
     for i, (p, (src, cfg, accs, table)) in enumerate(zip(progs, items)):

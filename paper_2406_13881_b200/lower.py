@@ -51,7 +51,7 @@ from dartomp.bounds import (enclosing_for_loops, find_indexing_var,  # noqa: E40
                             subscript_index_vars)
 from dartomp.dataflow import compute_region_extent  # noqa: E402
 from dartomp.nodes import NodeKind  # noqa: E402
-from dartomp.omp import DATA_MAPPING_KINDS  # noqa: E402
+from dartomp.omp import DATA_MAPPING_KINDS, KERNEL_KINDS  # noqa: E402
 
 # ---- opcodes (must match include/dfx.h) ----------------------------------
 OP_END = 0
@@ -144,6 +144,7 @@ class FnProgram:
     stmts: list = field(default_factory=list)
     kernel_stmts: list = field(default_factory=list)
     region: tuple | None = None          # (block, begin, end)
+    premapped: object = None             # first pre-annotated directive (see below)
 
     @property
     def n_vars(self) -> int:
@@ -678,7 +679,31 @@ class _Lowerer:
                     if self.region_begin is not None else None))
 
 
+def premapped_directive(root):
+    """First OpenMP directive under `root`, in the pre-order of
+    `AstNode.walk` (`nodes.py:108-111`), that `check_transform_preconditions`
+    (`pipeline.py:65-82`) refuses: a data-mapping construct, or an offload
+    directive that already has a `map` clause.  None if there is none.
+    Iterative, so the batched lowering can run the check per function in its
+    workers instead of one recursive generator walk over the whole unit."""
+    omp_kind = NodeKind.OMP_DIRECTIVE
+    stack = [root]
+    while stack:
+        node = stack.pop()
+        if node.kind is omp_kind and node.omp is not None:
+            info = node.omp
+            if info.kind in DATA_MAPPING_KINDS or (
+                    info.kind in KERNEL_KINDS and info.clause("map") is not None):
+                return node
+        ch = node.children
+        if ch:
+            stack.extend(reversed(ch))
+    return None
+
+
 def lower_function(src, cfg, accesses, table, allow_stale=frozenset()) -> FnProgram:
     lw = _Lowerer(src, cfg, accesses, table, allow_stale)
     lw.run()
-    return lw.finish()
+    prog = lw.finish()
+    prog.premapped = premapped_directive(cfg.function)
+    return prog

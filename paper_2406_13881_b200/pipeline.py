@@ -20,11 +20,14 @@ from dartomp.astcfg import build_astcfg  # noqa: E402
 from dartomp.lexer import expand_defines  # noqa: E402
 from dartomp.nodes import defined_functions  # noqa: E402
 from dartomp.parser import parse  # noqa: E402
+from dartomp.diagnostics import PreconditionError  # noqa: E402
+from dartomp.omp import DATA_MAPPING_KINDS  # noqa: E402
 from dartomp.pipeline import Analysis, check_transform_preconditions  # noqa: E402
 from dartomp.rewriter import apply_plans  # noqa: E402
 from dartomp.source import SourceFile  # noqa: E402
 
 from .dataflow import analyze_function, analyze_functions  # noqa: E402
+from .lower import premapped_directive  # noqa: E402
 from .interproc import apply_call_effects, summarize_all  # noqa: E402
 
 
@@ -54,15 +57,49 @@ def load(path: str | None = None, text: str | None = None,
                     defines=dict(pre.defines), warnings=warnings)
 
 
+def _precheck(analysis: Analysis, names: list):
+    """`check_transform_preconditions` (`pipeline.py:65-82`) over the unit in
+    the same pre-order: each function's first refused directive comes from
+    its lowering (`FnProgram.premapped`, found in the lowering workers); only
+    the nodes outside function definitions are walked here.  Raises the same
+    `PreconditionError` for the same first directive."""
+    def check(progs):
+        by_root = {id(analysis.cfgs[n].function): p for n, p in zip(names, progs)}
+        for top in analysis.tu.children:
+            p = by_root.get(id(top))
+            node = p.premapped if p is not None else premapped_directive(top)
+            if node is None:
+                continue
+            src, info = analysis.src, node.omp
+            line = src.line_of(node.span.start)
+            if info.kind in DATA_MAPPING_KINDS:
+                raise PreconditionError(
+                    "input already contains a '%s' directive; the transform "
+                    "expects offload regions without data-mapping constructs"
+                    % info.kind.value, path=src.path, line=line)
+            raise PreconditionError(
+                "input already contains a 'map' clause on an offload "
+                "directive; the transform expects unannotated kernels",
+                path=src.path, line=line)
+    return check
+
+
 def plan_transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset(),
                    replay_runner=None) -> list:
     """`dartomp.pipeline.plan_transform` (`pipeline.py:85-96`), one launch."""
-    check_transform_preconditions(analysis)
     names = list(analysis.cfgs)
     items = [(analysis.src, analysis.cfgs[n], analysis.accesses[n], analysis.table)
              for n in names]
+    try:
+        results = analyze_functions(items, allow_stale, runner=replay_runner,
+                                    precheck=_precheck(analysis, names))
+    except PreconditionError:
+        raise
+    except Exception:
+        check_transform_preconditions(analysis)   # the reference checks first
+        raise
     plans = []
-    for res in analyze_functions(items, allow_stale, runner=replay_runner):
+    for res in results:
         plan = res.get()            # raises the reference's error for that function
         if plan.region is not None or plan.all_plans:
             plans.append(plan)

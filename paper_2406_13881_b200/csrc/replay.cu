@@ -514,7 +514,7 @@ halt_all:
 //             identity across it)
 // Idempotent; fields the replay reads from these ops are untouched.
 constexpr int kRegionStack = kMaxBr + kMaxLoop;
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32)
 region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int fn_lo, int fn_hi) {
   const int f = fn_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= fn_hi) return;
@@ -526,8 +526,21 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
   bool st_br[kRegionStack + 1];
   int sp = 0, deep = 0;   // deep: open regions beyond the stack (never skipped)
   st_mask[0] = 0u; st_dyn[0] = 0; st_br[0] = false;
+  // (code, var) words of 8 ops per batch of independent loads: the stores
+  // below touch only words 2-3, so one memory latency per batch, not per op
+  constexpr int kBatch = 8;
+  int2 buf[kBatch];
   for (int pc = 0; pc < d.n_ops; pc++) {
-    const int4 op = o[pc];
+    if ((pc & (kBatch - 1)) == 0) {
+#pragma unroll
+      for (int i = 0; i < kBatch; i++)
+        buf[i] = pc + i < d.n_ops ? __ldcg(reinterpret_cast<const int2*>(o + pc + i))
+                                  : make_int2(DFX_OP_END, 0);
+    }
+    int2 op = buf[0];
+#pragma unroll
+    for (int i = 1; i < kBatch; i++)
+      if ((pc & (kBatch - 1)) == i) op = buf[i];
     const int code = op.x & 0xFF;
     if (code == DFX_OP_END) break;
     if (code >= DFX_OP_HR && code <= DFX_OP_DW) {
@@ -545,7 +558,7 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
       const bool loop = code == DFX_OP_LOOP_END;
       const int64_t dyn = loop ? 3 + 2 * st_dyn[sp] : 2 + st_dyn[sp];
       uint32_t mask = st_mask[sp];
-      if (dyn > 0x7FFFFFFF || loop != ((o[b].x & 0xFF) == DFX_OP_LOOP_BEGIN)) mask = ~0u;
+      if (dyn > 0x7FFFFFFF || loop == st_br[sp]) mask = ~0u;   // too long, or mismatched
       o[b].z = (int)mask;
       o[b].w = pc - b;
       o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (st_br[sp] ? 0x80000000u : 0u));
@@ -563,7 +576,7 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
 
 int replay_launch(const ReplayDev& r, cudaStream_t stream) {
   if (r.fn_hi > r.fn_lo) {
-    region_kernel<<<(r.fn_hi - r.fn_lo + 127) / 128, 128, 0, stream>>>(
+    region_kernel<<<(r.fn_hi - r.fn_lo + 31) / 32, 32, 0, stream>>>(
         r.fns, reinterpret_cast<int4*>(const_cast<int32_t*>(r.ops)), r.fn_lo, r.fn_hi);
   }
   int slots = r.max_slots;

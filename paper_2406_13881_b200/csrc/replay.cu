@@ -164,8 +164,12 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   L.halted = !active;
   int cur = c.cur;
   int record = 1;
-  uint64_t seq = 0;
+  // visit counter (`_Analyzer` op order, the event key) of the op at pc is
+  // sbase + pc + 1: it advances with pc, and sbase absorbs the jumps (loop
+  // rounds, skipped regions), so the op loop does no 64-bit counting
+  uint64_t sbase = 0;
   int pc = 0;
+  auto key_now = [&]() { return (sbase + (uint64_t)pc + 1u) << 24; };
 
   // plan-log window bookkeeping for the zero-trip skip merge (dataflow.py:573-589)
   auto log_plan = [&](int kind, int pos, int node) {
@@ -201,7 +205,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   int4 wop = make_int4(0, 0, 0, 0);
   unsigned rel = 0u;
   for (;;) {
-    if (pc < wbase || pc >= wbase + 32) {
+    if ((unsigned)(pc - wbase) >= 32u) {
       wbase = pc;
       bool r = true;
       if (wbase + lane < d.n_ops) {
@@ -213,24 +217,20 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     }
     const unsigned m = rel & (0xFFFFFFFFu << (pc - wbase));
     if (!m) {                       // the rest of the window is foreign accesses
-      seq += (uint64_t)(wbase + 32 - pc);
       pc = wbase + 32;
       continue;
     }
     const int src = __ffs(m) - 1;
-    seq += (uint64_t)(wbase + src - pc);
     pc = wbase + src;
     const int4 op = make_int4(__shfl_sync(0xFFFFFFFFu, wop.x, src), __shfl_sync(0xFFFFFFFFu, wop.y, src),
                               __shfl_sync(0xFFFFFFFFu, wop.z, src), __shfl_sync(0xFFFFFFFFu, wop.w, src));
     const int code = op.x & 0xFF, fl = op.x;
-    seq++;
-    const uint64_t key = seq << 24;
     if (code == DFX_OP_END) break;
     switch (code) {
       case DFX_OP_HR: {   // host_read, dataflow.py:299-324
         if (op.y != myvar || L.halted || getb(L.H, cur)) break;
         if (vflags & DFX_V_ALLOW_STALE) {
-          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_SUPPRESS, 0);
+          if (record) emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_SUPPRESS, 0);
           L.H = setb(L.H, cur, 1); break;
         }
         if (fl & DFX_F_AFTER_REGION) {
@@ -243,13 +243,13 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         else {
           int a = hoist(fsites + op.w, lim);
           if (a & DFX_AC_ERR) {
-            emit(events, event_count, event_cap, key, fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
+            emit(events, event_count, event_cap, key_now(), fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
             L.halted = 1; break;
           }
           pos = DFX_POS_BEFORE; node = a;
         }
         log_plan(DFX_EV_UPDATE_FROM, pos, node);
-        if (record) emit(events, event_count, event_cap, key, fi, var, node, DFX_EV_UPDATE_FROM, pos);
+        if (record) emit(events, event_count, event_cap, key_now(), fi, var, node, DFX_EV_UPDATE_FROM, pos);
         L.H = setb(L.H, cur, 1);
         break;
       }
@@ -263,16 +263,16 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       case DFX_OP_DR: {   // device_read, dataflow.py:332-368
         if (op.y != myvar || L.halted || getb(L.D, cur)) break;
         if (vflags & DFX_V_ALLOW_STALE) {
-          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_SUPPRESS, 0);
+          if (record) emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_SUPPRESS, 0);
           L.D = setb(L.D, cur, 1); break;
         }
         if ((fl & DFX_F_FP) && getb(L.H, cur)) {
-          if (record) emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_FIRSTPRIVATE, DFX_POS_KERNEL);
+          if (record) emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_FIRSTPRIVATE, DFX_POS_KERNEL);
           break;
         }
         L.presence = 1;
         if (record && (vflags & DFX_V_DECL_LATE)) {
-          emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_ERR_DECL, 0);
+          emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_ERR_DECL, 0);
           L.halted = 1; break;
         }
         uint32_t lw = prov[cur * 32 + lane] >> 16;
@@ -284,13 +284,13 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         else {
           int a = hoist(fsites + op.w, lim);
           if (a & DFX_AC_ERR) {
-            emit(events, event_count, event_cap, key, fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
+            emit(events, event_count, event_cap, key_now(), fi, var, a & DFX_AC_NODE_MASK, DFX_EV_ERR_BRACES_LOOP, 0);
             L.halted = 1; break;
           }
           pos = DFX_POS_BEFORE; node = a;
         }
         log_plan(DFX_EV_UPDATE_TO, pos, node);
-        if (record) emit(events, event_count, event_cap, key, fi, var, node, DFX_EV_UPDATE_TO, pos);
+        if (record) emit(events, event_count, event_cap, key_now(), fi, var, node, DFX_EV_UPDATE_TO, pos);
         L.D = setb(L.D, cur, 1);
         break;
       }
@@ -298,7 +298,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         if (op.y != myvar || L.halted) break;
         L.presence = 1;
         if (record && (vflags & DFX_V_DECL_LATE)) {
-          emit(events, event_count, event_cap, key, fi, var, op.z, DFX_EV_ERR_DECL, 0);
+          emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_ERR_DECL, 0);
           L.halted = 1; break;
         }
         L.D = setb(L.D, cur, 1); L.H = setb(L.H, cur, 0);
@@ -365,7 +365,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
             for (int i = 0; i < n; i++) {
               int s = arm[i];
               if (!(getb(L.D, s) && !getb(L.H, s))) continue;
-              uint64_t k2 = key | ((uint64_t)rank << 8) | (uint64_t)i;
+              uint64_t k2 = key_now() | ((uint64_t)rank << 8) | (uint64_t)i;
               int kind = __ldg(farms + 2 * (op.y + i)), node = __ldg(farms + 2 * (op.y + i) + 1);
               if (kind == DFX_ARM_ERR_ARM || kind == DFX_ARM_ERR_LOOP) {
                 emit(events, event_count, event_cap, k2, fi, var, node,
@@ -427,9 +427,10 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           copy_slot(f.slot, cur);
           record = f.rec_saved;
           L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
-          pc = f.body_pc;
           __syncwarp();
           if (c.fault) goto fault;
+          sbase += (uint64_t)(pc + 1 - f.body_pc);   // the planning round
+          pc = f.body_pc;
           continue;
         }
         if (f.may_skip) {        // zero-trip skip merge (dataflow.py:575-590)
@@ -446,7 +447,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       }
       case DFX_OP_ERR: {
         if (op.y == 1 && __ldg(item_chunk + item) == 0 && lane == 0)
-          emit(events, event_count, event_cap, key, fi, -1, op.z, DFX_EV_ERR_DATAMAP, 0);
+          emit(events, event_count, event_cap, key_now(), fi, -1, op.z, DFX_EV_ERR_DATAMAP, 0);
         goto halt_all;
       }
       default:
@@ -464,7 +465,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     // keeps the old slot and must stay frozen at this point (D4)
     {
       const uint32_t ew = (uint32_t)__ldg(&fops[pc + op.w].w);
-      seq += (uint64_t)(ew & 0x7FFFFFFFu) - 1u;
+      sbase += (uint64_t)(ew & 0x7FFFFFFFu) - (uint64_t)(op.w + 1);
       pc += op.w + 1;
       if (!(ew >> 31)) continue;
     }
@@ -494,7 +495,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   return;
 fault:
   if (lane == 0)
-    emit(events, event_count, event_cap, seq << 24, fi, 0, 0, DFX_EV_ERR_ENGINE, 0);
+    emit(events, event_count, event_cap, key_now(), fi, 0, 0, DFX_EV_ERR_ENGINE, 0);
 halt_all:
   if (active) var_out[d.var_off + var] = 0;
 }

@@ -73,7 +73,7 @@ __device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, i
 
 // `_State.merge_conj` provenance rule (dataflow.py:135-142)
 __device__ __forceinline__ uint32_t pick(const int32_t* span, uint32_t mine, uint32_t other) {
-  if (other == kNone) return mine;
+  if (other == kNone || other == mine) return mine;
   if (mine == kNone || st_end(span, other) > st_end(span, mine)) return other;
   return mine;
 }
@@ -190,10 +190,12 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   auto merge_conj = [&](int a, int b) {
     L.H = setb(L.H, a, getb(L.H, a) & getb(L.H, b));
     L.D = setb(L.D, a, getb(L.D, a) & getb(L.D, b));
-    uint32_t pa = prov[a * 32 + lane], pb = prov[b * 32 + lane];
-    uint32_t dp = pick(span, pa & 0xFFFFu, pb & 0xFFFFu);
-    uint32_t lw = pick(span, pa >> 16, pb >> 16);
-    prov[a * 32 + lane] = dp | (lw << 16);
+    const uint32_t pa = prov[a * 32 + lane], pb = prov[b * 32 + lane];
+    if (pa != pb) {   // equal provenance (the common case) merges to itself
+      const uint32_t dp = pick(span, pa & 0xFFFFu, pb & 0xFFFFu);
+      const uint32_t lw = pick(span, pa >> 16, pb >> 16);
+      prov[a * 32 + lane] = dp | (lw << 16);
+    }
   };
 
   // op window: lane i holds op (wbase + i); an op is fetched by shuffles

@@ -227,8 +227,9 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     const int4 op = make_int4(__shfl_sync(0xFFFFFFFFu, wop.x, src), __shfl_sync(0xFFFFFFFFu, wop.y, src),
                               __shfl_sync(0xFFFFFFFFu, wop.z, src), __shfl_sync(0xFFFFFFFFu, wop.w, src));
     const int code = op.x & 0xFF, fl = op.x;
-    if (code == DFX_OP_END) break;
     switch (code) {
+      case DFX_OP_END:
+        goto replay_done;
       case DFX_OP_HR: {   // host_read, dataflow.py:299-324
         if (op.y != myvar || L.halted || getb(L.H, cur)) break;
         if (vflags & DFX_V_ALLOW_STALE) {
@@ -319,6 +320,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           }
         }
         __syncwarp();
+        if (c.fault) goto fault;
         break;
       }
       case DFX_OP_ARM_FORK:      // state = saved.copy()  (F_CAPTURE: the arm is this slot)
@@ -328,10 +330,11 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           int s = alloc_slot(c, nslots);
           if (c.narm >= kMaxArmStk) c.fault = 1;
           c.bc0 = s; c.bc1 = b.saved;
+          const bool room = c.narm < kMaxArmStk;
           if (code == DFX_OP_ARM_FORK) {
             ref_dec(c, cur); c.cur = s;
-            if (fl & DFX_F_CAPTURE) { c.armstk[c.narm++] = (uint8_t)s; ref_inc(c, s); b.narms++; }
-          } else {
+            if ((fl & DFX_F_CAPTURE) && room) { c.armstk[c.narm++] = (uint8_t)s; ref_inc(c, s); b.narms++; }
+          } else if (room) {
             c.armstk[c.narm++] = (uint8_t)s; b.narms++;
           }
         }
@@ -340,6 +343,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         copy_slot(s, saved);
         cur = c.cur;
         __syncwarp();
+        if (c.fault) goto fault;
         break;
       }
       case DFX_OP_ARM_CLOSE: {   // switch arm = current slot
@@ -349,6 +353,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           else { c.armstk[c.narm++] = (uint8_t)cur; ref_inc(c, cur); b.narms++; }
         }
         __syncwarp();
+        if (c.fault) goto fault;
         break;
       }
       case DFX_OP_BR_END: {      // _merge_arms, dataflow.py:525-564
@@ -409,7 +414,8 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
           }
         }
         __syncwarp();
-        if (!c.fault) copy_slot(c.bc0, cur);
+        if (c.fault) goto fault;
+        copy_slot(c.bc0, cur);
         record = 0;
         __syncwarp();
         break;
@@ -455,8 +461,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       default:
         goto fault;
     }
-    if (code >= DFX_OP_BR_BEGIN && c.fault) goto fault;   // access ops never fault
-    pc++;
+    pc++;   // (control ops that can fault check c.fault in their case)
     continue;
   skip_region:
     // no access of this warp's variables (and no static error) anywhere in the
@@ -485,6 +490,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       if (c.fault) goto fault;
     }
   }
+replay_done:
   if (active) {
     uint8_t o = 0;
     if (L.presence) o |= DFX_OUT_PRESENCE;

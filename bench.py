@@ -476,7 +476,7 @@ def run_c4(args, rank, world, local):
                "d2h_bytes_per_step": int(d2h // args.e2e_steps),
                "path": "dfx_replay_batch (pinned host buffers): H2D programs in 16 function "
                        "ranges (copy stream), E1 replays per range and one longest-first launch "
-                       "over the last 40% (3 compute streams), D2H events per launch (D2H stream)"}
+                       "over the last 15% (3 compute streams), D2H events per launch (D2H stream)"}
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

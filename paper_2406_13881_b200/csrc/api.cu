@@ -234,9 +234,10 @@ int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap,
   r.events = (dfx_event*)up(nullptr, sizeof(dfx_event) * (size_t)r.event_cap);
   r.event_count = (unsigned long long*)up(nullptr, sizeof(unsigned long long));
   r.var_out = (uint8_t*)up(nullptr, (size_t)in->n_vars + 1);
+  r.next = (unsigned*)up(nullptr, sizeof(unsigned));
   for (void* p : rp->allocs)
     if (!p) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
-  if (rp->allocs.size() != 11) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
+  if (rp->allocs.size() != 12) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
   rp->n_vars = in->n_vars;
   rp->n_funcs = nf;
   CK(cudaEventCreate(&rp->e0));
@@ -395,9 +396,10 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   }
   auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[U]);
   auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (U + 1));
+  auto* d_next = (unsigned*)dbuf(h, "qnext", sizeof(unsigned) * (U + 1));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
   if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
-      !d_cnt || !d_vout)
+      !d_cnt || !d_vout || !d_next)
     return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
   CK(h->pipeline_init());
   cudaStream_t cs[dfx_handle::kComp];
@@ -429,6 +431,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     rk.events = d_ev + ev_off[k];
     rk.event_cap = ev_cap[k];
     rk.event_count = d_cnt + k;
+    rk.next = d_next + k;
     return rk;
   };
   auto lo = [&](int f, int32_t dfx_fn_desc::*off) -> int64_t { return f < nf ? in->fns[f].*off : -1; };
@@ -503,6 +506,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       rk.events = d_re;
       rk.event_cap = need;
       rk.event_count = d_cnt + U;
+      rk.next = d_next + U;
       CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home
       CK(cudaMemsetAsync(d_cnt + U, 0, sizeof(unsigned long long), st));
       int rc = dfx::replay_launch(rk, st);

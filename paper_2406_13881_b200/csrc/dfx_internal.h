@@ -23,6 +23,7 @@ struct ReplayDev {
   int64_t event_cap;
   unsigned long long* event_count;
   uint8_t* var_out;
+  unsigned* next;     // work-queue counter of this launch (cleared by replay_launch)
 };
 
 int replay_launch(const ReplayDev& r, cudaStream_t stream);

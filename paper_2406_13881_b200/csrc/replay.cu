@@ -110,23 +110,16 @@ __device__ __forceinline__ M setb(M m, int s, int v) {   // branch-free bit assi
   return m ^ ((((M)0 - (M)v) ^ m) & bit);
 }
 
+// One work item (function item_fn[item], 32-variable chunk item_chunk[item]).
 template <class M>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
-replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
+__device__ __forceinline__ void
+replay_one(int item, WarpCtl& c, uint32_t* prov, int lane, const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
               const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
               const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
               int n_items, int slots_per_warp, dfx_event* __restrict__ events,
               int64_t event_cap, unsigned long long* __restrict__ event_count,
               uint8_t* __restrict__ var_out) {
-  __shared__ WarpCtl ctl_all[kWarpsPerBlock];
-  extern __shared__ uint32_t prov_all[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x * kWarpsPerBlock + warp;
-  if (item >= n_items) return;
-  WarpCtl& c = ctl_all[warp];
-  uint32_t* prov = prov_all + warp * slots_per_warp * 32;
-
   const int fi = __ldg(item_fn + item);
   const dfx_fn_desc d = fns[fi];
   const int chunk = __ldg(item_chunk + item);
@@ -508,6 +501,34 @@ halt_all:
   if (active) var_out[d.var_off + var] = 0;
 }
 
+// Persistent: each warp takes work items from `next` (one atomic per item)
+// until none are left, so no warp idles on the rest of its block and the
+// long items (first in the order) never wait for a block slot.
+template <class M>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
+              const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
+              const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
+              const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
+              int n_items, int slots_per_warp, dfx_event* __restrict__ events,
+              int64_t event_cap, unsigned long long* __restrict__ event_count,
+              uint8_t* __restrict__ var_out, unsigned* __restrict__ next) {
+  __shared__ WarpCtl ctl_all[kWarpsPerBlock];
+  extern __shared__ uint32_t prov_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpCtl& c = ctl_all[warp];
+  uint32_t* prov = prov_all + warp * slots_per_warp * 32;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(next, 1u);
+    item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    if (item >= n_items) return;
+    replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
+                  item_chunk, n_items, slots_per_warp, events, event_cap, event_count, var_out);
+    __syncwarp();
+  }
+}
+
 // Region table, one thread per function (runs before the replay of the same
 // function range, on the same stream).  For every BR_BEGIN / LOOP_BEGIN it
 // writes into the device copy of the program
@@ -591,22 +612,27 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream) {
   int slots = r.max_slots;
   if (slots < 2) slots = 2;
   if (slots > kMaxSlots) return DFX_E_LIMIT;
-  size_t smem = (size_t)kWarpsPerBlock * slots * 32 * sizeof(uint32_t);
-  int blocks = (r.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (blocks == 0) return DFX_OK;
-  // slot bitmasks in 32-bit registers when every function of the batch needs
-  // at most 32 live state slots (all of C4), else 64-bit
-  if (slots <= 32) {
-    cudaFuncSetAttribute(replay_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    replay_kernel<uint32_t><<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
+  const size_t smem = (size_t)kWarpsPerBlock * slots * 32 * sizeof(uint32_t);
+  const int need = (r.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (need == 0) return DFX_OK;
+  if (cudaMemsetAsync(r.next, 0, sizeof(unsigned), stream) != cudaSuccess) return DFX_E_CUDA;
+  // a persistent grid (resident blocks x SMs) over the item queue; slot
+  // bitmasks in 32-bit registers when every function of the batch needs at
+  // most 32 live state slots (all of C4), else 64-bit
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
+    int blocks = sms * (per_sm > 0 ? per_sm : 1);
+    if (blocks > need) blocks = need;
+    kern<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
         r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
-        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
-  } else {
-    cudaFuncSetAttribute(replay_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    replay_kernel<uint64_t><<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
-        r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
-        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out);
-  }
+        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out, r.next);
+  };
+  if (slots <= 32) launch(replay_kernel<uint32_t>);
+  else launch(replay_kernel<uint64_t>);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 

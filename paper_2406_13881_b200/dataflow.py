@@ -16,6 +16,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import gc
+
 import numpy as np
 
 from . import _abi
@@ -228,23 +230,24 @@ def decode(prog: FnProgram, src, accesses, events: np.ndarray,
             errs = events[events["kind"] >= _abi.EV_ERR_DATAMAP]
             _raise_error(prog, src, errs[0])
         keys: set = set()
-        pvars, pstmts, fp_kind = prog.vars, prog.stmts, PlanKind.FIRSTPRIVATE
+        pstmts = prog.stmts
+        names = [v.name for v in prog.vars]
+        suppress, fp = _abi.EV_SUPPRESS, _abi.EV_FIRSTPRIVATE
         for kind, vi, ni, pi in zip(kinds, events["var"].tolist(), events["node"].tolist(),
                                     events["pos"].tolist()):
-            name = pvars[vi].name
-            if kind == _abi.EV_SUPPRESS:
+            name = names[vi]
+            if kind == suppress:
                 if name not in suppressed:
                     suppressed.append(name)
                 continue
-            anchor = pstmts[ni]
-            pos = _POS[pi]
-            pk = _PLAN_KIND[kind]
-            key = (pk, name, id(anchor), pos)           # `dataflow.py:264`
+            # `_add_plan`'s key (`dataflow.py:264`): kind, name, anchor
+            # identity (one statement per node index), position
+            key = (kind, name, ni, pi)
             if key in keys:
                 continue
             keys.add(key)
-            (firstprivates if pk is fp_kind else updates).append(
-                DirectivePlan(pk, (name,), anchor, pos))
+            (firstprivates if kind == fp else updates).append(
+                DirectivePlan(_PLAN_KIND[kind], (name,), pstmts[ni], _POS[pi]))
     # sets (`dataflow.py:214-216`) and `_escape_liveness` (`:671-676`)
     presence, to_comp, from_comp = set(), set(), set()
     for i, var in enumerate(prog.vars):
@@ -445,11 +448,24 @@ def _first_occurrences(evs: np.ndarray) -> np.ndarray:
     `decode` need not see it.  Error events are always kept."""
     if evs.shape[0] < 2:
         return np.ones(evs.shape[0], dtype=bool)
-    rec = np.empty(evs.shape[0], dtype=[("fn", "<i4"), ("var", "<i4"), ("node", "<i4"),
-                                        ("kind", "u1"), ("pos", "u1")])
-    for f in ("fn", "var", "node", "kind", "pos"):
-        rec[f] = evs[f]
-    _, first = np.unique(rec, return_index=True)
+    fn = evs["fn"].astype(np.int64)
+    var = evs["var"].astype(np.int64) + 1          # -1 (function-level errors) -> 0
+    node = evs["node"].astype(np.int64)
+    if (fn.min() >= 0 and fn.max() < (1 << 27) and var.max() < (1 << 15) and node.min() >= 0
+            and node.max() < (1 << 16)):
+        key = (fn << 36) | (var << 21) | (node << 5) | (evs["kind"].astype(np.int64) << 2) \
+            | evs["pos"].astype(np.int64)
+        _, first = np.unique(key, return_index=True)
+    else:
+        order = np.lexsort((evs["pos"], evs["kind"], node, var, fn))
+        k = np.stack([fn[order], var[order], node[order], evs["kind"][order].astype(np.int64),
+                      evs["pos"][order].astype(np.int64)])
+        new = np.ones(order.shape[0], dtype=bool)
+        new[1:] = (k[:, 1:] != k[:, :-1]).any(axis=0)
+        # first occurrence in event order of each distinct record
+        grp = np.cumsum(new) - 1
+        first = np.full(int(grp[-1]) + 1, np.iinfo(np.int64).max)
+        np.minimum.at(first, grp, order)
     keep = np.zeros(evs.shape[0], dtype=bool)
     keep[first] = True
     keep |= evs["kind"] >= _abi.EV_ERR_DATAMAP
@@ -464,6 +480,21 @@ def analyze_functions(items, allow_stale: frozenset[str] = frozenset(),
     `FunctionPlan` or raises the reference's exception).  `precheck(progs)`
     runs after the lowering and before the launch (the unit-level input
     checks of `plan_transform`, fed by the per-function lowering)."""
+    # The batch allocates a few objects per event on top of the caller's
+    # parse (millions of long-lived AST objects), so the cyclic collector's
+    # full passes -- each a walk of that whole heap -- would cost more than
+    # the analysis; it is paused for the call (nothing built here is cyclic
+    # garbage) and restored as it was.
+    gc_was = gc.isenabled()
+    gc.disable()
+    try:
+        return _analyze_functions(items, allow_stale, runner, precheck)
+    finally:
+        if gc_was:
+            gc.enable()
+
+
+def _analyze_functions(items, allow_stale, runner, precheck) -> list[_Deferred]:
     progs = lower_functions(items, allow_stale)
     if precheck is not None:
         precheck(progs)

@@ -33,3 +33,28 @@ def test_requirement_lists_split_on_firstprivate_flag():
     assert req[0, 0] == 2 and req[0, 1] == 1 << 8 and fp[0, 0] == 1 << 5
     assert not req[1].any() and not fp[1].any()
     assert req[2, 3] == 1 << 31 and fp[2, 0] == 1
+
+
+def test_first_occurrences_matches_a_python_scan():
+    """`dataflow._first_occurrences` (the event dedup before decode), both the
+    packed-key path and the lexsort path (forced by an out-of-range node)."""
+    import numpy as np
+    from paper_2406_13881_b200 import _abi
+    from paper_2406_13881_b200.dataflow import _first_occurrences
+    rng = np.random.default_rng(5)
+    for big in (False, True):
+        n = 3000
+        ev = np.zeros(n, dtype=_abi.EVENT_DTYPE)
+        ev["fn"] = np.sort(rng.integers(0, 40, n))
+        ev["key"] = np.arange(n)
+        ev["var"] = rng.integers(-1, 6, n)
+        ev["node"] = rng.integers(0, 5, n) + (70000 if big else 0)
+        ev["kind"] = rng.integers(1, 5, n)
+        ev["pos"] = rng.integers(0, 3, n)
+        ev["kind"][::97] = _abi.EV_ERR_DATAMAP          # errors are always kept
+        seen, exp = set(), np.zeros(n, dtype=bool)
+        for i, e in enumerate(ev):
+            k = (int(e["fn"]), int(e["var"]), int(e["node"]), int(e["kind"]), int(e["pos"]))
+            exp[i] = k not in seen or int(e["kind"]) >= _abi.EV_ERR_DATAMAP
+            seen.add(k)
+        assert np.array_equal(_first_occurrences(ev), exp)

@@ -343,10 +343,11 @@ class _Deferred:
 # (SURVEY §8f rank 1).  Functions are independent, so large batches are
 # lowered by forked worker processes that see the parsed translation unit
 # copy-on-write.  Objects cannot cross processes, so a worker returns the
-# program's arrays with node and variable references as indices (a node's
-# child-index path from the function's AST root; index of an access naming
-# the variable), and the parent maps them back to its own objects -- the
-# FunctionPlan anchors stay the caller's AstNodes.
+# program's arrays with node and variable references as indices (the CFG
+# node id of a statement that is one, else a child-index path from the
+# function's AST root; index of an access naming the variable), and the
+# parent maps them back to its own objects -- the FunctionPlan anchors stay
+# the caller's AstNodes.
 _FORK_ITEMS: list = []
 _FORK_ALLOW: frozenset = frozenset()
 
@@ -367,6 +368,19 @@ def _follow(root, path):
     return root
 
 
+def _ref(node, root, cfg):
+    """A node reference that survives the process boundary: the id of the
+    CFG node it is the statement of (most statements), else its child path."""
+    cn = cfg.node_of_ast.get(node)
+    if cn is not None and cn.ast is node and cfg.nodes[cn.id] is cn:
+        return cn.id
+    return _path(node, root)
+
+
+def _deref(ref, root, cfg):
+    return cfg.nodes[ref].ast if isinstance(ref, int) else _follow(root, ref)
+
+
 def _lower_portable(i: int):
     src, cfg, accs, table = _FORK_ITEMS[i]
     try:
@@ -378,11 +392,11 @@ def _lower_portable(i: int):
     for j, a in enumerate(accs):
         first.setdefault(id(a.var), j)
     try:
-        stmts = [_path(n, root) for n in prog.stmts]
-        kstmts = [_path(n, root) for n in prog.kernel_stmts]
-        region = None if prog.region is None else [_path(n, root) for n in prog.region]
+        stmts = [_ref(n, root, cfg) for n in prog.stmts]
+        kstmts = [_ref(n, root, cfg) for n in prog.kernel_stmts]
+        region = None if prog.region is None else [_ref(n, root, cfg) for n in prog.region]
         vars_ = [first[id(v)] for v in prog.vars]
-        premapped = None if prog.premapped is None else _path(prog.premapped, root)
+        premapped = None if prog.premapped is None else _ref(prog.premapped, root, cfg)
     except (KeyError, AttributeError, StopIteration):
         return ("serial", None)  # a reference not reachable this way: lower in the parent
     fields = {k: getattr(prog, k) for k in ("ops", "var_flags", "stmt_span", "sites", "arms",
@@ -431,12 +445,14 @@ def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | 
             continue
         fields, stmts, kstmts, region, vars_, premapped = r
         root = cfg.function
+        cfg_nodes = cfg.nodes
         progs.append(FnProgram(fn=root, **fields,
                                vars=[accs[j].var for j in vars_],
-                               stmts=[_follow(root, q) for q in stmts],
-                               kernel_stmts=[_follow(root, q) for q in kstmts],
-                               region=None if region is None else tuple(_follow(root, q) for q in region),
-                               premapped=None if premapped is None else _follow(root, premapped)))
+                               stmts=[cfg_nodes[q].ast if q.__class__ is int else _follow(root, q)
+                                      for q in stmts],
+                               kernel_stmts=[_deref(q, root, cfg) for q in kstmts],
+                               region=None if region is None else tuple(_deref(q, root, cfg) for q in region),
+                               premapped=None if premapped is None else _deref(premapped, root, cfg)))
     return progs
 
 

@@ -219,13 +219,21 @@ def decode(prog: FnProgram, src, accesses, events: np.ndarray,
            var_out: np.ndarray, presorted: bool = False) -> FunctionPlan:
     """Events of one function (any order, or key order with `presorted`) +
     per-variable bits -> FunctionPlan."""
+    if events.shape[0] and not presorted:
+        events = events[np.argsort(events["key"], kind="stable")]
+    return _decode_cols(prog, src, accesses, events, events["kind"].tolist(),
+                        events["var"].tolist(), events["node"].tolist(),
+                        events["pos"].tolist(), var_out)
+
+
+def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
+                 var_out) -> FunctionPlan:
+    """`decode` on the event columns as lists (key order); `events` (the same
+    events as a structured array) is read only to raise an error."""
     updates: list = []
     firstprivates: list = []
     suppressed: list[str] = []
-    if events.shape[0]:
-        if not presorted:
-            events = events[np.argsort(events["key"], kind="stable")]
-        kinds = events["kind"].tolist()
+    if kinds:
         if max(kinds) >= _abi.EV_ERR_DATAMAP:
             errs = events[events["kind"] >= _abi.EV_ERR_DATAMAP]
             _raise_error(prog, src, errs[0])
@@ -233,8 +241,7 @@ def decode(prog: FnProgram, src, accesses, events: np.ndarray,
         pstmts = prog.stmts
         names = [v.name for v in prog.vars]
         suppress, fp = _abi.EV_SUPPRESS, _abi.EV_FIRSTPRIVATE
-        for kind, vi, ni, pi in zip(kinds, events["var"].tolist(), events["node"].tolist(),
-                                    events["pos"].tolist()):
+        for kind, vi, ni, pi in zip(kinds, vis, nis, pis):
             name = names[vi]
             if kind == suppress:
                 if name not in suppressed:
@@ -519,14 +526,18 @@ def _analyze_functions(items, allow_stale, runner, precheck) -> list[_Deferred]:
     order = np.lexsort((raw.events["key"], raw.events["fn"]))   # by function, then visit key
     evs = raw.events[order]
     evs = evs[_first_occurrences(evs)]
-    bounds = np.searchsorted(evs["fn"], np.arange(len(progs) + 1))
+    bounds = np.searchsorted(evs["fn"], np.arange(len(progs) + 1)).tolist()
+    # columns once, as lists; per function a slice of each
+    kinds, vis = evs["kind"].tolist(), evs["var"].tolist()
+    nis, pis = evs["node"].tolist(), evs["pos"].tolist()
+    var_off, n_vars = batch.fns["var_off"].tolist(), batch.fns["n_vars"].tolist()
     out = []
     for i, (p, (src, cfg, accs, table)) in enumerate(zip(progs, items)):
-        d = batch.fns[i]
-        vo = raw.var_out[int(d["var_off"]):int(d["var_off"]) + int(d["n_vars"])]
+        a, b = bounds[i], bounds[i + 1]
+        vo = raw.var_out[var_off[i]:var_off[i] + n_vars[i]]
         try:
-            out.append(_Deferred(plan=decode(p, src, accs, evs[bounds[i]:bounds[i + 1]], vo,
-                                             presorted=True)))
+            out.append(_Deferred(plan=_decode_cols(p, src, accs, evs[a:b], kinds[a:b], vis[a:b],
+                                                   nis[a:b], pis[a:b], vo)))
         except Exception as e:  # the reference's ToolError subclasses
             out.append(_Deferred(error=e))
     return out

@@ -21,7 +21,7 @@ def wrap(name, f):
 df.lower_functions = wrap("lower", df.lower_functions)
 df.pack = wrap("pack", df.pack)
 df.run_replay = wrap("replay", df.run_replay)
-df.decode = wrap("decode", df.decode)
+df._decode_cols = wrap("decode", df._decode_cols)
 for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     T.clear()
     t = time.perf_counter(); eng.plan_transform(a); tot = time.perf_counter() - t

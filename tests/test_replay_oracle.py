@@ -101,6 +101,7 @@ def test_parallel_lowering_equals_serial():
         assert all(x is y for x, y in zip(p.stmts, s.stmts)) and len(p.stmts) == len(s.stmts)
         assert all(x is y for x, y in zip(p.vars, s.vars)) and len(p.vars) == len(s.vars)
         assert all(x is y for x, y in zip(p.kernel_stmts, s.kernel_stmts))
+        assert p.premapped is s.premapped
         assert (p.region is None) == (s.region is None)
         if p.region is not None:
             assert all(x is y for x, y in zip(p.region, s.region))

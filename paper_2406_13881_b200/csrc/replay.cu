@@ -33,8 +33,9 @@ constexpr uint32_t kNone = 0xFFFFu;
 struct BrFrame { int16_t saved, arm_base, narms, pad; };
 struct LoopFrame { int32_t stmt, body_pc, loop_start; int16_t slot; int8_t round, may_skip, rec_saved, pad[3]; };
 
+template <class M>
 struct WarpCtl {
-  unsigned long long live;   // bit i: ref[i] > 0
+  M live;                    // bit i: ref[i] > 0 (slot masks as wide as the lane's H/D masks)
   uint8_t ref[kMaxSlots];
   BrFrame br[kMaxBr];
   uint8_t armstk[kMaxArmStk];
@@ -47,17 +48,23 @@ __device__ __forceinline__ int st_start(const int32_t* span, int s) { return __l
 __device__ __forceinline__ int st_end(const int32_t* span, int s) { return __ldg(span + 2 * s + 1); }
 
 // first free slot from the live mask (lane 0 only)
-__device__ __forceinline__ int alloc_slot(WarpCtl& c, int nslots) {
-  const unsigned long long avail = ~c.live & (nslots >= 64 ? ~0ull : ((1ull << nslots) - 1ull));
+template <class M>
+__device__ __forceinline__ int alloc_slot(WarpCtl<M>& c, int nslots) {
+  constexpr int kBits = 8 * sizeof(M);
+  const M avail = ~c.live & (nslots >= kBits ? ~(M)0 : (((M)1 << nslots) - (M)1));
   if (!avail) { c.fault = 1; return 0; }
-  const int i = __ffsll((long long)avail) - 1;
+  int i;
+  if constexpr (sizeof(M) == 4) i = __ffs((int)avail) - 1;
+  else i = __ffsll((long long)avail) - 1;
   c.ref[i] = 1;
-  c.live |= 1ull << i;
+  c.live |= (M)1 << i;
   return i;
 }
-__device__ __forceinline__ void ref_inc(WarpCtl& c, int i) { c.ref[i]++; }
-__device__ __forceinline__ void ref_dec(WarpCtl& c, int i) {
-  if (--c.ref[i] == 0) c.live &= ~(1ull << i);
+template <class M>
+__device__ __forceinline__ void ref_inc(WarpCtl<M>& c, int i) { c.ref[i]++; }
+template <class M>
+__device__ __forceinline__ void ref_dec(WarpCtl<M>& c, int i) {
+  if (--c.ref[i] == 0) c.live &= ~((M)1 << i);
 }
 
 __device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, int64_t cap,
@@ -113,7 +120,7 @@ __device__ __forceinline__ M setb(M m, int s, int v) {   // branch-free bit assi
 // One work item (function item_fn[item], 32-variable chunk item_chunk[item]).
 template <class M>
 __device__ __forceinline__ void
-replay_one(int item, WarpCtl& c, uint32_t* prov, int lane, const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
+replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
               const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
               const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
@@ -141,7 +148,7 @@ replay_one(int item, WarpCtl& c, uint32_t* prov, int lane, const dfx_fn_desc* __
 
   if (lane == 0) {
     for (int i = 0; i < kMaxSlots; i++) c.ref[i] = 0;
-    c.live = 0ull;
+    c.live = (M)0;
     c.nbr = c.narm = c.nlp = 0;
     c.record = 1;
     c.fault = 0;
@@ -513,10 +520,10 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
               int n_items, int slots_per_warp, dfx_event* __restrict__ events,
               int64_t event_cap, unsigned long long* __restrict__ event_count,
               uint8_t* __restrict__ var_out, unsigned* __restrict__ next) {
-  __shared__ WarpCtl ctl_all[kWarpsPerBlock];
+  __shared__ WarpCtl<M> ctl_all[kWarpsPerBlock];
   extern __shared__ uint32_t prov_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpCtl& c = ctl_all[warp];
+  WarpCtl<M>& c = ctl_all[warp];
   uint32_t* prov = prov_all + warp * slots_per_warp * 32;
   for (;;) {
     int item = 0;

@@ -348,7 +348,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   // each of the last ranges.
   int m = K;
   if (K > 1) {
-    double merge_at = 0.85;   // measured: 0.6 / 0.75 / 0.85 / 0.93 / none -> 250 / 246 / 245 / 244 / 243 ms
+    double merge_at = 0.85;   // C4, persistent replay: 0.5 / 0.85 / none -> 269 / 221 / 236 ms
     if (const char* e = getenv("DFX_MERGE_AT")) merge_at = atof(e);
     m = 1;
     while (m < K && (double)(cut[m] < nf ? in->fns[cut[m]].op_off : in->n_ops) <

@@ -106,3 +106,22 @@ def test_host_buffer_call_with_uneven_event_density():
     small = ReplaySession(event_cap=1000)                          # NOSPC -> regrow
     got = small.run(b2)
     _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+
+
+@pytest.mark.gpu
+def test_cuda_replay_many_chunks_and_wide_slot_masks():
+    """Functions with 2,048 variables (64 warps each: the region table's
+    32-bit chunk masks alias chunk c and c + 32, which may only make a warp
+    skip less) and, separately, a batch whose slot budget exceeds 32, which
+    selects the 64-bit slot-mask kernel; both equal to the oracle."""
+    from paper_2406_13881_b200.batch import C4Config, c4_generate
+    b, _ = c4_generate(C4Config(n_funcs=40, n_min=64, n_max=600, var_choices=(2048,)),
+                       np.arange(40))
+    exp = run_replay(b, runner=_oracle.replay_runner_mt)
+    got = run_replay(b)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+    b2, _ = c4_generate(_cfg(), np.arange(120))
+    b2.fns["n_slots"][::7] = 48          # a larger budget than needed: same results
+    exp = run_replay(b2, runner=_oracle.replay_runner_mt)
+    got = run_replay(b2)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)

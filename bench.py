@@ -475,8 +475,9 @@ def run_c4(args, rank, world, local):
                "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h // args.e2e_steps),
                "path": "dfx_replay_batch (pinned host buffers): H2D programs in 16 function "
-                       "ranges (copy stream), E1 replays per range and one longest-first launch "
-                       "over the last 15% (3 compute streams), D2H events per launch (D2H stream)"}
+                       "ranges (copy stream), region tables per range (2 streams), one persistent "
+                       "E1 launch whose items wait for their range, D2H events per range as it "
+                       "completes (D2H stream)"}
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -1,9 +1,11 @@
 // api.cu -- C ABI of libdfx.so (include/dfx.h): handles, buffers, entry points.
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -25,6 +27,9 @@ struct dfx_handle {
   cudaEvent_t jev[kComp] = {};        // joins of the compute streams
   cudaEvent_t pev[1 + 2 * kPipeMax] = {};
   unsigned long long* pin_cnt = nullptr;   // pinned, kPipeMax counters
+  unsigned long long* host_done = nullptr; // mapped pinned: E1 range k complete (count + 1)
+  unsigned long long* host_done_dev = nullptr;
+  int* pin_one = nullptr;                  // pinned 1s: E1 range-ready flags (H2D)
   cudaError_t pipeline_init() {
     if (s_copy) return cudaSuccess;
     cudaError_t e = cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking);
@@ -36,6 +41,12 @@ struct dfx_handle {
     for (auto& ev : pev)
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&pin_cnt, sizeof(unsigned long long) * kPipeMax, cudaHostAllocDefault);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc((void**)&host_done, sizeof(unsigned long long) * kPipeMax, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&host_done_dev, host_done, 0);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&pin_one, sizeof(int) * kPipeMax, cudaHostAllocDefault);
+    if (e == cudaSuccess)
+      for (int i = 0; i < kPipeMax; i++) pin_one[i] = 1;
     return e;
   }
   int device = 0;
@@ -128,6 +139,8 @@ int dfx_close(dfx_handle* h) {
   for (auto& ev : h->pev)
     if (ev) cudaEventDestroy(ev);
   if (h->pin_cnt) cudaFreeHost(h->pin_cnt);
+  if (h->host_done) cudaFreeHost(h->host_done);
+  if (h->pin_one) cudaFreeHost(h->pin_one);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
   for (auto& cs : h->s_comp)
@@ -315,14 +328,20 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
                  d.arm_off >= e.arm_off;
     }
   }
-  // Pipeline over function ranges: the H2D of range k+1 (copy stream), the
-  // replay of range k (compute stream) and the D2H of range k-1's events
-  // (D2H stream) overlap.  Functions are independent (SURVEY F3 / SPEC), so
-  // ranges change nothing but the order of events in the buffer.  Range sizes
-  // (by ops) ramp up by 1.4x -- the replay of a range outlasts the H2D of the
-  // next one -- so the first H2D, which nothing overlaps, is short; they ramp
-  // down at the end for the same reason on the D2H side.
-  const int K = ordered && nf >= 256 ? dfx_handle::kPipeMax : 1;
+  // Pipeline: the programs go H2D in K function ranges (copy stream); a
+  // region stream builds each range's region table as it lands and then
+  // opens the range (ready[k] = 1); ONE persistent replay launch takes the
+  // work items in range order, each waiting only for its own range
+  // (GateDev), so the replay runs while the H2D of later ranges is still in
+  // flight; range k's events go home (D2H stream) as soon as its last item
+  // is done, which the kernel publishes in mapped host memory.  Functions
+  // are independent (SURVEY F3 / SPEC), so ranges change nothing but the
+  // order of events in the buffer.  Range sizes (by ops) ramp up and down by
+  // 1.4x: the first H2D, which nothing overlaps, is short, and so is the
+  // last range, which ends the launch.  Ranges start at functions whose ops
+  // begin on a 128-B line: no L1 line read by one range holds another
+  // range's region table before it is written.
+  int K = ordered && nf >= 256 ? dfx_handle::kPipeMax : 1;
   std::vector<int> cut(K + 1, nf);
   cut[0] = 0;
   if (K > 1) {
@@ -338,33 +357,17 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     for (int k = 1; k < K; k++) {
       acc += w[k - 1] / tot;
       while (f < nf && (double)in->fns[f].op_off < acc * (double)in->n_ops) f++;
+      while (f < nf && (in->fns[f].op_off & 7) != 0) f++;   // line-aligned start
       cut[k] = f;
     }
+    if (in->fns[0].op_off & 7) K = 1;        // the first range must start aligned too
   }
-  // Replays run per launch unit: ranges 0..m-1 one unit each, ranges m..K-1
-  // (the last 15% of the ops; $DFX_MERGE_AT) one unit, items longest first.  By the time the
-  // compute streams reach that unit its inputs are resident, and one launch
-  // sorted over all of them ends on short items, not on the long items of
-  // each of the last ranges.
-  int m = K;
-  if (K > 1) {
-    double merge_at = 0.85;   // C4, persistent replay: 0.5 / 0.85 / none -> 269 / 221 / 236 ms
-    if (const char* e = getenv("DFX_MERGE_AT")) merge_at = atof(e);
-    m = 1;
-    while (m < K && (double)(cut[m] < nf ? in->fns[cut[m]].op_off : in->n_ops) <
-                        merge_at * (double)in->n_ops)
-      m++;
-  }
-  const int U = m < K ? m + 1 : K;
-  std::vector<int> ucut(U + 1, nf), last_range(U, K - 1);
-  for (int u = 0; u < U; u++) {
-    ucut[u] = cut[u];
-    if (u < m) last_range[u] = u;
-  }
-  std::vector<int32_t> range_item0(U + 1, 0);
-  for (int u = 0; u < U; u++) {
-    append_items(in->fns, ucut[u], ucut[u + 1], item_fn, item_chunk);
-    range_item0[u + 1] = (int32_t)item_fn.size();
+  if (K == 1) { cut.assign(2, nf); cut[0] = 0; }
+  std::vector<int32_t> range_item0(K + 1, 0), range_items(K, 0);
+  for (int k = 0; k < K; k++) {
+    append_items(in->fns, cut[k], cut[k + 1], item_fn, item_chunk);
+    range_item0[k + 1] = (int32_t)item_fn.size();
+    range_items[k] = range_item0[k + 1] - range_item0[k];
   }
   const size_t n_items = item_fn.size();
   cudaStream_t st = h->st();
@@ -377,41 +380,53 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   void* d_ifn = dbuf(h, "ifn", sizeof(int32_t) * n_items + 16);
   void* d_ich = dbuf(h, "ich", sizeof(int32_t) * n_items + 16);
   const int64_t cap = out->event_cap;
-  // Per-range event regions and counters: consecutive ranges replay on
-  // different compute streams, so range k+1 fills the SMs while range k drains
-  // its longest warps (a range lasts at least as long as its longest function).
-  // A region is sized from the caller's capacity in proportion to the range's
-  // ops; a range that overflows its region is replayed again into a region of
-  // the exact size (rare), unless the total already exceeds the caller's
-  // capacity (then the call reports DFX_E_NOSPC with the total, as before).
-  std::vector<int64_t> ev_off(U + 1, 0), ev_cap(U, 0);
-  for (int u = 0; u < U; u++) {
-    const int f0 = ucut[u], f1 = ucut[u + 1];
-    int64_t ops_u = 0;
-    if (U == 1) ops_u = in->n_ops;
-    else if (f0 < f1) ops_u = (f1 < nf ? (int64_t)in->fns[f1].op_off : in->n_ops) - in->fns[f0].op_off;
-    const double share = in->n_ops > 0 ? (double)ops_u / (double)in->n_ops : 1.0;
-    ev_cap[u] = (int64_t)(1.25 * (double)(cap > 0 ? cap : 0) * share) + 4096;
-    ev_off[u + 1] = ev_off[u] + ev_cap[u];
+  // per-range event regions, sized from the caller's capacity by ops share;
+  // a range that overflows its region is replayed again into an exact-size
+  // one (rare) unless the total already exceeds the caller's capacity
+  std::vector<long long> ev_off(K + 1, 0), ev_cap(K, 0);
+  for (int k = 0; k < K; k++) {
+    const int f0 = cut[k], f1 = cut[k + 1];
+    int64_t ops_k = 0;
+    if (K == 1) ops_k = in->n_ops;
+    else if (f0 < f1) ops_k = (f1 < nf ? (int64_t)in->fns[f1].op_off : in->n_ops) - in->fns[f0].op_off;
+    const double share = in->n_ops > 0 ? (double)ops_k / (double)in->n_ops : 1.0;
+    ev_cap[k] = (long long)(1.25 * (double)(cap > 0 ? cap : 0) * share) + 4096;
+    ev_off[k + 1] = ev_off[k] + ev_cap[k];
   }
-  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[U]);
-  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (U + 1));
-  auto* d_next = (unsigned*)dbuf(h, "qnext", sizeof(unsigned) * (U + 1));
+  auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[K]);
+  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (K + 1));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
+  // gate block: fn_cut[K+1] ready[K] range_items[K] items_done[K] next[2]
+  // timed_out[1] (ints), then ev_off[K] ev_cap[K] (long long)
+  const size_t gate_ints = (size_t)(K + 1) + 3 * (size_t)K + 3;
+  auto* d_gate = (int*)dbuf(h, "gate", sizeof(int) * gate_ints + 16 + 2 * sizeof(long long) * K);
   if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
-      !d_cnt || !d_vout || !d_next)
+      !d_cnt || !d_vout || !d_gate)
     return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
+  int* g_cut = d_gate;
+  int* g_ready = g_cut + K + 1;
+  int* g_items = g_ready + K;
+  int* g_done = g_items + K;
+  int* g_next = g_done + K;          // [0] the launch, [1] a redo
+  int* g_timeout = g_next + 2;
+  auto* g_evoff = reinterpret_cast<long long*>(
+      reinterpret_cast<uintptr_t>(d_gate + gate_ints + 1) & ~(uintptr_t)7) + 1;
+  long long* g_evcap = g_evoff + K;
   CK(h->pipeline_init());
-  cudaStream_t cs[dfx_handle::kComp];
-  cs[0] = st;
-  for (int i = 1; i < dfx_handle::kComp; i++) cs[i] = h->s_comp[i];
+  for (int k = 0; k < K; k++) h->host_done[k] = 0ull;
   // small arrays first, on the call's stream
+  std::vector<int> gate_host(gate_ints, 0);
+  for (int k = 0; k <= K; k++) gate_host[k] = cut[k];
+  for (int k = 0; k < K; k++) gate_host[2 * K + 1 + k] = range_items[k];
   CK(cudaMemcpyAsync(d_fns, in->fns, sizeof(dfx_fn_desc) * (size_t)nf, cudaMemcpyHostToDevice, st));
   if (n_items) {
     CK(cudaMemcpyAsync(d_ifn, item_fn.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_ich, item_chunk.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
   }
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (U + 1), st));
+  CK(cudaMemcpyAsync(d_gate, gate_host.data(), sizeof(int) * gate_ints, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(g_evoff, ev_off.data(), sizeof(long long) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(g_evcap, ev_cap.data(), sizeof(long long) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (K + 1), st));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -419,30 +434,42 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   r.stmt_span = (const int32_t*)d_span;
   r.sites = (const int32_t*)d_sites;
   r.arms = (const int32_t*)d_arms;
+  r.item_fn = (const int32_t*)d_ifn;
+  r.item_chunk = (const int32_t*)d_ich;
+  r.n_items = (int)n_items;
+  r.fn_lo = 0;
+  r.fn_hi = nf;
   r.max_slots = max_slots;
+  r.events = d_ev;
+  r.event_cap = cap;
+  r.event_count = d_cnt;
   r.var_out = d_vout;
-  auto range_dev = [&](int k) {
-    dfx::ReplayDev rk = r;
-    rk.item_fn = (const int32_t*)d_ifn + range_item0[k];
-    rk.item_chunk = (const int32_t*)d_ich + range_item0[k];
-    rk.n_items = range_item0[k + 1] - range_item0[k];
-    rk.fn_lo = ucut[k];
-    rk.fn_hi = ucut[k + 1];
-    rk.events = d_ev + ev_off[k];
-    rk.event_cap = ev_cap[k];
-    rk.event_count = d_cnt + k;
-    rk.next = d_next + k;
-    return rk;
-  };
+  r.next = reinterpret_cast<unsigned*>(g_next);
+  dfx::GateDev gate{};
+  gate.K = K;
+  gate.fn_cut = g_cut;
+  gate.ready = g_ready;
+  gate.ev_off = g_evoff;
+  gate.ev_cap = g_evcap;
+  gate.range_items = reinterpret_cast<const unsigned*>(g_items);
+  gate.items_done = reinterpret_cast<unsigned*>(g_done);
+  gate.host_done = h->host_done_dev;
+  gate.timed_out = reinterpret_cast<unsigned*>(g_timeout);
   auto lo = [&](int f, int32_t dfx_fn_desc::*off) -> int64_t { return f < nf ? in->fns[f].*off : -1; };
-  CK(cudaEventRecord(h->pev[0], st));   // fns/items uploaded, counters cleared
+  // region tables on two streams, alternating by range: a region kernel
+  // shares the SMs with the running replay, so consecutive ranges' tables
+  // are built side by side rather than one after the other
+  cudaStream_t s_regs[2] = {h->s_comp[1], h->s_comp[2]};
+  CK(cudaEventRecord(h->pev[0], st));   // uploads done, gate state cleared
   if (h->trace) CK(cudaEventRecord(h->tev[3 * dfx_handle::kPipeMax], st));
   CK(cudaStreamWaitEvent(h->s_copy, h->pev[0], 0));
-  for (int i = 1; i < dfx_handle::kComp; i++) CK(cudaStreamWaitEvent(cs[i], h->pev[0], 0));
+  for (cudaStream_t sr : s_regs) CK(cudaStreamWaitEvent(sr, h->pev[0], 0));
+  // every copy and region launch is enqueued before the replay launch (a
+  // failed enqueue must not leave the kernel waiting for a range)
   for (int k = 0; k < K; k++) {
     const int f0 = cut[k], f1 = cut[k + 1];
     if (f0 < f1) {
-      struct Rng { const int32_t* src; void* dst; int64_t a, b; int unit; };
+      struct Rng { const int32_t* src; void* dst; int64_t a, b, n; int unit; };
       const int64_t ops_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::op_off);
       const int64_t ops_b = K == 1 || f1 == nf ? in->n_ops : lo(f1, &dfx_fn_desc::op_off);
       const int64_t vf_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::var_off);
@@ -453,42 +480,63 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       const int64_t si_b = K == 1 || f1 == nf ? in->n_sites : lo(f1, &dfx_fn_desc::site_off);
       const int64_t ar_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::arm_off);
       const int64_t ar_b = K == 1 || f1 == nf ? in->n_arms : lo(f1, &dfx_fn_desc::arm_off);
-      Rng rng[] = {{in->ops, d_ops, ops_a, ops_b, 4}, {in->var_flags, d_vf, vf_a, vf_b, 1},
-                   {in->stmt_span, d_span, sp_a, sp_b, 2}, {in->sites, d_sites, si_a, si_b, 1},
-                   {in->arms, d_arms, ar_a, ar_b, 2}};
-      for (auto& g : rng)
-        if (g.b > g.a)
+      // each copy runs 128 B into the next range's data, so no L1 line a
+      // range's warps read holds bytes not yet copied (the next copy writes
+      // the same bytes again)
+      Rng rng[] = {{in->ops, d_ops, ops_a, ops_b, in->n_ops, 4},
+                   {in->var_flags, d_vf, vf_a, vf_b, in->n_vars, 1},
+                   {in->stmt_span, d_span, sp_a, sp_b, in->n_stmts, 2},
+                   {in->sites, d_sites, si_a, si_b, in->n_sites, 1},
+                   {in->arms, d_arms, ar_a, ar_b, in->n_arms, 2}};
+      for (auto& g : rng) {
+        int64_t e = g.b + 32 / g.unit;
+        if (e > g.n) e = g.n;
+        if (e > g.a)
           CK(cudaMemcpyAsync((int32_t*)g.dst + g.a * g.unit, g.src + g.a * g.unit,
-                             sizeof(int32_t) * g.unit * (size_t)(g.b - g.a), cudaMemcpyHostToDevice,
+                             sizeof(int32_t) * g.unit * (size_t)(e - g.a), cudaMemcpyHostToDevice,
                              h->s_copy));
+      }
     }
     CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
     if (h->trace) CK(cudaEventRecord(h->tev[3 * k], h->s_copy));
-    const int u = k < m ? k : U - 1;
-    if (k != last_range[u]) continue;
-    cudaStream_t sk = cs[u % dfx_handle::kComp];
-    CK(cudaStreamWaitEvent(sk, h->pev[1 + k], 0));
-    if (u == 0) CK(cudaEventRecord(h->ev0, sk));
-    if (h->trace) CK(cudaEventRecord(h->tev[3 * u + 1], sk));
-    int rc = dfx::replay_launch(range_dev(u), sk);
-    if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    if (h->trace) CK(cudaEventRecord(h->tev[3 * u + 2], sk));
-    CK(cudaMemcpyAsync(h->pin_cnt + u, d_cnt + u, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sk));
-    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + u], sk));
+    cudaStream_t s_reg = s_regs[k & 1];
+    CK(cudaStreamWaitEvent(s_reg, h->pev[1 + k], 0));
+    int rc = dfx::region_launch(r, f0, f1, s_reg);
+    if (rc != DFX_OK) return fail(rc, "region_kernel launch failed");
+    CK(cudaMemcpyAsync(g_ready + k, h->pin_one + k, sizeof(int), cudaMemcpyHostToDevice, s_reg));
+    if (h->trace) CK(cudaEventRecord(h->tev[3 * k + 1], s_reg));
   }
-  for (int i = 1; i < dfx_handle::kComp; i++) {
-    CK(cudaEventRecord(h->jev[i], cs[i]));
-    CK(cudaStreamWaitEvent(st, h->jev[i], 0));
+  CK(cudaEventRecord(h->ev0, st));
+  {
+    const int rc = dfx::replay_launch(r, st, &gate);
+    if (rc != DFX_OK) {
+      for (cudaStream_t sr : s_regs) cudaStreamSynchronize(sr);   // the ranges open; the kernel drains
+      cudaStreamSynchronize(st);
+      return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
   }
   CK(cudaEventRecord(h->ev1, st));
-  // events of unit k go back as soon as unit k's replay is done
+  // range k's events go home as soon as its last item is done
+  const auto t_call = std::chrono::steady_clock::now();
+  std::vector<double> t_done(K, 0.0);
   unsigned long long count = 0, done = 0;
   std::vector<int> redo;
-  for (int k = 0; k < U; k++) {
-    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipeMax + k]));
-    const unsigned long long c = h->pin_cnt[k];
+  for (int k = 0; k < K; k++) {
+    volatile unsigned long long* hd = h->host_done + k;
+    if (range_items[k] > 0) {
+      while (*hd == 0ull) {
+        if (cudaEventQuery(h->ev1) != cudaErrorNotReady) break;   // finished (or failed)
+        std::this_thread::yield();
+      }
+      if (*hd == 0ull) {
+        CK(cudaEventSynchronize(h->ev1));
+        if (*hd == 0ull) return fail(DFX_E_CUDA, "dfx_replay_batch: range %d did not complete", k);
+      }
+    }
+    t_done[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+    const unsigned long long c = range_items[k] > 0 ? *hd - 1ull : 0ull;
     count += c;
-    if ((int64_t)c > ev_cap[k]) { redo.push_back(k); continue; }
+    if ((long long)c > ev_cap[k]) { redo.push_back(k); continue; }
     unsigned long long n = c;
     if (cap <= (int64_t)done) n = 0;
     else if ((int64_t)(done + n) > cap) n = (unsigned long long)cap - done;
@@ -497,19 +545,30 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
                          cudaMemcpyDeviceToHost, h->s_d2h));
     done += n;
   }
+  CK(cudaStreamSynchronize(st));
+  {
+    int timed_out = 0;
+    CK(cudaMemcpy(&timed_out, g_timeout, sizeof timed_out, cudaMemcpyDeviceToHost));
+    if (timed_out) return fail(DFX_E_CUDA, "dfx_replay_batch: a range never became ready");
+  }
   if (!redo.empty() && (int64_t)count <= cap) {
     for (int k : redo) {
-      const int64_t need = (int64_t)h->pin_cnt[k];
+      const int64_t need = (int64_t)(h->host_done[k] - 1ull);
       auto* d_re = (dfx_event*)dbuf(h, "events_redo", sizeof(dfx_event) * (size_t)need);
       if (!d_re) return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
-      dfx::ReplayDev rk = range_dev(k);
+      CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home
+      dfx::ReplayDev rk = r;
+      rk.item_fn = (const int32_t*)d_ifn + range_item0[k];
+      rk.item_chunk = (const int32_t*)d_ich + range_item0[k];
+      rk.n_items = range_items[k];
+      rk.fn_lo = cut[k];
+      rk.fn_hi = cut[k + 1];
       rk.events = d_re;
       rk.event_cap = need;
-      rk.event_count = d_cnt + U;
-      rk.next = d_next + U;
-      CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home
-      CK(cudaMemsetAsync(d_cnt + U, 0, sizeof(unsigned long long), st));
-      int rc = dfx::replay_launch(rk, st);
+      rk.event_count = d_cnt + K;
+      rk.next = reinterpret_cast<unsigned*>(g_next + 1);
+      CK(cudaMemsetAsync(d_cnt + K, 0, sizeof(unsigned long long), st));
+      const int rc = dfx::replay_launch(rk, st);   // tables rebuilt identically
       if (rc != DFX_OK) return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       CK(cudaStreamSynchronize(st));
       CK(cudaMemcpyAsync(out->events + done, d_re, sizeof(dfx_event) * (size_t)need,
@@ -517,27 +576,23 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       done += (unsigned long long)need;
     }
   }
-  if (in->n_vars) {
-    CK(cudaStreamWaitEvent(h->s_d2h, h->ev1, 0));
+  if (in->n_vars)
     CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost, h->s_d2h));
-  }
   CK(cudaStreamSynchronize(h->s_d2h));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   if (h->trace) {
     const cudaEvent_t t0 = h->tev[3 * dfx_handle::kPipeMax];
+    float k0 = 0.f;
+    cudaEventElapsedTime(&k0, t0, h->ev0);
+    fprintf(stderr, "dfx_replay_batch: K=%d, replay launch at %.2f ms\n", K, k0);
     for (int k = 0; k < K; k++) {
-      float a = 0.f;
+      float a = 0.f, b = 0.f;
       cudaEventElapsedTime(&a, t0, h->tev[3 * k]);
-      fprintf(stderr, "dfx_replay_batch range %2d: functions [%d, %d) h2d done %8.2f ms\n", k,
-              cut[k], cut[k + 1], a);
-    }
-    for (int u = 0; u < U; u++) {
-      float b = 0.f, c = 0.f;
-      cudaEventElapsedTime(&b, t0, h->tev[3 * u + 1]);
-      cudaEventElapsedTime(&c, t0, h->tev[3 * u + 2]);
-      fprintf(stderr, "dfx_replay_batch unit %2d: functions [%d, %d) replay %8.2f .. %8.2f ms "
-              "(%.2f)\n", u, ucut[u], ucut[u + 1], b, c, c - b);
+      cudaEventElapsedTime(&b, t0, h->tev[3 * k + 1]);
+      fprintf(stderr, "dfx_replay_batch range %2d: functions [%d, %d) h2d done %8.2f ms, open "
+              "%8.2f ms, complete %8.2f ms (host clock from launch)\n", k, cut[k], cut[k + 1],
+              a, b, t_done[k]);
     }
   }
   out->kernel_ms = ms;

@@ -26,7 +26,24 @@ struct ReplayDev {
   unsigned* next;     // work-queue counter of this launch (cleared by replay_launch)
 };
 
-int replay_launch(const ReplayDev& r, cudaStream_t stream);
+// Range gating of the host-buffer pipeline (replay.cu replay_kernel)
+struct GateDev {
+  int K;
+  const int* fn_cut;                 // [K+1] function bounds of the ranges
+  const int* ready;                  // [K]
+  const long long* ev_off;           // [K] region offsets into events
+  const long long* ev_cap;           // [K]
+  const unsigned* range_items;       // [K] items per range
+  unsigned* items_done;              // [K]
+  unsigned long long* host_done;     // [K] mapped host memory: count + 1 when done
+  unsigned* timed_out;
+};
+
+// region tables of functions [fn_lo, fn_hi) (replay.cu region_kernel)
+int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream);
+// replay (persistent grid); with `gate`, items wait for their range's ready
+// flag and the region tables are the caller's (region_launch per range)
+int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate = nullptr);
 
 }  // namespace dfx
 

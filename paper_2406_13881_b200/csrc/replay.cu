@@ -16,6 +16,7 @@
 // Outputs: order-keyed events (plans, suppressions, errors) appended with one
 // global atomic per event, and per-variable result bits.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/dfx.h"
@@ -508,10 +509,32 @@ halt_all:
   if (active) var_out[d.var_off + var] = 0;
 }
 
+// Range gating of the host-buffer pipeline (dfx_replay_batch): the programs
+// arrive in K function ranges; range k's items wait until ready[k] is set
+// (after its H2D and its region table), write their events into range k's
+// region, and the last item of range k publishes the range's event count in
+// mapped host memory, so its events go home while the launch runs on.
+
+// Bounded wait (lane 0) for *p != 0; false after ~20 s (a range whose inputs
+// never arrive must not hang the device)
+__device__ __noinline__ bool wait_set(const volatile int* p) {
+  if (*p) return true;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 64;
+  while (!*p) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) return false;
+    __nanosleep(ns);
+    if (ns < 4096) ns <<= 1;
+  }
+  return true;
+}
+
 // Persistent: each warp takes work items from `next` (one atomic per item)
 // until none are left, so no warp idles on the rest of its block and the
 // long items (first in the order) never wait for a block slot.
-template <class M>
+template <class M, bool GATED>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
@@ -519,7 +542,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
               const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
               int n_items, int slots_per_warp, dfx_event* __restrict__ events,
               int64_t event_cap, unsigned long long* __restrict__ event_count,
-              uint8_t* __restrict__ var_out, unsigned* __restrict__ next) {
+              uint8_t* __restrict__ var_out, unsigned* __restrict__ next, GateDev gate) {
   __shared__ WarpCtl<M> ctl_all[kWarpsPerBlock];
   extern __shared__ uint32_t prov_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -530,9 +553,32 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     if (lane == 0) item = (int)atomicAdd(next, 1u);
     item = __shfl_sync(0xFFFFFFFFu, item, 0);
     if (item >= n_items) return;
-    replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
-                  item_chunk, n_items, slots_per_warp, events, event_cap, event_count, var_out);
-    __syncwarp();
+    if constexpr (GATED) {
+      const int f = __ldg(item_fn + item);
+      int k = 0;
+      while (k + 1 < gate.K && f >= __ldg(gate.fn_cut + k + 1)) k++;
+      int ok = 1;
+      if (lane == 0) {
+        ok = wait_set(gate.ready + k);
+        if (!ok) atomicExch(gate.timed_out, 1u);
+      }
+      if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return;
+      replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
+                    item_chunk, n_items, slots_per_warp, events + __ldg(gate.ev_off + k),
+                    __ldg(gate.ev_cap + k), event_count + k, var_out);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0 &&
+          atomicAdd(gate.items_done + k, 1u) + 1u == __ldg(gate.range_items + k)) {
+        const unsigned long long cnt = atomicAdd(event_count + k, 0ull);
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(gate.host_done + k) = cnt + 1ull;
+      }
+    } else {
+      replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
+                    item_chunk, n_items, slots_per_warp, events, event_cap, event_count, var_out);
+      __syncwarp();
+    }
   }
 }
 
@@ -611,10 +657,17 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
   }
 }
 
-int replay_launch(const ReplayDev& r, cudaStream_t stream) {
-  if (r.fn_hi > r.fn_lo) {
-    region_kernel<<<(r.fn_hi - r.fn_lo + 31) / 32, 32, 0, stream>>>(
-        r.fns, reinterpret_cast<int4*>(const_cast<int32_t*>(r.ops)), r.fn_lo, r.fn_hi);
+int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream) {
+  if (fn_hi > fn_lo)
+    region_kernel<<<(fn_hi - fn_lo + 31) / 32, 32, 0, stream>>>(
+        r.fns, reinterpret_cast<int4*>(const_cast<int32_t*>(r.ops)), fn_lo, fn_hi);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) {
+  if (!gate && r.fn_hi > r.fn_lo) {
+    const int rc = region_launch(r, r.fn_lo, r.fn_hi, stream);
+    if (rc != DFX_OK) return rc;
   }
   int slots = r.max_slots;
   if (slots < 2) slots = 2;
@@ -633,13 +686,29 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
     int blocks = sms * (per_sm > 0 ? per_sm : 1);
+    // gated: leave room for the region kernels that open the ranges
+    if (gate) {
+      // block slots left to the region kernels that open the ranges (they
+      // run beside this launch); C4 sweep, free 16 / 48 / 96 / 148 / 296:
+      // 328 / 210 / 203 / 206 / 220 ms per host call
+      int free_blocks = sms * 2 / 3;
+      if (const char* e = getenv("DFX_GATE_FREE")) free_blocks = atoi(e);
+      blocks -= free_blocks;
+    }
     if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
     kern<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
         r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
-        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out, r.next);
+        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out, r.next,
+        gate ? *gate : GateDev{});
   };
-  if (slots <= 32) launch(replay_kernel<uint32_t>);
-  else launch(replay_kernel<uint64_t>);
+  if (slots <= 32) {
+    if (gate) launch(replay_kernel<uint32_t, true>);
+    else launch(replay_kernel<uint32_t, false>);
+  } else {
+    if (gate) launch(replay_kernel<uint64_t, true>);
+    else launch(replay_kernel<uint64_t, false>);
+  }
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 

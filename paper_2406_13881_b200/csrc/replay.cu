@@ -390,9 +390,11 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
         for (int i = 1; i < n; i++) merge_conj(arm[0], arm[i]);
         __syncwarp();
         if (lane == 0) {
-          int m = arm[0];
-          ref_inc(c, m); ref_dec(c, cur); c.cur = m;
-          for (int i = 0; i < n; i++) ref_dec(c, arm[i]);
+          // arm 0 becomes cur: its arm-stack reference turns into the cur
+          // reference (net zero), the old cur's and the other arms' drop
+          const int m = arm[0];
+          ref_dec(c, cur); c.cur = m;
+          for (int i = 1; i < n; i++) ref_dec(c, arm[i]);
           ref_dec(c, b.saved);
           c.narm = b.arm_base;
           c.nbr--;

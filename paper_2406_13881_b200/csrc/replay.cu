@@ -605,12 +605,17 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
   if (f >= fn_hi) return;
   const dfx_fn_desc d = fns[f];
   int4* o = ops + d.op_off;
+  // the open region's accumulators live in registers; the stack (local
+  // memory) holds the enclosing regions' and is touched only at BEGIN / END
   int32_t st_pc[kRegionStack + 1];
   uint32_t st_mask[kRegionStack + 1];
   int64_t st_dyn[kRegionStack + 1];
   bool st_br[kRegionStack + 1];
-  int sp = 0, deep = 0;   // deep: open regions beyond the stack (never skipped)
-  st_mask[0] = 0u; st_dyn[0] = 0; st_br[0] = false;
+  int cpc = -1;          // begin pc of the open region (-1: the function body)
+  uint32_t cmask = 0u;
+  int64_t cdyn = 0;
+  bool cbr = false;
+  int sp = 0, deep = 0;  // sp: enclosing regions stacked; deep: beyond the stack (never skipped)
   // (code, var) words of 8 ops per batch of independent loads: the stores
   // below touch only words 2-3, so one memory latency per batch, not per op
   constexpr int kBatch = 8;
@@ -629,32 +634,31 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
     const int code = op.x & 0xFF;
     if (code == DFX_OP_END) break;
     if (code >= DFX_OP_HR && code <= DFX_OP_DW) {
-      st_mask[sp] |= 1u << ((op.y >> 5) & 31);
-      st_dyn[sp]++;
+      cmask |= 1u << ((op.y >> 5) & 31);
+      cdyn++;
     } else if (code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN) {
       o[pc].z = -1;          // until its end is seen
-      if (deep || sp == kRegionStack) { deep++; st_mask[sp] = ~0u; continue; }
+      if (deep || sp == kRegionStack) { deep++; cmask = ~0u; continue; }
+      st_pc[sp] = cpc; st_mask[sp] = cmask; st_dyn[sp] = cdyn; st_br[sp] = cbr;
       sp++;
-      st_pc[sp] = pc; st_mask[sp] = 0u; st_dyn[sp] = 0; st_br[sp] = code == DFX_OP_BR_BEGIN;
+      cpc = pc; cmask = 0u; cdyn = 0; cbr = code == DFX_OP_BR_BEGIN;
     } else if (code == DFX_OP_BR_END || code == DFX_OP_LOOP_END) {
       if (deep) { deep--; continue; }
       if (sp == 0) continue; // unbalanced
-      const int b = st_pc[sp];
+      const int b = cpc;
       const bool loop = code == DFX_OP_LOOP_END;
-      const int64_t dyn = loop ? 3 + 2 * st_dyn[sp] : 2 + st_dyn[sp];
-      uint32_t mask = st_mask[sp];
-      if (dyn > 0x7FFFFFFF || loop == st_br[sp]) mask = ~0u;   // too long, or mismatched
+      const int64_t dyn = loop ? 3 + 2 * cdyn : 2 + cdyn;
+      uint32_t mask = cmask;
+      if (dyn > 0x7FFFFFFF || loop == cbr) mask = ~0u;   // too long, or mismatched
       o[b].z = (int)mask;
       o[b].w = pc - b;
-      o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (st_br[sp] ? 0x80000000u : 0u));
-      const bool br = st_br[sp];
+      o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (cbr ? 0x80000000u : 0u));
+      const bool br = cbr;
       sp--;
-      st_mask[sp] |= mask;
-      st_dyn[sp] += dyn;
-      st_br[sp] |= br;
+      cpc = st_pc[sp]; cmask = st_mask[sp] | mask; cdyn = st_dyn[sp] + dyn; cbr = st_br[sp] | br;
     } else {
-      if (code == DFX_OP_ERR) st_mask[sp] = ~0u;
-      st_dyn[sp]++;
+      if (code == DFX_OP_ERR) cmask = ~0u;
+      cdyn++;
     }
   }
 }

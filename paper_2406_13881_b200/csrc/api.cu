@@ -787,7 +787,7 @@ int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
 int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 64;
+  if (chunk_nodes <= 0) chunk_nodes = 56;   // C3 sweep 32..512 (scripts/tune_c3.py): 56 best
   cudaStream_t st = h->st();
   dfx::SolveStats s{};
   CK(cudaEventRecord(c->e0, st));
@@ -812,7 +812,7 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
 int dfx_csr_solve_async(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve_async: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 64;
+  if (chunk_nodes <= 0) chunk_nodes = 56;   // C3 sweep 32..512 (scripts/tune_c3.py): 56 best
   dfx::SolveStats s{};
   int rc = dfx::mfp_solve(c->p, c->d_cnt, c->flags, h->st(), chunk_nodes, &s, false);
   if (rc) return fail(rc, "mfp_solve failed: %s", cudaGetErrorString(cudaGetLastError()));

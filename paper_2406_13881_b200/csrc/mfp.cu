@@ -263,7 +263,7 @@ mfp_phase_kernel(CsrDev p, int q0, int chunk_nodes, int n_chunks, RoundCtl* ctl,
   // mark(r): round r flags successor chunks for round r+1, decided on round
   // r-1's change count (final: the previous launch has completed)
   auto marks = [&](int r) {
-    return r >= 2 && 8 * __ldcg(&ctl->ring[(r - 1) & 3].changed) <= 5ull * (unsigned long long)p.n_nodes;
+    return r >= 2 && 8 * __ldcg(&ctl->ring[(r - 1) & 3].changed) <= 3ull * (unsigned long long)p.n_nodes;
   };
   const bool mark = marks(round);
   const bool sparse = round >= 3 && marks(round - 1);

@@ -1,4 +1,5 @@
 // api.cu -- C ABI of libdfx.so (include/dfx.h): handles, buffers, entry points.
+#include <algorithm>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -20,7 +21,7 @@ namespace { int csr_destroy_impl(dfx_csr* c); }
 
 struct dfx_handle {
   static constexpr int kPipe = 8;      // node ranges of the pipelined CSR calls
-  static constexpr int kPipeMax = 16;  // function ranges of dfx_replay_batch
+  static constexpr int kPipeMax = 32;  // function ranges of dfx_replay_batch
   static constexpr int kComp = 3;     // compute streams of dfx_replay_batch
   cudaStream_t s_copy = nullptr, s_d2h = nullptr;
   cudaStream_t s_comp[kComp] = {};    // [0] unused: the call's own stream
@@ -336,27 +337,19 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   // flight; range k's events go home (D2H stream) as soon as its last item
   // is done, which the kernel publishes in mapped host memory.  Functions
   // are independent (SURVEY F3 / SPEC), so ranges change nothing but the
-  // order of events in the buffer.  Range sizes (by ops) ramp up and down by
-  // 1.4x: the first H2D, which nothing overlaps, is short, and so is the
-  // last range, which ends the launch.  Ranges start at functions whose ops
-  // begin on a 128-B line: no L1 line read by one range holds another
-  // range's region table before it is written.
+  // order of events in the buffer.  32 ranges of equal ops (C4 sweep: 8 /
+  // 16 / 32 / 64 ranges 216 / 191 / 188 / 198 ms; ramped sizes were no
+  // better).  Ranges start at functions whose ops begin on a 128-B line: no
+  // L1 line read by one range holds another range's region table before it
+  // is written.
   int K = ordered && nf >= 256 ? dfx_handle::kPipeMax : 1;
   std::vector<int> cut(K + 1, nf);
   cut[0] = 0;
   if (K > 1) {
-    double w[dfx_handle::kPipeMax], tot = 0.0;
-    for (int k = 0; k < K; k++) {
-      const int edge = k < K - 1 - k ? k : K - 1 - k;
-      w[k] = 1.0;
-      for (int i = 0; i < edge && i < 5; i++) w[k] *= 1.4;
-      tot += w[k];
-    }
-    double acc = 0.0;
     int f = 0;
     for (int k = 1; k < K; k++) {
-      acc += w[k - 1] / tot;
-      while (f < nf && (double)in->fns[f].op_off < acc * (double)in->n_ops) f++;
+      const double target = (double)k / K * (double)in->n_ops;
+      while (f < nf && (double)in->fns[f].op_off < target) f++;
       while (f < nf && (in->fns[f].op_off & 7) != 0) f++;   // line-aligned start
       cut[k] = f;
     }

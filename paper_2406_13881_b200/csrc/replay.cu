@@ -695,9 +695,10 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) 
     // gated: leave room for the region kernels that open the ranges
     if (gate) {
       // block slots left to the region kernels that open the ranges (they
-      // run beside this launch); C4 sweep, free 16 / 48 / 96 / 148 / 296:
-      // 328 / 210 / 203 / 206 / 220 ms per host call
-      int free_blocks = sms * 2 / 3;
+      // run beside this launch); C4 sweep with 32 ranges, free 32 / 64 / 98 /
+      // 148: 187.5 / 187.5 / 188.4 / 191.8 ms per host call (with 16 larger
+      // ranges, 16 free slots starved the region kernels: 328 ms)
+      int free_blocks = sms / 2;
       if (const char* e = getenv("DFX_GATE_FREE")) free_blocks = atoi(e);
       blocks -= free_blocks;
     }

@@ -557,8 +557,11 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
     if (item >= n_items) return;
     if constexpr (GATED) {
       const int f = __ldg(item_fn + item);
-      int k = 0;
-      while (k + 1 < gate.K && f >= __ldg(gate.fn_cut + k + 1)) k++;
+      int k = 0, hi = gate.K - 1;   // the range holding f: fn_cut[k] <= f < fn_cut[k+1]
+      while (k < hi) {
+        const int mid = (k + hi + 1) >> 1;
+        if (f >= __ldg(gate.fn_cut + mid)) k = mid; else hi = mid - 1;
+      }
       int ok = 1;
       if (lane == 0) {
         ok = wait_set(gate.ready + k);

@@ -85,8 +85,8 @@ def test_cuda_replay_matches_oracle_at_bench_shapes():
 @pytest.mark.gpu
 def test_host_buffer_call_with_uneven_event_density():
     """dfx_replay_batch gives each pipeline range an event region sized by its
-    share of the ops.  Here the first half of the functions carries all the
-    events (the second half only writes on the host), and the caller's
+    share of the ops.  Here the first 10% of the functions carry all the
+    events (the rest only write on the host), and the caller's
     capacity is the exact total, so the early ranges overflow their regions
     and are replayed again into exact-size ones: the result must not change."""
     import dataclasses
@@ -94,13 +94,13 @@ def test_host_buffer_call_with_uneven_event_density():
     from paper_2406_13881_b200.dataflow import ReplaySession
     b, _ = c4_generate(C4Config(), np.arange(400))
     ops = b.ops.copy()
-    start = int(b.fns[200]["op_off"])
+    start = int(b.fns[40]["op_off"])    # events only in the first 10% of the functions
     code = ops[start:, 0] & 0xFF
     acc = (code >= 1) & (code <= 4)
     ops[start:, 0][acc] = (ops[start:, 0][acc] & ~0xFF) | 2        # every access -> HW
     b2 = dataclasses.replace(b, ops=ops)
     exp = run_replay(b2, runner=_oracle.replay_runner_mt)
-    assert not (exp.events["fn"] >= 200).any() and exp.events.shape[0] > 100_000
+    assert not (exp.events["fn"] >= 40).any() and exp.events.shape[0] > 10_000
     got = ReplaySession(event_cap=int(exp.events.shape[0])).run(b2)
     _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
     small = ReplaySession(event_cap=1000)                          # NOSPC -> regrow

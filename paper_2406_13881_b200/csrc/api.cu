@@ -547,6 +547,9 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if (!redo.empty() && (int64_t)count <= cap) {
     for (int k : redo) {
       const int64_t need = (int64_t)(h->host_done[k] - 1ull);
+      if (h->trace)
+        fprintf(stderr, "dfx_replay_batch range %d: %lld events overflow its region of %lld; "
+                "replayed into an exact-size one\n", k, (long long)need, (long long)ev_cap[k]);
       auto* d_re = (dfx_event*)dbuf(h, "events_redo", sizeof(dfx_event) * (size_t)need);
       if (!d_re) return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
       CK(cudaStreamSynchronize(h->s_d2h));   // the previous redo's events are home

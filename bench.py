@@ -11,6 +11,14 @@ variables [4096 r, 4096 (r+1)) of the same graph; no collective touches the
 data path (variables are independent); timing is the max over
 ranks.
 
+The same line carries a `c4` record: configuration C4 (100k independent
+functions through the E1 replay kernel, LPT-sharded over the ranks, strong
+scaling) with its own value, e2e, per-rank ms, roofline, a parity check and
+the reference's own CPU baseline (dartomp analyze_function in a process
+pool over a 1,000-function sample of the C4 source batch).
+After the timed region the C3 outputs are checked against the CPU oracle on
+every variable word (`parity`).
+
 Contract: python bench.py --gpus N --steps K --warmup W  (torchrun for N>1)
 prints ONE JSON line on rank 0.  `--impl reference` times the reference path
 on the host cores instead: the reference package cannot ingest a CSR graph
@@ -51,6 +59,12 @@ def parse_args():
                     help="c3: 1M-node x 4096-var CSR fixpoint (default, the roofline "
                          "config); c4: 100k-function E1 batch, LPT-sharded")
     ap.add_argument("--c4-funcs", type=int, default=100_000)
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the C4 sub-record of the default (c3) run")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-run parity check of the timed outputs")
+    ap.add_argument("--c4-ref-funcs", type=int, default=1000,
+                    help="functions in the reference C4 CPU-baseline sample")
     return ap.parse_args()
 
 
@@ -187,6 +201,17 @@ def run_reference(args, rank, world):
             "config": workload_config(args, 1), "impl": "reference", "cpu_baseline": base,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    base.update(host_info())
+    if not args.no_c4:
+        # C4 (the batched-function workload): the reference package itself,
+        # analyze_function in a process pool over a fixed sample
+        sys.path.insert(0, str(ROOT / "tests"))
+        import _c4src  # noqa: E402
+        cb = _c4src.reference_c4_baseline(n_funcs=args.c4_ref_funcs)
+        line["c4"] = {"metric": METRIC, "value": cb["value"], "unit": UNIT,
+                      "impl": "reference", "cpu_baseline": cb,
+                      "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -361,12 +386,48 @@ def run_ours(args, rank, world, local):
                    "h2d_bytes_per_step": int(h2d_planes), "d2h_bytes_per_step": int(d2h_planes),
                    "path": "dfx_mfp_csr: H2D dense R/W bitplanes, D2H compacted mask rows"}}
 
+    # parity of what was timed (outside the timed region; checker only): the
+    # solve's OUT_H / OUT_D planes, kernel (b)'s requirement planes and the
+    # e2e call's per-node requirement lists == the CPU oracle on ALL variable
+    # words of this rank's slab, block by block
+    parity = None
+    if not args.no_parity:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import _oracle  # noqa: E402  (checker)
+        t0 = time.perf_counter()
+        OH, OD, _ = prob.download(True, True)
+        rq, rf = rows.to_planes()
+        bad = _oracle.c3_verify(cfg.seed, cfg.n_nodes, cfg.w0, cfg.words, cfg.n_scalar,
+                                OH, OD, rq, rf)
+        if e2e is not None:
+            lq, lf = out.to_planes()
+            bad["e2e_lists"] = int(np.count_nonzero(lq != rq) + np.count_nonzero(lf != rf))
+        ok = all(v == 0 for v in bad.values())
+        parity = {"status": "ok" if ok else "MISMATCH", "differing_words": bad,
+                  "checked": "all %d variable words x %d nodes of this rank's slab vs "
+                             "oracle/mfp_oracle.c (block-wise), plus the e2e lists"
+                             % (cfg.words, cfg.n_nodes),
+                  "check_s": time.perf_counter() - t0}
+        del OH, OD, rq, rf
+        pt = torch.tensor([0.0 if ok else 1.0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        if float(pt.item()) != 0.0:
+            parity["status"] = "MISMATCH"
+    del rows
+    if e2e is not None:
+        del out, asess
+    prob.close()
+    c4 = None
+    if not args.no_c4:
+        c4 = run_c4(args, rank, world, local, sub=True)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (counter-hash generator, DESIGN.md §C3)",
+            "parity": parity,
             "config": workload_config(args, world),
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -391,20 +452,40 @@ def run_ours(args, rank, world, local):
                              "output_bytes": int(rows.nbytes)}}
     if world == 1 and not args.no_cpu_baseline:
         base, _ = cpu_sample(args, steps=1)
+        base.update(host_info())
         line["cpu_baseline"] = base
+    if c4 is not None:
+        line["c4"] = c4
     print(json.dumps(line), flush=True)
 
 
-def run_c4(args, rank, world, local):
+def host_info() -> dict:
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _c4src  # noqa: E402
+    return _c4src.host_info()
+
+
+def c4_issue_profile():
+    """Warp instructions per replay launch of the C4 batch, from the ncu
+    capture committed under profiles/ (sm__inst_executed.sum)."""
+    p = ROOT / "profiles" / "c4_issue.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return None
+
+
+def run_c4(args, rank, world, local, sub=False):
     """Configuration C4: 100k independent functions through the E1 replay
-    kernel, LPT-sharded over the ranks (strong scaling: total work fixed)."""
+    kernel, LPT-sharded over the ranks (strong scaling: total work fixed).
+    sub=True: returns the record (the `c4` object of the default run's line)
+    instead of printing a line."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2406_13881_b200 import _abi
     from paper_2406_13881_b200.batch import (C4Config, ReplayBatch, c4_cost, c4_generate,
-                                             c4_shapes, lpt_shards)
+                                             c4_shapes, lpt_shards, program_visits)
     from paper_2406_13881_b200.dataflow import ReplaySession, run_replay
 
     torch.cuda.set_device(local)
@@ -417,6 +498,7 @@ def run_c4(args, rank, world, local):
     N, V = c4_shapes(cfg)
     shards = lpt_shards(c4_cost(N, V), world)
     mine = shards[rank]
+
     def pinned(shape, dtype):
         n = int(np.prod(shape)) * np.dtype(dtype).itemsize
         buf = torch.empty(max(1, n), dtype=torch.uint8, pin_memory=True)
@@ -424,6 +506,11 @@ def run_c4(args, rank, world, local):
 
     batch, facts_mine = c4_generate(cfg, mine, alloc=pinned)
     facts_total = int((N.astype(np.int64) * V).sum())
+    # fact-visits (SURVEY §8 d, E1): dynamic node visits x V_f, node visits
+    # scaled from the program's dynamic/static op ratio (loops run twice)
+    visits = program_visits(batch)
+    n_ops = batch.fns["n_ops"].astype(np.float64)
+    fact_visits_mine = float((visits / np.maximum(n_ops, 1) * N[mine] * V[mine]).sum())
     rb = ReplayBatch(batch, eng=eng)
     for _ in range(max(3, args.warmup)):
         rb.run()
@@ -432,6 +519,20 @@ def run_c4(args, rank, world, local):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world == 1:
+            return [x]
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
 
     barrier()
     kernel_ms = 0.0
@@ -445,11 +546,13 @@ def run_c4(args, rank, world, local):
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    t = torch.tensor([ev0.elapsed_time(ev1) / args.steps], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item())
+    my_ms = ev0.elapsed_time(ev1) / args.steps
+    per_rank_ms = all_ranks(my_ms)
+    ms_per_step = max(per_rank_ms)
     value = facts_total / (ms_per_step / 1e3)
+    kernel_ms_step = kernel_ms / args.steps
+    fv_total = sum(all_ranks(fact_visits_mine))
+    rb.close()
     # e2e: the host-buffer C-ABI call (dfx_replay_batch: H2D, kernel, D2H)
     e2e = None
     if args.e2e_steps > 0:
@@ -466,51 +569,87 @@ def run_c4(args, rank, world, local):
             d2h += raw.events.nbytes + raw.var_out.nbytes
         e1.record(stream)
         torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        et = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
         h2d = sum(a.nbytes for a in (batch.fns, batch.ops, batch.var_flags, batch.stmt_span,
                                      batch.sites, batch.arms))
-        e2e = {"value": facts_total / (float(et.item()) / 1e3), "unit": UNIT,
-               "ms_per_step": float(et.item()), "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": facts_total / (et / 1e3), "unit": UNIT,
+               "ms_per_step": et, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h // args.e2e_steps),
-               "path": "dfx_replay_batch (pinned host buffers): H2D programs in 16 function "
+               "path": "dfx_replay_batch (pinned host buffers): H2D programs in 32 function "
                        "ranges (copy stream), region tables per range (2 streams), one persistent "
                        "E1 launch whose items wait for their range, D2H events per range as it "
                        "completes (D2H stream)"}
-    if rank != 0:
-        return
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic (dfx_gen_c4 structured-program generator)",
-            "config": {"workload": "C4: batch of %d independent functions, 64-2048 nodes, "
-                                   "32-512 vars, LPT-sharded" % cfg.n_funcs,
-                       "functions": cfg.n_funcs, "facts_total": facts_total,
-                       "parallelism": "function-sharded (LPT), %d GPU(s)" % world,
-                       "l2": "programs %.1f GB > 126 MB L2" % (batch.ops.nbytes / 1e9)},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 2 * args.steps,
-            "replay": {"kernel": "replay_kernel", "launches_per_step": ["region_kernel",
-                                                                       "replay_kernel"], "kernel_ms_per_step": kernel_ms / args.steps,
-                       "events": n_ev, "functions_rank0": int(len(mine)),
-                       "ops_rank0": int(batch.ops.shape[0])}}
-    if world == 1 and not args.no_cpu_baseline:
+        del sess, raw
+    # parity of the engine on this batch: a fixed sample of the same
+    # functions through the host-buffer call == the CPU oracle (checker)
+    parity = None
+    if not args.no_parity and rank == 0:
         sys.path.insert(0, str(ROOT / "tests"))
-        import _oracle  # noqa: E402  (cpu_baseline leg)
-        # all host threads over a fixed sample of 2,000 functions (every 50th)
-        n_s = min(2000, cfg.n_funcs)
-        sample = np.arange(0, cfg.n_funcs, max(1, cfg.n_funcs // n_s), dtype=np.int32)[:n_s]
-        sb, sfacts = c4_generate(cfg, sample)
-        t0 = time.perf_counter()
-        run_replay(sb, runner=_oracle.replay_runner_mt)
-        dt = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": sfacts / dt, "unit": UNIT, "cores": _oracle.num_threads(),
-                                "kind": "port",
-                                "sample": "oracle/replay_oracle.c (OpenMP over functions) on %d "
-                                          "functions of the same batch (every %d-th)"
-                                          % (len(sample), cfg.n_funcs // n_s),
-                                "seconds_per_sample": dt}
-    print(json.dumps(line), flush=True)
+        import _golden  # noqa: E402
+        import _oracle  # noqa: E402  (checker)
+        samp = mine[:: max(1, len(mine) // 1000)][:1000]
+        sb, _ = c4_generate(cfg, samp)
+        exp = run_replay(sb, runner=_oracle.replay_runner_mt)
+        got = run_replay(sb)
+        try:
+            _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+            st = "ok"
+        except AssertionError as e:
+            st = "MISMATCH: %s" % str(e)[:200]
+        parity = {"status": st, "checked": "%d functions of this batch (every %d-th of rank 0's "
+                                           "shard): events + per-variable bits == "
+                                           "oracle/replay_oracle.c" % (len(samp), max(1, len(mine) // 1000))}
+    peak, peak_src = measured_peak()
+    alg_bytes = 1.125 * fv_total
+    prof = c4_issue_profile()
+    issue = None
+    if prof is not None and world == 1 and prof.get("n_funcs") == cfg.n_funcs:
+        clock = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+        peak_issue = 148 * 4 * clock               # warp instructions / s (4 schedulers / SM)
+        inst = float(prof["inst_per_launch"])
+        issue = {"achieved_warp_inst_per_s": inst / (kernel_ms_step / 1e3),
+                 "peak_warp_inst_per_s": peak_issue,
+                 "frac": inst / (kernel_ms_step / 1e3) / peak_issue,
+                 "inst_per_launch": inst, "source": prof.get("source")}
+    rec = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "ms_per_step": ms_per_step, "per_rank_ms": per_rank_ms,
+           "higher_is_better": True, "scaling": "strong",
+           "config": {"workload": "C4: batch of %d independent functions, 64-2048 nodes, "
+                                  "32-512 vars, LPT-sharded" % cfg.n_funcs,
+                      "functions": cfg.n_funcs, "facts_total": facts_total,
+                      "parallelism": "function-sharded (LPT), %d GPU(s)" % world,
+                      "l2": "programs %.1f GB > 126 MB L2" % (batch.ops.nbytes / 1e9)},
+           "data": "synthetic (dfx_gen_c4 structured-program generator; C source form: "
+                   "gen/c4src.py, pinned to the reference by tests/test_c4_source.py)",
+           "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 2 * args.steps,
+           "parity": parity,
+           "roofline": {"bound": "issue", "kernel": "replay_kernel (E1)",
+                        "hbm_equivalent": {"achieved": alg_bytes / (kernel_ms_step / 1e3) / 1e9,
+                                           "peak": peak, "unit": "GB/s",
+                                           "frac": alg_bytes / (kernel_ms_step / 1e3) / 1e9 / peak,
+                                           "algorithmic_bytes_per_step": alg_bytes,
+                                           "fact_visits_per_step": fv_total,
+                                           "bytes_per_fact_visit": 1.125,
+                                           "peak_source": peak_src},
+                        "issue": issue},
+           "replay": {"kernel": "replay_kernel", "launches_per_step": ["region_kernel",
+                                                                      "replay_kernel"],
+                      "kernel_ms_per_step": kernel_ms_step,
+                      "events": n_ev, "functions_rank0": int(len(mine)),
+                      "ops_rank0": int(batch.ops.shape[0]),
+                      "dynamic_over_static_ops": float(visits.sum() / max(1.0, n_ops.sum()))}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import _c4src  # noqa: E402  (cpu_baseline leg: the reference itself)
+        rec["cpu_baseline"] = _c4src.reference_c4_baseline(n_funcs=args.c4_ref_funcs)
+        rec["cpu_baseline"]["extrapolated_full_batch_s"] = facts_total / rec["cpu_baseline"]["value"]
+    if sub:
+        return rec if rank == 0 else None
+    if rank != 0:
+        return None
+    rec.update({"warmup": args.warmup, "vs_baseline": None, "dtype": "u32"})
+    print(json.dumps(rec), flush=True)
+    return None
 
 
 def main():

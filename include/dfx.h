@@ -164,6 +164,10 @@ int dfx_gen_c4(uint64_t seed, const int32_t *fids, int32_t n, int32_t n_min, int
                const int32_t *var_choices, int32_t n_choices, dfx_fn_desc *fns, int32_t *ops,
                int32_t *var_flags, int32_t *stmt_span, int32_t *sites, int32_t *arms,
                int64_t *sizes, int64_t *facts_out);
+/* Dynamic op visits per function (loops: dry + planning round; branches
+ * once): the final value of E1's visit counter, for roofline accounting. */
+int dfx_program_visits(const dfx_fn_desc *fns, int32_t n_funcs, const int32_t *ops,
+                       int64_t *visits);
 
 /* ------------------------------------------------------------------------ */
 /* Kernels (a)+(b): CSR fixpoint and transfer requirements (north star)      */

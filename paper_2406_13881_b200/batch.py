@@ -94,6 +94,20 @@ def c4_generate(cfg: C4Config, fids: np.ndarray, alloc=np.zeros) -> tuple[Packed
                        arms=arms[:2 * n_arms]), int(facts.value)
 
 
+def program_visits(batch: PackedBatch) -> np.ndarray:
+    """Dynamic op visits of every function (`dfx_program_visits`): ops the
+    reference schedule executes, loops twice (dataflow.py:566-590)."""
+    lib = _lib()
+    out = np.zeros(batch.fns.shape[0], dtype=np.int64)
+    fns = np.ascontiguousarray(batch.fns)
+    ops = np.ascontiguousarray(batch.ops)
+    rc = lib.dfx_program_visits(C.c_void_p(fns.ctypes.data), C.c_int32(fns.shape[0]),
+                                C.c_void_p(ops.ctypes.data), C.c_void_p(out.ctypes.data))
+    if rc != 0:
+        raise _abi.EngineError("dfx_program_visits failed (%d)" % rc)
+    return out
+
+
 class ReplayBatch:
     """A packed batch resident in HBM (`dfx_replay_create`)."""
 

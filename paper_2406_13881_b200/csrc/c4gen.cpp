@@ -306,3 +306,44 @@ int dfx_gen_c4(uint64_t seed, const int32_t* fids, int32_t n, int32_t n_min, int
 }
 
 }  // extern "C"
+
+// Dynamic op visits of each function's replay program: the number of ops the
+// reference schedule executes (`_Analyzer` visit order), i.e. the final value
+// of E1's visit counter -- loops run their body twice (dry round + planning
+// round, dataflow.py:566-590: 3 + 2 x content), branches once (2 + content).
+// Host-side accounting for the C4 roofline (algorithmic bytes per fact-visit).
+extern "C" int dfx_program_visits(const dfx_fn_desc* fns, int32_t n, const int32_t* ops,
+                                  int64_t* visits) {
+  if (!fns || !ops || !visits || n < 0) return DFX_E_ARG;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 32) nt = 32;
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; t++)
+    th.emplace_back([&, t] {
+      std::vector<int64_t> stk;
+      std::vector<char> is_loop;
+      for (int32_t f = (int32_t)t; f < n; f += (int32_t)nt) {
+        const int32_t* o = ops + 4 * fns[f].op_off;
+        int64_t cur = 0;
+        stk.clear(); is_loop.clear();
+        for (int32_t pc = 0; pc < fns[f].n_ops; pc++) {
+          const int code = o[4 * pc] & 0xFF;
+          if (code == DFX_OP_END) break;
+          if (code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN) {
+            stk.push_back(cur); is_loop.push_back(code == DFX_OP_LOOP_BEGIN);
+            cur = 0;
+          } else if ((code == DFX_OP_BR_END || code == DFX_OP_LOOP_END) && !stk.empty()) {
+            const int64_t dyn = is_loop.back() ? 3 + 2 * cur : 2 + cur;
+            cur = stk.back() + dyn;
+            stk.pop_back(); is_loop.pop_back();
+          } else {
+            cur++;
+          }
+        }
+        visits[f] = cur;
+      }
+    });
+  for (auto& x : th) x.join();
+  return DFX_OK;
+}

@@ -105,3 +105,26 @@ def num_threads() -> int:
 
 def summaries_runner(cin, cout) -> int:
     return lib().oracle_summaries(C.byref(cin), C.byref(cout))
+
+
+def c3_verify(seed: int, n_nodes: int, w0: int, words: int, n_scalar: int, OH, OD,
+              REQ=None, FP=None, block: int = 32) -> dict:
+    """Exact check of full-size solve outputs (OUT_H/OUT_D planes, and the
+    requirement / firstprivate planes when given) against the oracle, one
+    block of `block` variable words at a time (variables are independent, so
+    each block is an exact sub-problem; memory stays O(n_nodes x block)).
+    Returns the number of differing words per output."""
+    bad = {"OUT_H": 0, "OUT_D": 0}
+    if REQ is not None:
+        bad.update(REQ=0, FP=0)
+    for b0 in range(0, words, block):
+        nb = min(block, words - b0)
+        g = c3_generate(seed, n_nodes, w0 + b0, nb, n_scalar)
+        eh, ed, _ = c3_solve(g)
+        bad["OUT_H"] += int(np.count_nonzero(OH[:, b0:b0 + nb] != eh))
+        bad["OUT_D"] += int(np.count_nonzero(OD[:, b0:b0 + nb] != ed))
+        if REQ is not None:
+            rq, fp = c3_requirements(g, eh, ed)
+            bad["REQ"] += int(np.count_nonzero(REQ[:, b0:b0 + nb] != rq))
+            bad["FP"] += int(np.count_nonzero(FP[:, b0:b0 + nb] != fp))
+    return bad

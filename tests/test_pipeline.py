@@ -55,13 +55,15 @@ def test_install_patches_reference_cli(tmp_path, capsys):
     assert rc == rc_ref and capsys.readouterr().out == ref_out
 
 
-CORPUS = pathlib.Path("/root/reference/pkg/tests/corpus")
+# the reference's own 27-file corpus (pkg/tests/corpus), committed as test
+# inputs so the GPU box (which has no /root/reference) runs it too
+CORPUS = pathlib.Path(__file__).parent / "golden" / "corpus"
 
 
-@pytest.mark.skipif(not CORPUS.exists(), reason="reference corpus not present (GPU box)")
-def test_corpus_matches_golden_report_and_text_cpu_oracle():
+def _corpus_check(runners):
     """Every corpus file through the drop-in pipeline reproduces the golden
-    `report` lines and the sha256 of the `transform` output."""
+    `report` lines (or error text) and the sha256 of the `transform` output
+    that the reference produced (tests/golden/make_golden.py)."""
     import hashlib
     import _golden
     from dartomp.report import plan_lines
@@ -71,9 +73,9 @@ def test_corpus_matches_golden_report_and_text_cpu_oracle():
     for p in sorted(CORPUS.glob("*/*.c")):
         key = "corpus/%s/%s" % (p.parent.name, p.name)
         exp = gold[key]
-        a = load(path=key, text=p.read_text(), summary_runner=_oracle.summaries_runner)
+        a = load(path=key, text=p.read_text(), summary_runner=runners.get("summary_runner"))
         try:
-            result, plans = transform(a, replay_runner=_oracle.replay_runner)
+            result, plans = transform(a, replay_runner=runners.get("replay_runner"))
         except Exception as e:
             got = ["<%s: %s>" % (type(e).__name__, e.render())]
             assert got == exp["report"], key
@@ -87,6 +89,17 @@ def test_corpus_matches_golden_report_and_text_cpu_oracle():
         assert lines == exp["report"], key
         n += 1
     assert n == 27
+
+
+def test_corpus_matches_golden_report_and_text_cpu_oracle():
+    _corpus_check(CPU)
+
+
+@pytest.mark.gpu
+def test_corpus_matches_golden_report_and_text_cuda():
+    """The same 27 files end to end through the CUDA engine (kernels E1 and
+    (c)): byte-identical `transform` text and identical report lines."""
+    _corpus_check({})
 
 
 @pytest.mark.parametrize("seed", range(4))

@@ -414,6 +414,9 @@ def run_ours(args, rank, world, local):
             dist.all_reduce(pt, op=dist.ReduceOp.MAX)
         if float(pt.item()) != 0.0:
             parity["status"] = "MISMATCH"
+    req_rec = {"kernel": "requirements_kernel + compact_kernel",
+               "ms": req_ms, "nonzero_masks": int(rows.masks.shape[0]),
+               "output_bytes": int(rows.nbytes)}
     del rows
     if e2e is not None:
         del out, asess
@@ -447,9 +450,7 @@ def run_ours(args, rank, world, local):
                       "rows_read": stats_last["rows_read"],
                       "rows_written": stats_last["rows_written"],
                       "device_ms_incl_round_checks": ms_per_step},
-            "requirements": {"kernel": "requirements_kernel + compact_kernel",
-                             "ms": req_ms, "nonzero_masks": int(rows.masks.shape[0]),
-                             "output_bytes": int(rows.nbytes)}}
+            "requirements": req_rec}
     if world == 1 and not args.no_cpu_baseline:
         base, _ = cpu_sample(args, steps=1)
         base.update(host_info())

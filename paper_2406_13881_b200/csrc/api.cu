@@ -169,6 +169,7 @@ struct dfx_replay {
   dfx::ReplayDev r{};
   int64_t n_vars = 0;
   int32_t n_funcs = 0;
+  std::vector<dfx_event> host_events;   // functions beyond the wide limits (fn_class 2)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   ~dfx_replay() {
     for (void* p : allocs) cudaFree(p);
@@ -184,7 +185,7 @@ namespace {
 // the long warps start in the first waves and a launch does not end on a
 // tail of them; chunks of one function stay adjacent (similar cost in a block).
 void append_items(const dfx_fn_desc* fns, int f0, int f1, std::vector<int32_t>& item_fn,
-                  std::vector<int32_t>& item_chunk) {
+                  std::vector<int32_t>& item_chunk, const std::vector<uint8_t>& cls, int want) {
   constexpr int kBins = 4096;
   auto bin = [&](int f) {
     const int b = fns[f].n_ops >> 4;
@@ -195,6 +196,7 @@ void append_items(const dfx_fn_desc* fns, int f0, int f1, std::vector<int32_t>& 
   for (int b = 0; b < kBins; b++) start[b + 1] += start[b];
   for (int f = f0; f < f1; f++) order[start[bin(f)]++] = f;
   for (int f : order) {
+    if (cls[f] != want) continue;
     int chunks = (fns[f].n_vars + 31) / 32;
     if (chunks == 0) chunks = 1;
     for (int c = 0; c < chunks; c++) {
@@ -203,7 +205,45 @@ void append_items(const dfx_fn_desc* fns, int f0, int f1, std::vector<int32_t>& 
     }
   }
 }
+// A function beyond the wide replay's limits gets one engine-error event
+// (visit key 0): the host raises for that function only.
+dfx_event engine_error_event(int f) {
+  dfx_event e{};
+  e.key = 0; e.fn = f; e.var = -1; e.node = 0;
+  e.kind = (uint8_t)DFX_EV_ERR_ENGINE; e.pos = 0; e.pad = 0;
+  return e;
+}
+
+// Classify every function (dfx::fn_class) and fold the per-class slot maxima.
+void classify(const dfx_replay_in* in, std::vector<uint8_t>& cls, int& max_slots,
+              int& wide_slots, std::vector<dfx_event>& host_events) {
+  const int nf = in->n_funcs;
+  cls.assign((size_t)nf, 0);
+  max_slots = wide_slots = 2;
+  for (int f = 0; f < nf; f++) {
+    const dfx_fn_desc& d = in->fns[f];
+    cls[f] = (uint8_t)dfx::fn_class(d);
+    if (cls[f] == 0 && d.n_slots > max_slots) max_slots = d.n_slots;
+    if (cls[f] == 1 && d.n_slots > wide_slots) wide_slots = d.n_slots;
+    if (cls[f] == 2) host_events.push_back(engine_error_event(f));
+  }
+}
 }  // namespace
+
+namespace dfx {
+// Narrow replay limits (replay.cu Narrow): 64 slots, loop depth 24, branch
+// depth 48, 192 open arms, statement ids < 0xFFFF (16-bit provenance).  Wide:
+// 256 / 64 / 256 / 1024, ids < 2^20 - 1 (the hoist table's node field).
+int fn_class(const dfx_fn_desc& d) {
+  if (d.n_slots <= 64 && d.max_loop_depth <= 24 && d.max_br_depth <= 48 && d.max_arms <= 192 &&
+      d.n_stmts < 0xFFFF)
+    return 0;
+  if (d.n_slots <= 256 && d.max_loop_depth <= 64 && d.max_br_depth <= 256 && d.max_arms <= 1024 &&
+      d.n_stmts < DFX_AC_NODE_MASK)
+    return 1;
+  return 2;
+}
+}  // namespace dfx
 
 extern "C" {
 
@@ -211,18 +251,15 @@ int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap,
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_replay_create: null argument");
   CK(cudaSetDevice(h->device));
   const int nf = in->n_funcs;
-  std::vector<int32_t> item_fn, item_chunk;
-  int max_slots = 2;
-  for (int f = 0; f < nf; f++) {
-    const dfx_fn_desc& d = in->fns[f];
-    if (d.n_slots > 64 || d.max_loop_depth > 24 || d.max_br_depth > 48 || d.max_arms > 192)
-      return fail(DFX_E_LIMIT, "function %d exceeds replay limits (slots %d, loops %d, "
-                  "branches %d, arms %d)", f, d.n_slots, d.max_loop_depth, d.max_br_depth,
-                  d.max_arms);
-    if (d.n_slots > max_slots) max_slots = d.n_slots;
-  }
-  append_items(in->fns, 0, nf, item_fn, item_chunk);
+  std::vector<int32_t> item_fn, item_chunk, wide_fn, wide_chunk;
+  std::vector<uint8_t> cls;
+  std::vector<dfx_event> host_events;
+  int max_slots = 2, wide_slots = 2;
+  classify(in, cls, max_slots, wide_slots, host_events);
+  append_items(in->fns, 0, nf, item_fn, item_chunk, cls, 0);
+  append_items(in->fns, 0, nf, wide_fn, wide_chunk, cls, 1);
   auto* rp = new dfx_replay();
+  rp->host_events = std::move(host_events);
   cudaStream_t st = h->st();
   auto up = [&](const void* src, size_t bytes) -> void* {
     void* p = nullptr;
@@ -249,9 +286,14 @@ int dfx_replay_create(dfx_handle* h, const dfx_replay_in* in, int64_t event_cap,
   r.event_count = (unsigned long long*)up(nullptr, sizeof(unsigned long long));
   r.var_out = (uint8_t*)up(nullptr, (size_t)in->n_vars + 1);
   r.next = (unsigned*)up(nullptr, sizeof(unsigned));
+  r.wide_item_fn = (const int32_t*)up(wide_fn.data(), sizeof(int32_t) * wide_fn.size());
+  r.wide_item_chunk = (const int32_t*)up(wide_chunk.data(), sizeof(int32_t) * wide_chunk.size());
+  r.n_wide_items = (int)wide_fn.size();
+  r.wide_max_slots = wide_slots;
+  r.wide_next = (unsigned*)up(nullptr, sizeof(unsigned));
   for (void* p : rp->allocs)
     if (!p) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
-  if (rp->allocs.size() != 12) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
+  if (rp->allocs.size() != 15) { delete rp; return fail(DFX_E_CUDA, "dfx_replay_create: allocation failed"); }
   rp->n_vars = in->n_vars;
   rp->n_funcs = nf;
   CK(cudaEventCreate(&rp->e0));
@@ -275,7 +317,7 @@ int dfx_replay_run(dfx_handle* h, dfx_replay* rp, int64_t* n_events, float* kern
   CK(cudaStreamSynchronize(st));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, rp->e0, rp->e1));
-  if (n_events) *n_events = (int64_t)count;
+  if (n_events) *n_events = (int64_t)count + (int64_t)rp->host_events.size();
   if (kernel_ms) *kernel_ms = ms;
   if ((int64_t)count > rp->r.event_cap)
     return fail(DFX_E_NOSPC, "event capacity %lld < %llu", (long long)rp->r.event_cap, count);
@@ -294,8 +336,11 @@ int dfx_replay_fetch(dfx_handle* h, dfx_replay* rp, dfx_replay_out* out) {
   if (n) CK(cudaMemcpyAsync(out->events, rp->r.events, sizeof(dfx_event) * (size_t)n, cudaMemcpyDeviceToHost, st));
   if (rp->n_vars) CK(cudaMemcpyAsync(out->var_out, rp->r.var_out, (size_t)rp->n_vars, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  out->n_events = (int64_t)count;
-  return (int64_t)count > out->event_cap ? DFX_E_NOSPC : DFX_OK;
+  const int64_t total = (int64_t)count + (int64_t)rp->host_events.size();
+  for (size_t i = 0; i < rp->host_events.size(); i++)
+    if (n + (int64_t)i < out->event_cap) out->events[n + i] = rp->host_events[i];
+  out->n_events = total;
+  return total > out->event_cap ? DFX_E_NOSPC : DFX_OK;
 }
 
 int dfx_replay_destroy(dfx_handle* h, dfx_replay* rp) {
@@ -312,16 +357,14 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_replay_batch: null argument");
   CK(cudaSetDevice(h->device));
   const int nf = in->n_funcs;
-  std::vector<int32_t> item_fn, item_chunk;
-  int max_slots = 2;
+  std::vector<int32_t> item_fn, item_chunk, wide_fn, wide_chunk;
+  std::vector<uint8_t> cls;
+  std::vector<dfx_event> host_events;
+  int max_slots = 2, wide_slots = 2;
+  classify(in, cls, max_slots, wide_slots, host_events);
   bool ordered = true;   // per-function array ranges ascending and contiguous
   for (int f = 0; f < nf; f++) {
     const dfx_fn_desc& d = in->fns[f];
-    if (d.n_slots > 64 || d.max_loop_depth > 24 || d.max_br_depth > 48 || d.max_arms > 192)
-      return fail(DFX_E_LIMIT, "function %d exceeds replay limits (slots %d, loops %d, "
-                  "branches %d, arms %d)", f, d.n_slots, d.max_loop_depth, d.max_br_depth,
-                  d.max_arms);
-    if (d.n_slots > max_slots) max_slots = d.n_slots;
     if (f > 0) {
       const dfx_fn_desc& e = in->fns[f - 1];
       ordered &= d.op_off >= e.op_off + e.n_ops && d.var_off >= e.var_off + e.n_vars &&
@@ -358,11 +401,14 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   if (K == 1) { cut.assign(2, nf); cut[0] = 0; }
   std::vector<int32_t> range_item0(K + 1, 0), range_items(K, 0);
   for (int k = 0; k < K; k++) {
-    append_items(in->fns, cut[k], cut[k + 1], item_fn, item_chunk);
+    append_items(in->fns, cut[k], cut[k + 1], item_fn, item_chunk, cls, 0);
     range_item0[k + 1] = (int32_t)item_fn.size();
     range_items[k] = range_item0[k + 1] - range_item0[k];
   }
   const size_t n_items = item_fn.size();
+  // functions beyond the narrow limits: one wide launch after the gated one
+  append_items(in->fns, 0, nf, wide_fn, wide_chunk, cls, 1);
+  const size_t n_wide = wide_fn.size();
   cudaStream_t st = h->st();
   void* d_fns = dbuf(h, "fns", sizeof(dfx_fn_desc) * (size_t)nf + 16);
   void* d_ops = dbuf(h, "ops", sizeof(int32_t) * 4 * (size_t)in->n_ops + 16);
@@ -372,6 +418,8 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   void* d_arms = dbuf(h, "arms", sizeof(int32_t) * 2 * (size_t)in->n_arms + 16);
   void* d_ifn = dbuf(h, "ifn", sizeof(int32_t) * n_items + 16);
   void* d_ich = dbuf(h, "ich", sizeof(int32_t) * n_items + 16);
+  void* d_iwf = dbuf(h, "iwf", sizeof(int32_t) * n_wide + 16);
+  void* d_iwc = dbuf(h, "iwc", sizeof(int32_t) * n_wide + 16);
   const int64_t cap = out->event_cap;
   // per-range event regions, sized from the caller's capacity by ops share;
   // a range that overflows its region is replayed again into an exact-size
@@ -387,21 +435,21 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     ev_off[k + 1] = ev_off[k] + ev_cap[k];
   }
   auto* d_ev = (dfx_event*)dbuf(h, "events", sizeof(dfx_event) * (size_t)ev_off[K]);
-  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (K + 1));
+  auto* d_cnt = (unsigned long long*)dbuf(h, "evcount", sizeof(unsigned long long) * (K + 2));
   auto* d_vout = (uint8_t*)dbuf(h, "vout", (size_t)in->n_vars + 1);
-  // gate block: fn_cut[K+1] ready[K] range_items[K] items_done[K] next[2]
+  // gate block: fn_cut[K+1] ready[K] range_items[K] items_done[K] next[3]
   // timed_out[1] (ints), then ev_off[K] ev_cap[K] (long long)
-  const size_t gate_ints = (size_t)(K + 1) + 3 * (size_t)K + 3;
+  const size_t gate_ints = (size_t)(K + 1) + 3 * (size_t)K + 4;
   auto* d_gate = (int*)dbuf(h, "gate", sizeof(int) * gate_ints + 16 + 2 * sizeof(long long) * K);
   if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
-      !d_cnt || !d_vout || !d_gate)
+      !d_cnt || !d_vout || !d_gate || !d_iwf || !d_iwc)
     return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
   int* g_cut = d_gate;
   int* g_ready = g_cut + K + 1;
   int* g_items = g_ready + K;
   int* g_done = g_items + K;
-  int* g_next = g_done + K;          // [0] the launch, [1] a redo
-  int* g_timeout = g_next + 2;
+  int* g_next = g_done + K;          // [0] the launch, [1] a redo, [2] the wide launch
+  int* g_timeout = g_next + 3;
   auto* g_evoff = reinterpret_cast<long long*>(
       reinterpret_cast<uintptr_t>(d_gate + gate_ints + 1) & ~(uintptr_t)7) + 1;
   long long* g_evcap = g_evoff + K;
@@ -416,10 +464,14 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     CK(cudaMemcpyAsync(d_ifn, item_fn.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_ich, item_chunk.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
   }
+  if (n_wide) {
+    CK(cudaMemcpyAsync(d_iwf, wide_fn.data(), sizeof(int32_t) * n_wide, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_iwc, wide_chunk.data(), sizeof(int32_t) * n_wide, cudaMemcpyHostToDevice, st));
+  }
   CK(cudaMemcpyAsync(d_gate, gate_host.data(), sizeof(int) * gate_ints, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(g_evoff, ev_off.data(), sizeof(long long) * K, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(g_evcap, ev_cap.data(), sizeof(long long) * K, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (K + 1), st));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * (K + 2), st));
   dfx::ReplayDev r{};
   r.fns = (const dfx_fn_desc*)d_fns;
   r.ops = (const int32_t*)d_ops;
@@ -438,6 +490,11 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   r.event_count = d_cnt;
   r.var_out = d_vout;
   r.next = reinterpret_cast<unsigned*>(g_next);
+  r.wide_item_fn = (const int32_t*)d_iwf;
+  r.wide_item_chunk = (const int32_t*)d_iwc;
+  r.n_wide_items = (int)n_wide;
+  r.wide_max_slots = wide_slots;
+  r.wide_next = reinterpret_cast<unsigned*>(g_next + 2);
   dfx::GateDev gate{};
   gate.K = K;
   gate.fn_cut = g_cut;
@@ -572,9 +629,48 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       done += (unsigned long long)need;
     }
   }
+  // the wide functions (rare): one ungated launch, all ranges have landed;
+  // their events go into their own region (regrown once if it overflows)
+  if (n_wide) {
+    int64_t ops_w = 0;
+    for (size_t i = 0; i < n_wide; i++)
+      if (i == 0 || wide_fn[i] != wide_fn[i - 1]) ops_w += in->fns[wide_fn[i]].n_ops;
+    int64_t cap_w = (int64_t)(1.25 * (double)(cap > 0 ? cap : 0) *
+                              ((double)ops_w / (double)(in->n_ops > 0 ? in->n_ops : 1))) + 4096;
+    for (int attempt = 0; attempt < 2; attempt++) {
+      auto* d_ew = (dfx_event*)dbuf(h, "events_wide", sizeof(dfx_event) * (size_t)cap_w);
+      if (!d_ew) return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
+      CK(cudaStreamSynchronize(h->s_d2h));
+      dfx::ReplayDev rw = r;
+      rw.events = d_ew;
+      rw.event_cap = cap_w;
+      rw.event_count = d_cnt + K + 1;
+      CK(cudaMemsetAsync(d_cnt + K + 1, 0, sizeof(unsigned long long), st));
+      const int rc = dfx::replay_launch_wide(rw, st);
+      if (rc != DFX_OK) return fail(rc, "wide replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      CK(cudaEventRecord(h->ev1, st));
+      unsigned long long cw = 0;
+      CK(cudaMemcpyAsync(&cw, d_cnt + K + 1, sizeof cw, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if ((int64_t)cw > cap_w && attempt == 0) { cap_w = (int64_t)cw; continue; }
+      count += cw;
+      unsigned long long n = cw;
+      if (cap <= (int64_t)done) n = 0;
+      else if ((int64_t)(done + n) > cap) n = (unsigned long long)cap - done;
+      if (n)
+        CK(cudaMemcpyAsync(out->events + done, d_ew, sizeof(dfx_event) * (size_t)n,
+                           cudaMemcpyDeviceToHost, h->s_d2h));
+      done += n;
+      break;
+    }
+  }
   if (in->n_vars)
     CK(cudaMemcpyAsync(out->var_out, d_vout, (size_t)in->n_vars, cudaMemcpyDeviceToHost, h->s_d2h));
   CK(cudaStreamSynchronize(h->s_d2h));
+  for (const dfx_event& e : host_events) {     // functions beyond the wide limits
+    if ((int64_t)done < cap) out->events[done++] = e;
+    count++;
+  }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   if (h->trace) {

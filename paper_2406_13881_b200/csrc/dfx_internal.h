@@ -24,6 +24,13 @@ struct ReplayDev {
   unsigned long long* event_count;
   uint8_t* var_out;
   unsigned* next;     // work-queue counter of this launch (cleared by replay_launch)
+  // functions beyond the narrow replay's limits (api.cu fn_class): their
+  // items run in a second, wide launch (replay.cu Wide traits)
+  const int32_t* wide_item_fn = nullptr;
+  const int32_t* wide_item_chunk = nullptr;
+  int n_wide_items = 0;
+  int wide_max_slots = 0;
+  unsigned* wide_next = nullptr;
 };
 
 // Range gating of the host-buffer pipeline (replay.cu replay_kernel)
@@ -43,7 +50,13 @@ struct GateDev {
 int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream);
 // replay (persistent grid); with `gate`, items wait for their range's ready
 // flag and the region tables are the caller's (region_launch per range)
+// (without a gate, the wide items follow in a second launch on the stream)
 int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate = nullptr);
+// the wide items only (no region pass): after a gated launch
+int replay_launch_wide(const ReplayDev& r, cudaStream_t stream);
+
+// replay class of a function: 0 narrow, 1 wide, 2 beyond the wide limits
+int fn_class(const dfx_fn_desc& d);
 
 }  // namespace dfx
 

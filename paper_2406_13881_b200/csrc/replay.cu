@@ -24,23 +24,50 @@
 
 namespace dfx {
 
-constexpr int kWarpsPerBlock = 4;
-constexpr int kMaxSlots = 64;
-constexpr int kMaxBr = 48;
-constexpr int kMaxArmStk = 192;
-constexpr int kMaxLoop = 24;
-constexpr uint32_t kNone = 0xFFFFu;
+// Two instantiations of the same replay.  Narrow (every C4 function, the
+// corpus, all generated programs): up to 64 live state slots as 32/64-bit
+// register masks, 16-bit provenance statement ids, small control stacks, 4
+// warps per block.  Wide (rare: e.g. an else-if chain of 13+ branches needs
+// more than 64 slots, or a function of more than 65,534 statements): 256 slots
+// as a 4 x 64-bit register mask, 32-bit provenance ids, deeper stacks, 2
+// warps per block (provenance is 64 KB per warp at 256 slots).  The host
+// routes each function to the narrow launch when it fits, else to the wide
+// one (api.cu fn_class); the semantics are the same code.
+struct Narrow {
+  static constexpr int kWarps = 4, kMaxSlots = 64, kMaxBr = 48, kMaxArmStk = 192, kMaxLoop = 24;
+  using Prov = uint32_t;        // device_producer | last_host_write << 16
+  using Ref = uint8_t;
+  using Skip = uint32_t;
+  static constexpr uint32_t kNone = 0xFFFFu;
+  __device__ static uint32_t dp(Prov p) { return p & 0xFFFFu; }
+  __device__ static uint32_t lw(Prov p) { return p >> 16; }
+  __device__ static Prov pack(uint32_t d, uint32_t l) { return d | (l << 16); }
+};
+struct Wide {
+  static constexpr int kWarps = 2, kMaxSlots = 256, kMaxBr = 256, kMaxArmStk = 1024, kMaxLoop = 64;
+  using Prov = uint64_t;        // device_producer | last_host_write << 32
+  using Ref = uint16_t;
+  using Skip = uint64_t;
+  static constexpr uint32_t kNone = 0xFFFFFFFFu;
+  __device__ static uint32_t dp(Prov p) { return (uint32_t)p; }
+  __device__ static uint32_t lw(Prov p) { return (uint32_t)(p >> 32); }
+  __device__ static Prov pack(uint32_t d, uint32_t l) { return (uint64_t)d | ((uint64_t)l << 32); }
+};
+
+// 256-bit slot mask for the wide replay; every index is resolved with
+// compile-time word selects so the mask stays in registers
+struct Mask256 { uint64_t w[4]; };
 
 struct BrFrame { int16_t saved, arm_base, narms, pad; };
 struct LoopFrame { int32_t stmt, body_pc, loop_start; int16_t slot; int8_t round, may_skip, rec_saved, pad[3]; };
 
-template <class M>
+template <class M, class P>
 struct WarpCtl {
   M live;                    // bit i: ref[i] > 0 (slot masks as wide as the lane's H/D masks)
-  uint8_t ref[kMaxSlots];
-  BrFrame br[kMaxBr];
-  uint8_t armstk[kMaxArmStk];
-  LoopFrame lp[kMaxLoop];
+  typename P::Ref ref[P::kMaxSlots];
+  BrFrame br[P::kMaxBr];
+  uint8_t armstk[P::kMaxArmStk];
+  LoopFrame lp[P::kMaxLoop];
   int cur, nbr, narm, nlp, record, fault;
   int bc0, bc1;          // broadcast scratch
 };
@@ -48,24 +75,67 @@ struct WarpCtl {
 __device__ __forceinline__ int st_start(const int32_t* span, int s) { return __ldg(span + 2 * s); }
 __device__ __forceinline__ int st_end(const int32_t* span, int s) { return __ldg(span + 2 * s + 1); }
 
-// first free slot from the live mask (lane 0 only)
-template <class M>
-__device__ __forceinline__ int alloc_slot(WarpCtl<M>& c, int nslots) {
-  constexpr int kBits = 8 * sizeof(M);
-  const M avail = ~c.live & (nslots >= kBits ? ~(M)0 : (((M)1 << nslots) - (M)1));
-  if (!avail) { c.fault = 1; return 0; }
-  int i;
-  if constexpr (sizeof(M) == 4) i = __ffs((int)avail) - 1;
-  else i = __ffsll((long long)avail) - 1;
-  c.ref[i] = 1;
-  c.live |= (M)1 << i;
-  return i;
+// ---- slot-mask primitives (integer masks and Mask256) ----------------------
+template <class M> __device__ __forceinline__ M mzero() { return (M)0; }
+template <class M> __device__ __forceinline__ M mones() { return ~(M)0; }
+template <> __device__ __forceinline__ Mask256 mzero<Mask256>() { return Mask256{{0, 0, 0, 0}}; }
+template <> __device__ __forceinline__ Mask256 mones<Mask256>() {
+  return Mask256{{~0ull, ~0ull, ~0ull, ~0ull}};
 }
 template <class M>
-__device__ __forceinline__ void ref_inc(WarpCtl<M>& c, int i) { c.ref[i]++; }
+__device__ __forceinline__ int getb(M m, int s) { return (int)((m >> s) & (M)1); }
 template <class M>
-__device__ __forceinline__ void ref_dec(WarpCtl<M>& c, int i) {
-  if (--c.ref[i] == 0) c.live &= ~((M)1 << i);
+__device__ __forceinline__ M setb(M m, int s, int v) {   // branch-free bit assignment
+  const M bit = (M)1 << s;
+  return m ^ ((((M)0 - (M)v) ^ m) & bit);
+}
+__device__ __forceinline__ int getb(const Mask256& m, int s) {
+  const int k = s >> 6;
+  const uint64_t x = k == 0 ? m.w[0] : k == 1 ? m.w[1] : k == 2 ? m.w[2] : m.w[3];
+  return (int)((x >> (s & 63)) & 1ull);
+}
+__device__ __forceinline__ Mask256 setb(Mask256 m, int s, int v) {
+  const int k = s >> 6;
+  const uint64_t bit = 1ull << (s & 63), fill = 0ull - (uint64_t)v;
+#pragma unroll
+  for (int j = 0; j < 4; j++)
+    if (j == k) m.w[j] ^= (fill ^ m.w[j]) & bit;
+  return m;
+}
+// first slot index < nslots that is clear in `live`, or -1
+template <class M>
+__device__ __forceinline__ int first_free(M live, int nslots) {
+  constexpr int kBits = 8 * sizeof(M);
+  const M avail = ~live & (nslots >= kBits ? ~(M)0 : (((M)1 << nslots) - (M)1));
+  if (!avail) return -1;
+  if constexpr (sizeof(M) == 4) return __ffs((int)avail) - 1;
+  else return __ffsll((long long)avail) - 1;
+}
+__device__ __forceinline__ int first_free(const Mask256& live, int nslots) {
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int lo = 64 * j;
+    const uint64_t lim = nslots >= lo + 64 ? ~0ull : nslots > lo ? (1ull << (nslots - lo)) - 1ull : 0ull;
+    const uint64_t avail = ~live.w[j] & lim;
+    if (avail) return lo + __ffsll((long long)avail) - 1;
+  }
+  return -1;
+}
+
+// first free slot from the live mask (lane 0 only)
+template <class M, class P>
+__device__ __forceinline__ int alloc_slot(WarpCtl<M, P>& c, int nslots) {
+  const int i = first_free(c.live, nslots);
+  if (i < 0) { c.fault = 1; return 0; }
+  c.ref[i] = 1;
+  c.live = setb(c.live, i, 1);
+  return i;
+}
+template <class M, class P>
+__device__ __forceinline__ void ref_inc(WarpCtl<M, P>& c, int i) { c.ref[i]++; }
+template <class M, class P>
+__device__ __forceinline__ void ref_dec(WarpCtl<M, P>& c, int i) {
+  if (--c.ref[i] == 0) c.live = setb(c.live, i, 0);
 }
 
 __device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, int64_t cap,
@@ -80,9 +150,10 @@ __device__ __forceinline__ void emit(dfx_event* ev, unsigned long long* count, i
 }
 
 // `_State.merge_conj` provenance rule (dataflow.py:135-142)
+template <class P>
 __device__ __forceinline__ uint32_t pick(const int32_t* span, uint32_t mine, uint32_t other) {
-  if (other == kNone || other == mine) return mine;
-  if (mine == kNone || st_end(span, other) > st_end(span, mine)) return other;
+  if (other == P::kNone || other == mine) return mine;
+  if (mine == P::kNone || st_end(span, other) > st_end(span, mine)) return other;
   return mine;
 }
 
@@ -102,26 +173,18 @@ __device__ __forceinline__ int hoist(const int32_t* t, int loc_lim) {
   return acc;
 }
 
-template <class M>
+template <class M, class P>
 struct Lane {
   M H, D;
-  uint32_t skipH, skipD;
+  typename P::Skip skipH, skipD;
   int presence, to_comp, from_comp;
   int halted;
 };
 
-template <class M>
-__device__ __forceinline__ int getb(M m, int s) { return (int)((m >> s) & (M)1); }
-template <class M>
-__device__ __forceinline__ M setb(M m, int s, int v) {   // branch-free bit assignment
-  const M bit = (M)1 << s;
-  return m ^ ((((M)0 - (M)v) ^ m) & bit);
-}
-
 // One work item (function item_fn[item], 32-variable chunk item_chunk[item]).
-template <class M>
+template <class M, class P>
 __device__ __forceinline__ void
-replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
+replay_one(int item, WarpCtl<M, P>& c, typename P::Prov* prov, int lane, const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
               const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
               const int32_t* __restrict__ item_fn, const int32_t* __restrict__ item_chunk,
@@ -148,18 +211,19 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
   const int rbs = d.region_begin_start;
 
   if (lane == 0) {
-    for (int i = 0; i < kMaxSlots; i++) c.ref[i] = 0;
-    c.live = (M)0;
+    for (int i = 0; i < P::kMaxSlots; i++) c.ref[i] = 0;
+    c.live = mzero<M>();
     c.nbr = c.narm = c.nlp = 0;
     c.record = 1;
     c.fault = 0;
     c.cur = alloc_slot(c, nslots);
   }
-  for (int s = 0; s < slots_per_warp; s++) prov[s * 32 + lane] = 0xFFFFFFFFu;
+  for (int s = 0; s < slots_per_warp; s++) prov[s * 32 + lane] = P::pack(P::kNone, P::kNone);
   __syncwarp();
 
-  Lane<M> L;
-  L.H = ~(M)0; L.D = (M)0;
+  using Skip = typename P::Skip;
+  Lane<M, P> L;
+  L.H = mones<M>(); L.D = mzero<M>();
   L.skipH = L.skipD = 0u;
   L.presence = L.to_comp = L.from_comp = 0;
   L.halted = !active;
@@ -180,7 +244,7 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
       int pre = (pos == DFX_POS_BEFORE && st_start(span, node) <= f.loop_start) ||
                 (pos == DFX_POS_AFTER && st_end(span, node) <= f.loop_start);
       if (!pre) continue;
-      if (kind == DFX_EV_UPDATE_FROM) L.skipH |= 1u << l; else L.skipD |= 1u << l;
+      if (kind == DFX_EV_UPDATE_FROM) L.skipH |= (Skip)1 << l; else L.skipD |= (Skip)1 << l;
     }
   };
   auto copy_slot = [&](int dst, int src) {
@@ -191,11 +255,11 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
   auto merge_conj = [&](int a, int b) {
     L.H = setb(L.H, a, getb(L.H, a) & getb(L.H, b));
     L.D = setb(L.D, a, getb(L.D, a) & getb(L.D, b));
-    const uint32_t pa = prov[a * 32 + lane], pb = prov[b * 32 + lane];
+    const typename P::Prov pa = prov[a * 32 + lane], pb = prov[b * 32 + lane];
     if (pa != pb) {   // equal provenance (the common case) merges to itself
-      const uint32_t dp = pick(span, pa & 0xFFFFu, pb & 0xFFFFu);
-      const uint32_t lw = pick(span, pa >> 16, pb >> 16);
-      prov[a * 32 + lane] = dp | (lw << 16);
+      const uint32_t dp = pick<P>(span, P::dp(pa), P::dp(pb));
+      const uint32_t lw = pick<P>(span, P::lw(pa), P::lw(pb));
+      prov[a * 32 + lane] = P::pack(dp, lw);
     }
   };
 
@@ -240,8 +304,8 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
         if (fl & DFX_F_AFTER_REGION) {
           L.presence = 1; L.from_comp = 1; L.H = setb(L.H, cur, 1); break;
         }
-        uint32_t dp = prov[cur * 32 + lane] & 0xFFFFu;
-        int lim = dp == kNone ? 0 : st_end(span, dp);
+        uint32_t dp = P::dp(prov[cur * 32 + lane]);
+        int lim = dp == P::kNone ? 0 : st_end(span, dp);
         int pos, node;
         if (fl & DFX_F_OVR) { pos = DFX_POS_BODY_END; node = op.w; }
         else {
@@ -260,8 +324,7 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
       case DFX_OP_HW: {   // host_write, dataflow.py:326-330
         if (op.y != myvar || L.halted) break;
         L.H = setb(L.H, cur, 1); L.D = setb(L.D, cur, 0);
-        uint32_t p = prov[cur * 32 + lane];
-        prov[cur * 32 + lane] = (p & 0xFFFFu) | ((uint32_t)op.z << 16);
+        prov[cur * 32 + lane] = P::pack(P::dp(prov[cur * 32 + lane]), (uint32_t)op.z);
         break;
       }
       case DFX_OP_DR: {   // device_read, dataflow.py:332-368
@@ -279,8 +342,8 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
           emit(events, event_count, event_cap, key_now(), fi, var, op.z, DFX_EV_ERR_DECL, 0);
           L.halted = 1; break;
         }
-        uint32_t lw = prov[cur * 32 + lane] >> 16;
-        bool in_region = lw != kNone && rbs >= 0 && st_start(span, lw) >= rbs;
+        uint32_t lw = P::lw(prov[cur * 32 + lane]);
+        bool in_region = lw != P::kNone && rbs >= 0 && st_start(span, lw) >= rbs;
         if (!in_region) { L.to_comp = 1; L.D = setb(L.D, cur, 1); break; }
         int lim = st_end(span, lw);
         int pos, node;
@@ -306,14 +369,13 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
           L.halted = 1; break;
         }
         L.D = setb(L.D, cur, 1); L.H = setb(L.H, cur, 0);
-        uint32_t p = prov[cur * 32 + lane];
-        prov[cur * 32 + lane] = (p & 0xFFFF0000u) | (uint32_t)op.z;
+        prov[cur * 32 + lane] = P::pack((uint32_t)op.z, P::lw(prov[cur * 32 + lane]));
         break;
       }
       case DFX_OP_BR_BEGIN: {  // saved = self.state
         if (!(((uint32_t)op.z >> (chunk & 31)) & 1u)) goto skip_region;
         if (lane == 0) {
-          if (c.nbr >= kMaxBr) c.fault = 1;
+          if (c.nbr >= P::kMaxBr) c.fault = 1;
           else {
             BrFrame& b = c.br[c.nbr++];
             b.saved = (int16_t)cur; ref_inc(c, cur);
@@ -329,9 +391,9 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
         if (lane == 0) {
           BrFrame& b = c.br[c.nbr - 1];
           int s = alloc_slot(c, nslots);
-          if (c.narm >= kMaxArmStk) c.fault = 1;
+          if (c.narm >= P::kMaxArmStk) c.fault = 1;
           c.bc0 = s; c.bc1 = b.saved;
-          const bool room = c.narm < kMaxArmStk;
+          const bool room = c.narm < P::kMaxArmStk;
           if (code == DFX_OP_ARM_FORK) {
             ref_dec(c, cur); c.cur = s;
             if ((fl & DFX_F_CAPTURE) && room) { c.armstk[c.narm++] = (uint8_t)s; ref_inc(c, s); b.narms++; }
@@ -350,7 +412,7 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
       case DFX_OP_ARM_CLOSE: {   // switch arm = current slot
         if (lane == 0) {
           BrFrame& b = c.br[c.nbr - 1];
-          if (c.narm >= kMaxArmStk) c.fault = 1;
+          if (c.narm >= P::kMaxArmStk) c.fault = 1;
           else { c.armstk[c.narm++] = (uint8_t)cur; ref_inc(c, cur); b.narms++; }
         }
         __syncwarp();
@@ -406,7 +468,7 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
       case DFX_OP_LOOP_BEGIN: {  // _loop_rounds: entry = state.copy(); dry round
         if (!(((uint32_t)op.z >> (chunk & 31)) & 1u)) goto skip_region;
         if (lane == 0) {
-          if (c.nlp >= kMaxLoop) c.fault = 1;
+          if (c.nlp >= P::kMaxLoop) c.fault = 1;
           else {
             LoopFrame& f = c.lp[c.nlp++];
             f.stmt = op.y; f.loop_start = st_start(span, op.y);
@@ -437,7 +499,7 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
           __syncwarp();
           copy_slot(f.slot, cur);
           record = f.rec_saved;
-          L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
+          L.skipH &= ~((Skip)1 << lvl); L.skipD &= ~((Skip)1 << lvl);
           __syncwarp();
           if (c.fault) goto fault;
           sbase += (uint64_t)(pc + 1 - f.body_pc);   // the planning round
@@ -446,11 +508,11 @@ replay_one(int item, WarpCtl<M>& c, uint32_t* prov, int lane, const dfx_fn_desc*
         }
         if (f.may_skip) {        // zero-trip skip merge (dataflow.py:575-590)
           int w = f.slot;
-          if (L.skipH & (1u << lvl)) L.H = setb(L.H, w, 1);
-          if (L.skipD & (1u << lvl)) L.D = setb(L.D, w, 1);
+          if (L.skipH & ((Skip)1 << lvl)) L.H = setb(L.H, w, 1);
+          if (L.skipD & ((Skip)1 << lvl)) L.D = setb(L.D, w, 1);
           merge_conj(cur, w);
         }
-        L.skipH &= ~(1u << lvl); L.skipD &= ~(1u << lvl);
+        L.skipH &= ~((Skip)1 << lvl); L.skipD &= ~((Skip)1 << lvl);
         __syncwarp();
         if (lane == 0) { ref_dec(c, f.slot); c.nlp--; }
         __syncwarp();
@@ -536,8 +598,8 @@ __device__ __noinline__ bool wait_set(const volatile int* p) {
 // Persistent: each warp takes work items from `next` (one atomic per item)
 // until none are left, so no warp idles on the rest of its block and the
 // long items (first in the order) never wait for a block slot.
-template <class M, bool GATED>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+template <class M, class P, bool GATED>
+__global__ void __launch_bounds__(P::kWarps * 32, 8)
 replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ ops,
               const int32_t* __restrict__ var_flags, const int32_t* __restrict__ stmt_span,
               const int32_t* __restrict__ sites, const int32_t* __restrict__ arms,
@@ -545,11 +607,11 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
               int n_items, int slots_per_warp, dfx_event* __restrict__ events,
               int64_t event_cap, unsigned long long* __restrict__ event_count,
               uint8_t* __restrict__ var_out, unsigned* __restrict__ next, GateDev gate) {
-  __shared__ WarpCtl<M> ctl_all[kWarpsPerBlock];
-  extern __shared__ uint32_t prov_all[];
+  __shared__ WarpCtl<M, P> ctl_all[P::kWarps];
+  extern __shared__ __align__(16) unsigned char prov_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpCtl<M>& c = ctl_all[warp];
-  uint32_t* prov = prov_all + warp * slots_per_warp * 32;
+  WarpCtl<M, P>& c = ctl_all[warp];
+  typename P::Prov* prov = reinterpret_cast<typename P::Prov*>(prov_raw) + warp * slots_per_warp * 32;
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(next, 1u);
@@ -568,7 +630,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         if (!ok) atomicExch(gate.timed_out, 1u);
       }
       if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return;
-      replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
+      replay_one<M, P>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
                     item_chunk, n_items, slots_per_warp, events + __ldg(gate.ev_off + k),
                     __ldg(gate.ev_cap + k), event_count + k, var_out);
       __threadfence();
@@ -580,7 +642,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
         *reinterpret_cast<volatile unsigned long long*>(gate.host_done + k) = cnt + 1ull;
       }
     } else {
-      replay_one<M>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
+      replay_one<M, P>(item, c, prov, lane, fns, ops, var_flags, stmt_span, sites, arms, item_fn,
                     item_chunk, n_items, slots_per_warp, events, event_cap, event_count, var_out);
       __syncwarp();
     }
@@ -601,7 +663,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 //             | 1 << 31 if the region holds a branch (the current slot changes
 //             identity across it)
 // Idempotent; fields the replay reads from these ops are untouched.
-constexpr int kRegionStack = kMaxBr + kMaxLoop;
+constexpr int kRegionStack = Narrow::kMaxBr + Narrow::kMaxLoop;
 __global__ void __launch_bounds__(32)
 region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int fn_lo, int fn_hi) {
   const int f = fn_lo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -673,27 +735,27 @@ int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream)
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
-int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) {
-  if (!gate && r.fn_hi > r.fn_lo) {
-    const int rc = region_launch(r, r.fn_lo, r.fn_hi, stream);
-    if (rc != DFX_OK) return rc;
-  }
-  int slots = r.max_slots;
+namespace {
+// one persistent launch over an item list: narrow (slot bitmasks in 32-bit
+// registers when every function of the list needs at most 32 live state
+// slots -- all of C4 -- else 64-bit) or wide (Mask256, Wide traits)
+int launch_items(const ReplayDev& r, const int32_t* item_fn, const int32_t* item_chunk,
+                 int n_items, int slots, unsigned* next, bool wide, cudaStream_t stream,
+                 const GateDev* gate) {
   if (slots < 2) slots = 2;
-  if (slots > kMaxSlots) return DFX_E_LIMIT;
-  const size_t smem = (size_t)kWarpsPerBlock * slots * 32 * sizeof(uint32_t);
-  const int need = (r.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (slots > (wide ? Wide::kMaxSlots : Narrow::kMaxSlots)) return DFX_E_LIMIT;
+  const int wpb = wide ? Wide::kWarps : Narrow::kWarps;
+  const size_t smem = (size_t)wpb * slots * 32 * (wide ? sizeof(Wide::Prov) : sizeof(Narrow::Prov));
+  const int need = (n_items + wpb - 1) / wpb;
   if (need == 0) return DFX_OK;
-  if (cudaMemsetAsync(r.next, 0, sizeof(unsigned), stream) != cudaSuccess) return DFX_E_CUDA;
-  // a persistent grid (resident blocks x SMs) over the item queue; slot
-  // bitmasks in 32-bit registers when every function of the batch needs at
-  // most 32 live state slots (all of C4), else 64-bit
+  if (cudaMemsetAsync(next, 0, sizeof(unsigned), stream) != cudaSuccess) return DFX_E_CUDA;
+  // a persistent grid (resident blocks x SMs) over the item queue
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
     int blocks = sms * (per_sm > 0 ? per_sm : 1);
     // gated: leave room for the region kernels that open the ranges
     if (gate) {
@@ -707,19 +769,40 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) 
     }
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    kern<<<blocks, kWarpsPerBlock * 32, smem, stream>>>(
-        r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, r.item_fn, r.item_chunk,
-        r.n_items, slots, r.events, r.event_cap, r.event_count, r.var_out, r.next,
+    kern<<<blocks, wpb * 32, smem, stream>>>(
+        r.fns, r.ops, r.var_flags, r.stmt_span, r.sites, r.arms, item_fn, item_chunk,
+        n_items, slots, r.events, r.event_cap, r.event_count, r.var_out, next,
         gate ? *gate : GateDev{});
   };
-  if (slots <= 32) {
-    if (gate) launch(replay_kernel<uint32_t, true>);
-    else launch(replay_kernel<uint32_t, false>);
+  if (wide) {
+    if (gate) return DFX_E_ARG;             // the wide list runs after the gated launch
+    launch(replay_kernel<Mask256, Wide, false>);
+  } else if (slots <= 32) {
+    if (gate) launch(replay_kernel<uint32_t, Narrow, true>);
+    else launch(replay_kernel<uint32_t, Narrow, false>);
   } else {
-    if (gate) launch(replay_kernel<uint64_t, true>);
-    else launch(replay_kernel<uint64_t, false>);
+    if (gate) launch(replay_kernel<uint64_t, Narrow, true>);
+    else launch(replay_kernel<uint64_t, Narrow, false>);
   }
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+}  // namespace
+
+int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) {
+  if (!gate && r.fn_hi > r.fn_lo) {
+    const int rc = region_launch(r, r.fn_lo, r.fn_hi, stream);
+    if (rc != DFX_OK) return rc;
+  }
+  int rc = launch_items(r, r.item_fn, r.item_chunk, r.n_items, r.max_slots, r.next, false,
+                        stream, gate);
+  if (rc != DFX_OK || gate) return rc;
+  return replay_launch_wide(r, stream);
+}
+
+int replay_launch_wide(const ReplayDev& r, cudaStream_t stream) {
+  if (r.n_wide_items <= 0) return DFX_OK;
+  return launch_items(r, r.wide_item_fn, r.wide_item_chunk, r.n_wide_items, r.wide_max_slots,
+                      r.wide_next, true, stream, nullptr);
 }
 
 }  // namespace dfx

@@ -103,6 +103,22 @@ def pack(progs: list[FnProgram]) -> PackedBatch:
     )
 
 
+def concat_batches(batches: list[PackedBatch]) -> PackedBatch:
+    """One packed batch holding the functions of several, in order (each
+    function's offsets shifted by the sizes of the batches before it)."""
+    fns, offs = [], np.zeros(5, dtype=np.int64)
+    for b in batches:
+        f = b.fns.copy()
+        for k, name in enumerate(("op_off", "var_off", "stmt_off", "site_off", "arm_off")):
+            f[name] += offs[k]
+        fns.append(f)
+        offs += (b.ops.shape[0], b.var_flags.shape[0], b.stmt_span.shape[0],
+                 b.sites.shape[0], b.arms.shape[0] // 2)
+    cat = lambda k: np.ascontiguousarray(np.concatenate([getattr(b, k) for b in batches]))  # noqa: E731
+    return PackedBatch(fns=np.concatenate(fns), ops=cat("ops"), var_flags=cat("var_flags"),
+                       stmt_span=cat("stmt_span"), sites=cat("sites"), arms=cat("arms"))
+
+
 @dataclass
 class RawResult:
     events: np.ndarray     # EVENT_DTYPE, all functions

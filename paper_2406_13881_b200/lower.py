@@ -100,7 +100,10 @@ POS_AFTER = 1
 POS_BODY_END = 2
 POS_KERNEL = 3
 
-MAX_STMTS = 0xFFFE        # provenance ids are uint16 with 0xFFFF = none
+# statement ids: functions with fewer than 0xFFFF statements replay with 16-bit
+# provenance ids (replay.cu Narrow), larger ones with 32-bit ids (Wide); the
+# hoist table's 20-bit node field (DFX_AC_NODE_MASK) is the hard bound
+MAX_STMTS = (1 << 20) - 2
 
 
 class LoweringError(Exception):

@@ -195,6 +195,24 @@ def c3_scalar_mask(cfg: C3Config) -> np.ndarray:
     return out
 
 
+def _check_graph_shapes(n: int, words: int, row_ptr, col, kind, S, planes=()) -> None:
+    """Host buffer shapes the C ABI trusts (it copies n+1 / nnz / n x words
+    elements from these pointers); the graph's contents are validated on the
+    device (acc.cu check_csr)."""
+    if row_ptr.ndim != 1 or row_ptr.shape[0] != n + 1:
+        raise ValueError("row_ptr must have n_nodes + 1 = %d entries" % (n + 1))
+    nnz = int(row_ptr[-1]) if n >= 0 else 0
+    if col.ndim != 1 or col.shape[0] < nnz:
+        raise ValueError("col has %d entries, row_ptr[-1] = %d" % (col.shape[0], nnz))
+    if kind.shape != (n,):
+        raise ValueError("node_kind must have n_nodes = %d entries" % n)
+    if S.shape != (words,):
+        raise ValueError("S must have words = %d entries" % words)
+    for P in planes:
+        if P.shape != (n, words):
+            raise ValueError("bitplanes must be (n_nodes, words) = (%d, %d)" % (n, words))
+
+
 class CsrProblem:
     def __init__(self, eng: _abi.Engine, handle: C.c_void_p, n_nodes: int, words: int):
         self.eng = eng
@@ -223,7 +241,8 @@ class CsrProblem:
         row_ptr, col, kind, R, W, S = arrs
         assert row_ptr.dtype == np.int32 and col.dtype == np.int32 and kind.dtype == np.uint8
         assert R.dtype == np.uint32 and W.dtype == np.uint32 and S.dtype == np.uint32
-        cin = CsrIn(n, words, int(col.shape[0]), *(a.ctypes.data for a in arrs))
+        _check_graph_shapes(n, words, row_ptr, col, kind, S, (R, W))
+        cin = CsrIn(n, words, int(row_ptr[-1]), *(a.ctypes.data for a in arrs))
         h = C.c_void_p()
         eng.check(eng.lib.dfx_csr_create(eng.h, C.byref(cin), C.byref(h)), "dfx_csr_create")
         return cls(eng, h, n, words)
@@ -362,7 +381,8 @@ class MfpSession:
     def run(self, row_ptr, col, kind, R, W, S) -> ReqRows:
         n, words = R.shape
         arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, R, W, S)]
-        cin = CsrIn(n, words, int(arrs[1].shape[0]), *(a.ctypes.data for a in arrs))
+        _check_graph_shapes(n, words, arrs[0], arrs[1], arrs[2], arrs[5], (arrs[3], arrs[4]))
+        cin = CsrIn(n, words, int(arrs[0][-1]), *(a.ctypes.data for a in arrs))
         if self.capacity == 0:
             self.capacity = max(1024, n * words // 2)
         ow = 2 * ((words + 31) // 32)
@@ -389,7 +409,10 @@ def _acc_in(row_ptr, col, kind, acc_off, acc, S, words):
     assert row_ptr.dtype == np.int32 and col.dtype == np.int32 and kind.dtype == np.uint8
     assert acc_off.dtype == np.int64 and acc.dtype == np.uint16 and S.dtype == np.uint32
     n = int(row_ptr.shape[0]) - 1
-    cin = AccIn(n, words, int(col.shape[0]), int(acc_off[-1]),
+    _check_graph_shapes(n, words, row_ptr, col, kind, S)
+    if acc_off.shape != (n + 1,) or acc.shape[0] < int(acc_off[-1]):
+        raise ValueError("acc_off must have n_nodes + 1 entries and acc at least acc_off[-1]")
+    cin = AccIn(n, words, int(row_ptr[-1]), int(acc_off[-1]),
                 *(a.ctypes.data for a in arrs))
     return cin, arrs
 

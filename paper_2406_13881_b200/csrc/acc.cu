@@ -161,6 +161,37 @@ compact_list_kernel(int64_t n_lo, int64_t n_hi, int words, const uint32_t* __res
   }
 }
 
+// Graph validation on the device, before any kernel indexes through the CSR
+// (ADVICE r1): row_ptr[0] == 0, non-decreasing, row_ptr[n] == nnz, every
+// predecessor id in [0, n).  Sets bit 2 of *bad.
+__global__ void __launch_bounds__(256)
+check_csr_kernel(const int32_t* __restrict__ row_ptr, int64_t n, const int32_t* __restrict__ col,
+                 int64_t nnz, int* bad) {
+  int ok = 1;
+  const int64_t total = n + 1 + nnz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i <= n) {
+      const int32_t r = __ldg(row_ptr + i);
+      if (r < 0 || (int64_t)r > nnz) ok = 0;
+      if (i == 0 && r != 0) ok = 0;
+      if (i > 0 && r < __ldg(row_ptr + i - 1)) ok = 0;
+      if (i == n && (int64_t)r != nnz) ok = 0;
+    } else if ((uint64_t)(uint32_t)__ldg(col + (i - n - 1)) >= (uint64_t)n) {
+      ok = 0;
+    }
+  }
+  if (!__all_sync(0xFFFFFFFFu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 2);
+}
+
+int check_csr(const CsrDev& p, int* bad, cudaStream_t st) {
+  int64_t blocks = (p.n_nodes + 1 + p.nnz + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  check_csr_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(p.row_ptr, p.n_nodes, p.col,
+                                                                   p.nnz, bad);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 static int grid_nodes(int64_t n) {
   int64_t g = (n + kWarps - 1) / kWarps;
   if (g > 148 * 16) g = 148 * 16;

@@ -797,6 +797,7 @@ int csr_alloc_all(dfx_csr* c, int64_t n, int words, int64_t nnz, const uint32_t*
 
 int check_words(int64_t n, int words) {
   if (n <= 0 || n > 0x7FFFFFFF) return fail(DFX_E_ARG, "n_nodes %lld out of range", (long long)n);
+  if (words <= 0) return fail(DFX_E_ARG, "words=%d out of range", words);
   if (dfx::vpl_for(words) < 0)
     return fail(DFX_E_LIMIT, "words=%d: need a multiple of 4 and at most 512", words);
   return DFX_OK;
@@ -809,12 +810,32 @@ extern "C" {
 }  // extern "C"
 
 namespace {
+int check_nnz(int64_t nnz) {
+  if (nnz < 0 || nnz > 0x7FFFFFFF) return fail(DFX_E_ARG, "nnz %lld out of range (int32 row_ptr)", (long long)nnz);
+  return DFX_OK;
+}
+
+// the uploaded CSR is well formed (device check, one round trip) before any
+// kernel gathers through it; a bad graph is an argument error, not a fault
+int validate_csr(dfx_csr* c, cudaStream_t st) {
+  CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
+  if (dfx::check_csr(c->p, c->d_bad, st)) return fail(DFX_E_CUDA, "check_csr launch failed");
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) return fail(DFX_E_ARG, "CSR: row_ptr must run from 0 to nnz without decreasing and "
+                                  "every predecessor id must lie in [0, n_nodes)");
+  return DFX_OK;
+}
+
 // H2D of one problem's inputs into already-allocated buffers (+ A = R|W)
 int csr_upload(dfx_csr* c, const dfx_csr_in* in, cudaStream_t st) {
   dfx::CsrDev& p = c->p;
   const size_t plane = sizeof(uint32_t) * (size_t)in->n_nodes * in->words;
   CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
   if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  int vrc = validate_csr(c, st);
+  if (vrc) return vrc;
   CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(p.USE, in->R, plane, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(p.B, in->W, plane, cudaMemcpyHostToDevice, st));
@@ -839,7 +860,10 @@ int dfx_csr_create(dfx_handle* h, const dfx_csr_in* in, dfx_csr** out) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_csr_create: null argument");
   CK(cudaSetDevice(h->device));
   int rc = check_words(in->n_nodes, in->words);
+  if (!rc) rc = check_nnz(in->nnz);
   if (rc) return rc;
+  if (!in->row_ptr || !in->node_kind || !in->R || !in->W || !in->S || (in->nnz && !in->col))
+    return fail(DFX_E_ARG, "dfx_csr_in: null array");
   auto* c = new dfx_csr();
   rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
   if (!rc) rc = csr_upload(c, in, h->st());
@@ -990,6 +1014,11 @@ int64_t dfx_csr_nnz(dfx_csr* c) { return c ? c->p.nnz : -1; }
 int dfx_mfp_csr(dfx_handle* h, const dfx_csr_in* in, dfx_req_out* out, dfx_csr_stats* stats) {
   if (!h || !in) return fail(DFX_E_ARG, "dfx_mfp_csr: null argument");
   CK(cudaSetDevice(h->device));
+  {
+    int vr = check_words(in->n_nodes, in->words);
+    if (!vr) vr = check_nnz(in->nnz);
+    if (vr) return vr;
+  }
   // device buffers persist in the handle across calls of the same shape
   dfx_csr* c = h->csr_cache;
   if (c && (c->p.n_nodes != in->n_nodes || c->p.words != in->words || c->p.nnz != in->nnz ||
@@ -1021,6 +1050,10 @@ int check_acc_in(const dfx_acc_in* in) {
   if (!in->row_ptr || !in->node_kind || !in->acc_off || !in->S || (in->nnz && !in->col) ||
       (in->n_acc && !in->acc))
     return fail(DFX_E_ARG, "dfx_acc_in: null array");
+  int rc = check_nnz(in->nnz);
+  if (rc) return rc;
+  if (in->n_acc < 0 || in->acc_off[0] != 0 || in->acc_off[in->n_nodes] != in->n_acc)
+    return fail(DFX_E_ARG, "dfx_acc_in: acc_off must run from 0 to n_acc");
   return check_words(in->n_nodes, in->words);
 }
 
@@ -1031,12 +1064,15 @@ int check_acc_in(const dfx_acc_in* in) {
 // built meanwhile.  The validation flag is read back by check_bad().
 int csr_upload_acc(dfx_handle* h, dfx_csr* c, const dfx_acc_in* in, cudaStream_t st) {
   dfx::CsrDev& p = c->p;
+  int rc0;
   auto* d_off = (int64_t*)dbuf(h, "acc_off", sizeof(int64_t) * (size_t)(in->n_nodes + 1));
   auto* d_acc = (uint16_t*)dbuf(h, "acc", sizeof(uint16_t) * (size_t)(in->n_acc > 0 ? in->n_acc : 1));
   if (!d_off || !d_acc) return fail(DFX_E_CUDA, "access-list buffers: allocation failed");
   CK(h->pipeline_init());
   CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
   if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  rc0 = validate_csr(c, st);
+  if (rc0) return rc0;
   CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
   CK(cudaEventRecord(h->pev[0], st));

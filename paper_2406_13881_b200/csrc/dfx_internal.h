@@ -99,6 +99,8 @@ struct SolveStats {
 
 int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch, size_t scratch_bytes);
 int or_planes(const CsrDev& p, cudaStream_t st);
+// CSR validation (acc.cu): bit 2 of *bad on a malformed row_ptr / col
+int check_csr(const CsrDev& p, int* bad, cudaStream_t st);
 int build_desc(const CsrDev& p, cudaStream_t st);
 int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tmp, cudaStream_t st);
 int vpl_for(int words);

@@ -33,3 +33,24 @@ def test_library_exports_all_declared_symbols():
     assert not missing, missing
     lib.dfx_abi_version.restype = ctypes.c_int
     assert lib.dfx_abi_version() == _abi.ABI_VERSION
+
+
+def test_graph_shape_checks_on_host():
+    """Short host arrays are rejected before the C ABI copies from them."""
+    import numpy as np
+    import pytest
+    from paper_2406_13881_b200.csr import _check_graph_shapes
+    rp = np.array([0, 1, 2], dtype=np.int32)
+    col = np.array([0, 1], dtype=np.int32)
+    kind = np.zeros(2, dtype=np.uint8)
+    S = np.zeros(4, dtype=np.uint32)
+    R = np.zeros((2, 4), dtype=np.uint32)
+    _check_graph_shapes(2, 4, rp, col, kind, S, (R, R))
+    with pytest.raises(ValueError):
+        _check_graph_shapes(2, 4, rp, col[:1], kind, S)
+    with pytest.raises(ValueError):
+        _check_graph_shapes(3, 4, rp, col, kind, S)
+    with pytest.raises(ValueError):
+        _check_graph_shapes(2, 4, rp, col, kind, S, (R[:1],))
+    with pytest.raises(ValueError):
+        _check_graph_shapes(2, 4, rp, col, kind, S[:2])

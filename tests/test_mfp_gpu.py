@@ -222,3 +222,40 @@ def test_acc_lists_edge_cases():
     OH, OD, _ = prob.download(True, True)
     assert np.array_equal(OH, eh) and np.array_equal(OD, ed)
     _check_lists(prob.requirements_list(capacity=1), g, eh, ed)   # NOSPC, then exact
+
+
+# ---- malformed graphs: argument errors, never device faults
+
+def _small_graph(seed=3, words=4, n=300):
+    rng = np.random.default_rng(seed)
+    return _mfp_ref.random_graph(rng, n, words)
+
+
+@pytest.mark.parametrize("what", ["col_high", "col_neg", "rowptr_dec", "rowptr_start",
+                                  "acc_col_high"])
+def test_malformed_csr_is_an_argument_error_and_engine_survives(what):
+    from paper_2406_13881_b200 import _abi
+    row_ptr, col, kind, R, W, S = _small_graph()
+    col = col.copy()
+    row_ptr = row_ptr.copy()
+    n = row_ptr.shape[0] - 1
+    if what in ("col_high", "acc_col_high"):
+        col[len(col) // 2] = n + 5
+    elif what == "col_neg":
+        col[3] = -1
+    elif what == "rowptr_dec":
+        row_ptr[n // 2] = row_ptr[n // 2 + 1] + 1
+    elif what == "rowptr_start":
+        row_ptr[0] = 1
+    with pytest.raises(_abi.EngineError, match="CSR|row_ptr"):
+        if what == "acc_col_high":
+            off, acc = planes_to_acc(R, W)
+            AccSession().run(row_ptr, col, kind, off, acc, S, R.shape[1])
+        else:
+            CsrProblem.from_arrays(row_ptr, col, kind, R, W, S)
+    # the context is intact: a good problem on the same engine solves exactly
+    row_ptr, col, kind, R, W, S = _small_graph(seed=4)
+    g = {"row_ptr": row_ptr, "col": col, "kind": kind, "A": R | W, "B": W, "USE": R, "S": S}
+    _check(CsrProblem.from_arrays(row_ptr, col, kind, R, W, S), g)
+    rows, _ = mfp_csr(row_ptr, col, kind, R, W, S)
+    assert rows.masks.shape[0] >= 0

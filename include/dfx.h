@@ -341,6 +341,26 @@ typedef struct {
 /* replaces dartomp.interproc.summarize_all: host buffers in and out */
 int dfx_summaries(dfx_handle *h, const dfx_cg_in *in, dfx_cg_out *out);
 
+/* NCCL on the handle (SURVEY §8 b): one communicator per handle, for the
+ * multi-GPU summaries solve.  dfx_comm_unique_id fills DFX_COMM_ID_BYTES
+ * bytes on one rank; every rank passes them to dfx_comm_init (e.g. after a
+ * broadcast).  NCCL is loaded at run time (libnccl.so.2). */
+#define DFX_COMM_ID_BYTES 128
+int dfx_comm_unique_id(void *id_out);
+int dfx_comm_init(dfx_handle *h, const void *unique_id, int32_t nranks, int32_t rank);
+int dfx_comm_destroy(dfx_handle *h);
+
+/* summarize_all across the communicator's ranks, sharded by call-graph
+ * component (replaces interproc.py:90-144 like dfx_summaries): owner[f] is
+ * the rank that rebuilds function f, and a function and its callees must
+ * share an owner.  Per pass: one cooperative launch over the rank's own
+ * waves, then ONE ncclAllReduce(MAX) of the pass's changed flag (the
+ * reference's global termination test); after the last pass ONE
+ * ncclAllGather of the owned rows.  Every rank receives every summary;
+ * *n_collectives = passes + 1 (+0 at one rank). */
+int dfx_summaries_sharded(dfx_handle *h, const dfx_cg_in *in, const int32_t *owner,
+                          dfx_cg_out *out, int32_t *n_collectives);
+
 /* Sharded building blocks (multi-GPU: one process per GPU; the caller
  * all-gathers the rows each shard computed after every wave).  Tables are
  * caller-owned DEVICE memory: bits [n_funcs * nsp] uint8, list

@@ -11,6 +11,8 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "../../include/dfx.h"
 #include "dfx_internal.h"
@@ -60,6 +62,8 @@ struct dfx_handle {
   bool trace = false;
   cudaEvent_t tev[3 * kPipeMax + 1] = {};
   struct dfx_csr* csr_cache = nullptr;   // reused by dfx_mfp_csr across calls
+  ncclComm_t comm = nullptr;             // dfx_comm_init: the handle's NCCL communicator
+  int comm_rank = 0, comm_size = 1;
   std::unordered_map<std::string, std::pair<void*, size_t>> bufs;
 };
 
@@ -137,6 +141,7 @@ int dfx_close(dfx_handle* h) {
   for (auto& e : h->tev)
     if (e) cudaEventDestroy(e);
   if (h->csr_cache) csr_destroy_impl(h->csr_cache);
+  dfx_comm_destroy(h);
   for (auto& ev : h->pev)
     if (ev) cudaEventDestroy(ev);
   if (h->pin_cnt) cudaFreeHost(h->pin_cnt);
@@ -1499,89 +1504,307 @@ int dfx_cgp_destroy(dfx_handle* h, dfx_cgp* p) {
 }
 
 // replaces dartomp.interproc.summarize_all (pkg/src/dartomp/interproc.py:90-144)
+}  // extern "C"
+
+namespace {
+// NCCL, loaded at run time: the process's libnccl.so.2 (torch's, when torch
+// has loaded one) or the system's; no link-time dependency of libdfx.so
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) { x.why = dlerror() ? dlerror() : "libnccl.so.2 not found"; return x; }
+    auto sym = [&](const char* name) { return dlsym(lib, name); };
+    x.GetUniqueId = (decltype(x.GetUniqueId))sym("ncclGetUniqueId");
+    x.CommInitRank = (decltype(x.CommInitRank))sym("ncclCommInitRank");
+    x.CommDestroy = (decltype(x.CommDestroy))sym("ncclCommDestroy");
+    x.AllReduce = (decltype(x.AllReduce))sym("ncclAllReduce");
+    x.AllGather = (decltype(x.AllGather))sym("ncclAllGather");
+    x.GetErrorString = (decltype(x.GetErrorString))sym("ncclGetErrorString");
+    x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.AllReduce && x.AllGather &&
+           x.GetErrorString;
+    if (!x.ok) x.why = "libnccl.so.2 lacks a required symbol";
+    return x;
+  }();
+  return n;
+}
+
+#define NK(expr)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(DFX_E_CUDA, "%s: %s (%s:%d)", #expr, nccl().GetErrorString(r_), __FILE__, \
+                  __LINE__);                                                              \
+  } while (0)
+
+// Device state of one summaries solve (grow-only handle buffers).
+struct CgRun {
+  dfx::CgDev g{};
+  int nf = 0, ns = 0, nsp = 0, maxp = 1;
+  int32_t* d_woff = nullptr;
+  int* d_flags = nullptr;
+  uint8_t* tb[2] = {};
+  int16_t* tl[2] = {};
+  int32_t* tn[2] = {};
+  uint8_t* d_stage = nullptr;
+};
+
+// Upload the graph and pass-0 tables; `wave_off`/`wave_fns` (host) are the
+// schedule this rank runs (the whole graph's, or its owned functions').
+int cg_setup(dfx_handle* h, const dfx_cg_in* in, const int32_t* wave_off, const int32_t* wave_fns,
+             int n_waves, int n_wave_fns, CgRun& R) {
+  cudaStream_t st = h->st();
+  const int nf = in->n_funcs, ns = in->n_slots;
+  R.nf = nf; R.ns = ns;
+  R.nsp = ((ns + 31) / 32) * 32;                  // padded row (16-B quads, 32-bit seen words)
+  const int nsp = R.nsp;
+  R.maxp = in->max_passes > 0 ? in->max_passes : 1;
+  const int maxp = R.maxp;
+  const size_t rows = (size_t)(nf > 0 ? nf : 1);
+  auto* d_direct = (uint8_t*)dbuf(h, "cg_direct", rows * nsp + 16);
+  auto* d_srcoff = (int32_t*)dbuf(h, "cg_srcoff", sizeof(int32_t) * (rows + 1));
+  auto* d_src = (int32_t*)dbuf(h, "cg_src", sizeof(int32_t) * 4 * (size_t)(in->n_src + 1));
+  auto* d_slist = (int16_t*)dbuf(h, "cg_slist", sizeof(int16_t) * (size_t)(in->n_slist + 1));
+  auto* d_bind = (int32_t*)dbuf(h, "cg_bind", sizeof(int32_t) * 2 * (size_t)(in->n_bind + 1));
+  auto* d_wfns = (int32_t*)dbuf(h, "cg_wfns", sizeof(int32_t) * (size_t)(n_wave_fns + 1));
+  R.d_woff = (int32_t*)dbuf(h, "cg_woff", sizeof(int32_t) * (size_t)(n_waves + 1));
+  R.d_flags = (int*)dbuf(h, "cg_flags", sizeof(int) * (size_t)(maxp + 2));
+  R.tb[0] = (uint8_t*)dbuf(h, "cg_b0", rows * nsp + 16);
+  R.tb[1] = (uint8_t*)dbuf(h, "cg_b1", rows * nsp + 16);
+  R.tl[0] = (int16_t*)dbuf(h, "cg_l0", sizeof(int16_t) * rows * nsp + 16);
+  R.tl[1] = (int16_t*)dbuf(h, "cg_l1", sizeof(int16_t) * rows * nsp + 16);
+  R.tn[0] = (int32_t*)dbuf(h, "cg_n0", sizeof(int32_t) * rows);
+  R.tn[1] = (int32_t*)dbuf(h, "cg_n1", sizeof(int32_t) * rows);
+  // dense rows go up contiguously into a staging buffer and are re-pitched
+  // to the padded layout on the device (one DMA per array)
+  R.d_stage = (uint8_t*)dbuf(h, "cg_stage", sizeof(int16_t) * rows * nsp + 16);
+  if (!d_direct || !d_srcoff || !d_src || !d_slist || !d_bind || !d_wfns || !R.d_woff ||
+      !R.d_flags || !R.tb[0] || !R.tb[1] || !R.tl[0] || !R.tl[1] || !R.tn[0] || !R.tn[1] ||
+      !R.d_stage)
+    return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
+  if (nf && ns) {
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = 0;
+    CK(cudaMemcpyAsync(R.d_stage, in->direct, nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(R.d_stage, ns, d_direct, nsp, ns, nf, st);
+    CK(cudaMemcpyAsync(R.d_stage, in->init_bits, nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(R.d_stage, ns, R.tb[0], nsp, ns, nf, st);
+    CK(cudaMemcpyAsync(R.d_stage, in->init_list, 2 * nb, cudaMemcpyHostToDevice, st));
+    rc0 |= dfx::repitch(R.d_stage, 2 * (size_t)ns, R.tl[0], 2 * (size_t)nsp, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(DFX_E_CUDA, "dfx_summaries: repitch failed");
+  }
+  if (nf) CK(cudaMemcpyAsync(R.tn[0], in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_srcoff, in->src_off, sizeof(int32_t) * (size_t)(nf + 1), cudaMemcpyHostToDevice, st));
+  if (in->n_src) CK(cudaMemcpyAsync(d_src, in->src, sizeof(int32_t) * 4 * (size_t)in->n_src, cudaMemcpyHostToDevice, st));
+  if (in->n_slist) CK(cudaMemcpyAsync(d_slist, in->slist, sizeof(int16_t) * (size_t)in->n_slist, cudaMemcpyHostToDevice, st));
+  if (in->n_bind) CK(cudaMemcpyAsync(d_bind, in->bind, sizeof(int32_t) * 2 * (size_t)in->n_bind, cudaMemcpyHostToDevice, st));
+  if (n_wave_fns) CK(cudaMemcpyAsync(d_wfns, wave_fns, sizeof(int32_t) * n_wave_fns, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(R.d_woff, wave_off, sizeof(int32_t) * (size_t)(n_waves + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(R.d_flags, 0, sizeof(int) * (size_t)(maxp + 2), st));
+  dfx::CgDev& g = R.g;
+  g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = n_waves;
+  g.direct = d_direct; g.src_off = d_srcoff; g.src = d_src; g.slist = d_slist; g.bind = d_bind;
+  g.wave_fns = d_wfns;
+  g.h_wave_off = wave_off;
+  return DFX_OK;
+}
+
+// D2H of table `last` as dense rows (re-pitched on the device)
+int cg_download(dfx_handle* h, CgRun& R, int last, dfx_cg_out* out) {
+  cudaStream_t st = h->st();
+  const int nf = R.nf, ns = R.ns, nsp = R.nsp;
+  const size_t rows = (size_t)(nf > 0 ? nf : 1);
+  if (nf && ns) {
+    const size_t nb = (size_t)nf * ns;
+    int rc0 = dfx::repitch(R.tb[last], nsp, R.d_stage, ns, ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
+    CK(cudaMemcpyAsync(out->bits, R.d_stage, nb, cudaMemcpyDeviceToHost, st));
+    auto* d_stage2 = (uint8_t*)dbuf(h, "cg_stage2", sizeof(int16_t) * rows * nsp + 16);
+    if (!d_stage2) return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
+    rc0 = dfx::repitch(R.tl[last], 2 * (size_t)nsp, d_stage2, 2 * (size_t)ns, 2 * (size_t)ns, nf, st);
+    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
+    CK(cudaMemcpyAsync(out->list, d_stage2, 2 * nb, cudaMemcpyDeviceToHost, st));
+  }
+  if (nf) CK(cudaMemcpyAsync(out->len, R.tn[last], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DFX_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int dfx_summaries(dfx_handle* h, const dfx_cg_in* in, dfx_cg_out* out) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_summaries: null argument");
   if (in->n_funcs < 0 || in->n_slots < 0 || in->n_waves < 0)
     return fail(DFX_E_ARG, "dfx_summaries: negative size");
   CK(cudaSetDevice(h->device));
   cudaStream_t st = h->st();
-  const int nf = in->n_funcs, ns = in->n_slots;
-  const int nsp = ((ns + 31) / 32) * 32;                 // padded row (16-B quads, 32-bit seen words)
-  const int maxp = in->max_passes > 0 ? in->max_passes : 1;
-  const size_t rows = (size_t)(nf > 0 ? nf : 1);
-  // device arrays: grow-only handle buffers, no per-call allocation
-  auto* d_direct = (uint8_t*)dbuf(h, "cg_direct", rows * nsp + 16);
-  auto* d_srcoff = (int32_t*)dbuf(h, "cg_srcoff", sizeof(int32_t) * (rows + 1));
-  auto* d_src = (int32_t*)dbuf(h, "cg_src", sizeof(int32_t) * 4 * (size_t)(in->n_src + 1));
-  auto* d_slist = (int16_t*)dbuf(h, "cg_slist", sizeof(int16_t) * (size_t)(in->n_slist + 1));
-  auto* d_bind = (int32_t*)dbuf(h, "cg_bind", sizeof(int32_t) * 2 * (size_t)(in->n_bind + 1));
-  auto* d_wfns = (int32_t*)dbuf(h, "cg_wfns", sizeof(int32_t) * rows);
-  auto* d_woff = (int32_t*)dbuf(h, "cg_woff", sizeof(int32_t) * (size_t)(in->n_waves + 1));
-  auto* d_flags = (int*)dbuf(h, "cg_flags", sizeof(int) * (size_t)(maxp + 2));
-  uint8_t* tb[2] = {(uint8_t*)dbuf(h, "cg_b0", rows * nsp + 16), (uint8_t*)dbuf(h, "cg_b1", rows * nsp + 16)};
-  int16_t* tl[2] = {(int16_t*)dbuf(h, "cg_l0", sizeof(int16_t) * rows * nsp + 16),
-                    (int16_t*)dbuf(h, "cg_l1", sizeof(int16_t) * rows * nsp + 16)};
-  int32_t* tn[2] = {(int32_t*)dbuf(h, "cg_n0", sizeof(int32_t) * rows), (int32_t*)dbuf(h, "cg_n1", sizeof(int32_t) * rows)};
-  if (!d_direct || !d_srcoff || !d_src || !d_slist || !d_bind || !d_wfns || !d_woff || !d_flags ||
-      !tb[0] || !tb[1] || !tl[0] || !tl[1] || !tn[0] || !tn[1])
-    return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
-  // dense rows go up contiguously into a staging buffer and are re-pitched
-  // to the padded layout on the device (one DMA per array)
-  auto* d_stage = (uint8_t*)dbuf(h, "cg_stage", sizeof(int16_t) * rows * nsp + 16);
-  if (!d_stage) return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
-  if (nf && ns) {
-    const size_t nb = (size_t)nf * ns;
-    int rc0 = 0;
-    CK(cudaMemcpyAsync(d_stage, in->direct, nb, cudaMemcpyHostToDevice, st));
-    rc0 |= dfx::repitch(d_stage, ns, d_direct, nsp, ns, nf, st);
-    CK(cudaMemcpyAsync(d_stage, in->init_bits, nb, cudaMemcpyHostToDevice, st));
-    rc0 |= dfx::repitch(d_stage, ns, tb[0], nsp, ns, nf, st);
-    CK(cudaMemcpyAsync(d_stage, in->init_list, 2 * nb, cudaMemcpyHostToDevice, st));
-    rc0 |= dfx::repitch(d_stage, 2 * (size_t)ns, tl[0], 2 * (size_t)nsp, 2 * (size_t)ns, nf, st);
-    if (rc0) return fail(DFX_E_CUDA, "dfx_summaries: repitch failed");
-  }
-  if (nf) CK(cudaMemcpyAsync(tn[0], in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_srcoff, in->src_off, sizeof(int32_t) * (size_t)(nf + 1), cudaMemcpyHostToDevice, st));
-  if (in->n_src) CK(cudaMemcpyAsync(d_src, in->src, sizeof(int32_t) * 4 * (size_t)in->n_src, cudaMemcpyHostToDevice, st));
-  if (in->n_slist) CK(cudaMemcpyAsync(d_slist, in->slist, sizeof(int16_t) * (size_t)in->n_slist, cudaMemcpyHostToDevice, st));
-  if (in->n_bind) CK(cudaMemcpyAsync(d_bind, in->bind, sizeof(int32_t) * 2 * (size_t)in->n_bind, cudaMemcpyHostToDevice, st));
-  if (nf) CK(cudaMemcpyAsync(d_wfns, in->wave_fns, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_woff, in->wave_off, sizeof(int32_t) * (size_t)(in->n_waves + 1), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(d_flags, 0, sizeof(int) * (size_t)(maxp + 2), st));
-  dfx::CgDev g{};
-  g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = in->n_waves;
-  g.direct = d_direct; g.src_off = d_srcoff; g.src = d_src; g.slist = d_slist; g.bind = d_bind;
-  g.wave_fns = d_wfns;
-  g.h_wave_off = in->wave_off;
+  CgRun R;
+  int rc = cg_setup(h, in, in->wave_off, in->wave_fns, in->n_waves, in->n_funcs, R);
+  if (rc) return rc;
   // all passes in one persistent cooperative launch (waves separated by grid
   // barriers); passes alternate tables t0 -> t1 -> t0 ...
   CK(cudaEventRecord(h->ev0, st));
-  int rc = dfx::cg_solve(g, tb[0], tl[0], tn[0], tb[1], tl[1], tn[1], d_woff, maxp, d_flags,
-                         d_flags + maxp + 1, st);
+  rc = dfx::cg_solve(R.g, R.tb[0], R.tl[0], R.tn[0], R.tb[1], R.tl[1], R.tn[1], R.d_woff, R.maxp,
+                     R.d_flags, R.d_flags + R.maxp + 1, st);
   CK(cudaEventRecord(h->ev1, st));
   if (rc) return fail(rc, "cg_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
   int passes = 0;
-  CK(cudaMemcpyAsync(&passes, d_flags + maxp + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&passes, R.d_flags + R.maxp + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  const int last = passes & 1;          // the table the last pass wrote
-  if (nf && ns) {   // re-pitch to dense rows on the device, one DMA per array
-    const size_t nb = (size_t)nf * ns;
-    int rc0 = dfx::repitch(tb[last], nsp, d_stage, ns, ns, nf, st);
-    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
-    CK(cudaMemcpyAsync(out->bits, d_stage, nb, cudaMemcpyDeviceToHost, st));
-    auto* d_stage2 = (uint8_t*)dbuf(h, "cg_stage2", sizeof(int16_t) * rows * nsp + 16);
-    if (!d_stage2) return fail(DFX_E_CUDA, "dfx_summaries: device allocation failed");
-    rc0 = dfx::repitch(tl[last], 2 * (size_t)nsp, d_stage2, 2 * (size_t)ns, 2 * (size_t)ns, nf, st);
-    if (rc0) return fail(rc0, "dfx_summaries: repitch failed");
-    CK(cudaMemcpyAsync(out->list, d_stage2, 2 * nb, cudaMemcpyDeviceToHost, st));
-  }
-  if (nf) CK(cudaMemcpyAsync(out->len, tn[last], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  rc = cg_download(h, R, passes & 1, out);       // the table the last pass wrote
+  if (rc) return rc;
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   out->kernel_ms = ms;
   out->passes = passes;
   out->launches = 1;
+  return DFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL on the handle, and kernel (c) sharded by call-graph components
+// ---------------------------------------------------------------------------
+int dfx_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(DFX_E_ARG, "dfx_comm_unique_id: null argument");
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(DFX_E_CUDA, "NCCL unavailable: %s", n.why.c_str());
+  ncclUniqueId id;
+  NK(n.GetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof id);
+  return DFX_OK;
+}
+
+int dfx_comm_init(dfx_handle* h, const void* unique_id, int32_t nranks, int32_t rank) {
+  if (!h || !unique_id) return fail(DFX_E_ARG, "dfx_comm_init: null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(DFX_E_ARG, "dfx_comm_init: rank %d of %d", rank, nranks);
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(DFX_E_CUDA, "NCCL unavailable: %s", n.why.c_str());
+  CK(cudaSetDevice(h->device));
+  dfx_comm_destroy(h);
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  NK(n.CommInitRank(&h->comm, nranks, id, rank));
+  h->comm_rank = rank;
+  h->comm_size = nranks;
+  return DFX_OK;
+}
+
+int dfx_comm_destroy(dfx_handle* h) {
+  if (!h || !h->comm) return DFX_OK;
+  nccl().CommDestroy(h->comm);
+  h->comm = nullptr;
+  h->comm_rank = 0;
+  h->comm_size = 1;
+  return DFX_OK;
+}
+
+// Kernel (c) across the ranks of the handle's communicator, sharded by
+// call-graph component: owner[f] is the rank that rebuilds f.  The caller
+// guarantees that a function and every function it calls share an owner (a
+// union of connected components of the call graph), so no rank ever reads a
+// row another rank produces while the passes run.  Per pass each rank runs
+// its own functions' waves (the reference's order, interproc.py:105-143,
+// restricted to them) in one cooperative launch, then ONE ncclAllReduce(MAX)
+// of the pass's changed flag decides, on every rank alike, whether another
+// pass follows -- the reference's global termination test, so every
+// component runs exactly the reference's number of passes (insertion orders
+// may still evolve after a component's sets settle).  After the last pass
+// ONE ncclAllGather of the owned rows gives every rank every summary.
+int dfx_summaries_sharded(dfx_handle* h, const dfx_cg_in* in, const int32_t* owner,
+                          dfx_cg_out* out, int32_t* n_collectives) {
+  if (!h || !in || !out || !owner) return fail(DFX_E_ARG, "dfx_summaries_sharded: null argument");
+  if (!h->comm) return fail(DFX_E_ARG, "dfx_summaries_sharded: no communicator (dfx_comm_init)");
+  if (in->n_funcs < 0 || in->n_slots < 0 || in->n_waves < 0)
+    return fail(DFX_E_ARG, "dfx_summaries_sharded: negative size");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const Nccl& nc = nccl();
+  const int nf = in->n_funcs, me = h->comm_rank, world = h->comm_size;
+  for (int f = 0; f < nf; f++)
+    if (owner[f] < 0 || owner[f] >= world)
+      return fail(DFX_E_ARG, "dfx_summaries_sharded: owner[%d] = %d of %d ranks", f, owner[f], world);
+  // this rank's schedule: its functions, wave by wave in the reference order
+  std::vector<int32_t> woff(1, 0), wfns;
+  for (int w = 0; w < in->n_waves; w++) {
+    for (int i = in->wave_off[w]; i < in->wave_off[w + 1]; i++)
+      if (owner[in->wave_fns[i]] == me) wfns.push_back(in->wave_fns[i]);
+    if ((int)wfns.size() > woff.back()) woff.push_back((int32_t)wfns.size());
+  }
+  const int n_waves = (int)woff.size() - 1;
+  CgRun R;
+  int rc = cg_setup(h, in, woff.data(), wfns.data(), n_waves, (int)wfns.size(), R);
+  if (rc) return rc;
+  int collectives = 0;
+  CK(cudaEventRecord(h->ev0, st));
+  int passes = 0;
+  int* d_pass = R.d_flags + R.maxp + 1;
+  for (int p = 1; p <= R.maxp; p++) {
+    if (n_waves > 0) {
+      rc = dfx::cg_solve(R.g, R.tb[0], R.tl[0], R.tn[0], R.tb[1], R.tl[1], R.tn[1], R.d_woff, p,
+                         R.d_flags, d_pass, st, p);
+      if (rc) return fail(rc, "cg_solve failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    NK(nc.AllReduce(R.d_flags + p, R.d_flags + p, 1, ncclInt32, ncclMax, h->comm, st));
+    collectives++;
+    int changed = 0;
+    CK(cudaMemcpyAsync(&changed, R.d_flags + p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    passes = p;
+    if (!changed) break;
+  }
+  const int last = passes & 1;
+  // final exchange: every rank's owned rows to every rank
+  std::vector<int32_t> cnt(world, 0);
+  for (int f = 0; f < nf; f++) cnt[owner[f]]++;
+  const int per = *std::max_element(cnt.begin(), cnt.end());
+  if (world > 1 && per > 0) {
+    const int rowb = 3 * R.nsp + 4;
+    std::vector<int32_t> lists;      // rank r's functions at [r * per, r * per + cnt[r])
+    lists.assign((size_t)world * per, 0);
+    std::vector<int> fill(world, 0);
+    for (int f = 0; f < nf; f++) lists[(size_t)owner[f] * per + fill[owner[f]]++] = f;
+    auto* d_lists = (int32_t*)dbuf(h, "cg_xlists", sizeof(int32_t) * lists.size() + 16);
+    auto* d_send = (uint8_t*)dbuf(h, "cg_xsend", (size_t)per * rowb + 16);
+    auto* d_recv = (uint8_t*)dbuf(h, "cg_xrecv", (size_t)world * per * rowb + 16);
+    if (!d_lists || !d_send || !d_recv) return fail(DFX_E_CUDA, "dfx_summaries_sharded: allocation failed");
+    CK(cudaMemcpyAsync(d_lists, lists.data(), sizeof(int32_t) * lists.size(), cudaMemcpyHostToDevice, st));
+    rc = dfx::cg_pack(R.tb[last], R.tl[last], R.tn[last], R.nsp, d_lists + (size_t)me * per, cnt[me],
+                      d_send, rowb, false, st);
+    if (rc) return fail(rc, "cg_pack failed");
+    NK(nc.AllGather(d_send, d_recv, (size_t)per * rowb, ncclUint8, h->comm, st));
+    collectives++;
+    for (int r = 0; r < world; r++) {
+      if (r == me) continue;
+      rc = dfx::cg_pack(R.tb[last], R.tl[last], R.tn[last], R.nsp, d_lists + (size_t)r * per, cnt[r],
+                        d_recv + (size_t)r * per * rowb, rowb, true, st);
+      if (rc) return fail(rc, "cg_unpack failed");
+    }
+  }
+  CK(cudaEventRecord(h->ev1, st));
+  rc = cg_download(h, R, last, out);
+  if (rc) return rc;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  out->kernel_ms = ms;
+  out->passes = passes;
+  out->launches = n_waves > 0 ? passes : 0;
+  if (n_collectives) *n_collectives = collectives;
   return DFX_OK;
 }
 

@@ -161,6 +161,10 @@ int cg_peer_wait(const unsigned long long* arrive, unsigned long long expect, lo
                  int* err, cudaStream_t st);
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
-             int* d_passes, cudaStream_t st);
+             int* d_passes, cudaStream_t st, int first_pass = 1);
+// pack (unpack=false) the listed functions' rows of a table into `out`
+// (rowb = 3*nsp + 4 bytes per row), or scatter them back (unpack=true)
+int cg_pack(uint8_t* b, int16_t* l, int32_t* n, int nsp, const int32_t* fns, int count,
+            uint8_t* out, int rowb, bool unpack, cudaStream_t st);
 
 }  // namespace dfx

@@ -151,8 +151,8 @@ cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int ns
 // uniformly after the first pass that changed no bit set.  changed[p] is the
 // flag of pass p (zeroed by the host); *passes_out = passes run.
 __global__ void __launch_bounds__(kCgWarps * 32)
-cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, int max_passes,
-                int* __restrict__ changed, int* __restrict__ passes_out) {
+cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, int first_pass,
+                int max_passes, int* __restrict__ changed, int* __restrict__ passes_out) {
   namespace cgr = cooperative_groups;
   cgr::grid_group grid = cgr::this_grid();
   extern __shared__ uint32_t seen_all[];
@@ -160,7 +160,7 @@ cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, i
   uint32_t* seen = seen_all + warp * (g.nsp >> 5);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int pass = 1; pass <= max_passes; pass++) {
+  for (int pass = first_pass; pass <= max_passes; pass++) {
     const CgBuf& prev = (pass & 1) ? t0 : t1;
     const CgBuf& cur = (pass & 1) ? t1 : t0;
     bool any = false;
@@ -192,6 +192,46 @@ int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 
+// Final exchange of the component-sharded solve (api.cu
+// dfx_summaries_sharded): each rank packs the rows it owns -- bits, insertion
+// order, length -- into one contiguous send block; after the all-gather every
+// rank scatters the other ranks' blocks into its table.  One warp per row.
+__global__ void cg_pack_kernel(CgBuf t, int nsp, const int32_t* __restrict__ fns, int n,
+                               uint8_t* __restrict__ out, int rowb) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const int f = __ldg(fns + i);
+    uint8_t* o = out + (size_t)i * rowb;
+    for (int c = lane; c < nsp; c += 32) o[c] = t.bits[(size_t)f * nsp + c];
+    int16_t* ol = reinterpret_cast<int16_t*>(o + nsp);
+    for (int c = lane; c < nsp; c += 32) ol[c] = t.list[(size_t)f * nsp + c];
+    if (lane == 0) *reinterpret_cast<int32_t*>(o + 3 * nsp) = t.len[f];
+  }
+}
+__global__ void cg_unpack_kernel(CgBuf t, int nsp, const int32_t* __restrict__ fns, int n,
+                                 const uint8_t* __restrict__ in, int rowb) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const int f = __ldg(fns + i);
+    const uint8_t* o = in + (size_t)i * rowb;
+    for (int c = lane; c < nsp; c += 32) t.bits[(size_t)f * nsp + c] = o[c];
+    const int16_t* ol = reinterpret_cast<const int16_t*>(o + nsp);
+    for (int c = lane; c < nsp; c += 32) t.list[(size_t)f * nsp + c] = ol[c];
+    if (lane == 0) t.len[f] = *reinterpret_cast<const int32_t*>(o + 3 * nsp);
+  }
+}
+
+int cg_pack(uint8_t* b, int16_t* l, int32_t* n, int nsp, const int32_t* fns, int count,
+            uint8_t* out, int rowb, bool unpack, cudaStream_t st) {
+  if (count <= 0) return DFX_OK;
+  int blocks = (count + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  CgBuf t{b, l, n};
+  if (unpack) cg_unpack_kernel<<<blocks, 256, 0, st>>>(t, nsp, fns, count, out, rowb);
+  else cg_pack_kernel<<<blocks, 256, 0, st>>>(t, nsp, fns, count, out, rowb);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 // row re-pitching between the ABI's dense [rows][n] layout and the kernels'
 // padded [rows][np] layout (elements of `es` bytes; padding zero-filled)
 __global__ void repitch_kernel(const uint8_t* __restrict__ src, size_t sp, uint8_t* __restrict__ dst,
@@ -216,7 +256,7 @@ int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size
 // whole solve on the device; returns the passes run through *passes (device)
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
-             int* d_passes, cudaStream_t st) {
+             int* d_passes, cudaStream_t st, int first_pass) {
   static int sms = 0, per_sm = 0;
   const size_t smem = (size_t)kCgWarps * (g.nsp / 32) * sizeof(uint32_t);
   if (!sms) {
@@ -240,7 +280,7 @@ int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1,
   if (blocks < 1) blocks = 1;
   CgDev gg = g;
   CgBuf t0{b0, l0, n0}, t1{b1, l1, n1};
-  void* args[] = {&gg, &t0, &t1, &d_wave_off, &max_passes, &d_changed, &d_passes};
+  void* args[] = {&gg, &t0, &t1, &d_wave_off, &first_pass, &max_passes, &d_changed, &d_passes};
   if (cudaLaunchCooperativeKernel((const void*)cg_solve_kernel, dim3(blocks), dim3(kCgWarps * 32),
                                   args, smem, st) != cudaSuccess)
     return DFX_E_CUDA;

@@ -1,6 +1,17 @@
 """Multi-GPU drivers: one process per GPU, `torch.distributed` for plumbing.
 
-* Kernel (c) across GPUs (`ShardedSummaries`): each wave of the reference's
+* Kernel (c) across GPUs, component-sharded (`ComponentSummaries`, the
+  product path): functions are owned by ranks whole call-graph component at
+  a time (LPT on component cost), so during the passes no rank reads a row
+  another rank writes.  Per pass each rank runs its own functions' waves,
+  then ONE all-reduce(MAX) of the changed flag (the reference's global
+  termination test, `interproc.py:105-143`); after the last pass ONE
+  all-gather of the owned rows.  On GPUs all of it runs inside
+  `dfx_summaries_sharded` over the handle's NCCL communicator
+  (`dfx_comm_init`); the same protocol runs on CPU tensors with gloo for the
+  world-size-2 tests.
+* Kernel (c) across GPUs, wave-sharded (`ShardedSummaries`, for a call graph
+  that is one giant component): each wave of the reference's
   pass schedule is split round-robin over the ranks; a rank rebuilds its
   share of the wave's functions on its GPU (`dfx_cg_wave`), then the ranks
   all-gather the rebuilt summary rows (bits + insertion order + length) --
@@ -27,6 +38,169 @@ from . import _abi
 
 class CgTables(C.Structure):
     _fields_ = [("bits", C.c_void_p), ("list", C.c_void_p), ("len", C.c_void_p)]
+
+
+def call_components(g) -> np.ndarray:
+    """Connected components of the call graph (union-find over the calls to
+    defined functions, SRC_CALL rows): component id per function."""
+    from .interproc import SRC_CALL
+    nf = g.init_bits.shape[0]
+    parent = np.arange(nf, dtype=np.int64)
+
+    def find(x):
+        r = x
+        while parent[r] != r:
+            r = parent[r]
+        while parent[x] != r:
+            parent[x], x = r, parent[x]
+        return r
+    src = np.asarray(g.src).reshape(-1, 4)
+    for f in range(nf):
+        for k in range(int(g.src_off[f]), int(g.src_off[f + 1])):
+            if (int(src[k, 0]) & 0xFF) == SRC_CALL:
+                a, b = find(f), find(int(src[k, 1]))
+                if a != b:
+                    parent[max(a, b)] = min(a, b)
+    return np.array([find(f) for f in range(nf)], dtype=np.int64)
+
+
+def component_owner(g, world: int) -> np.ndarray:
+    """Owner rank of every function: whole components, longest processing
+    time first on cost = functions + call-graph sources of the component."""
+    from .batch import lpt_shards
+    comp = call_components(g)
+    nf = comp.shape[0]
+    ids, inv = np.unique(comp, return_inverse=True)
+    srcs = np.diff(np.asarray(g.src_off, dtype=np.int64))
+    cost = np.bincount(inv, weights=1.0 + srcs, minlength=ids.shape[0])
+    owner = np.zeros(nf, dtype=np.int32)
+    for r, cs in enumerate(lpt_shards(cost, world)):
+        owner[np.isin(inv, cs)] = r
+    return owner
+
+
+class ComponentSummaries:
+    """summarize_all across ranks, one collective per pass (see the module
+    docstring).  GPU: `dfx_summaries_sharded` on a handle whose NCCL
+    communicator this object initialises (rank 0's unique id is broadcast
+    through `torch.distributed`).  `wave_impl` selects the same protocol on
+    CPU tensors with `torch.distributed` collectives (gloo tests)."""
+
+    def __init__(self, g, rank: int = 0, world: int = 1, eng: _abi.Engine | None = None,
+                 max_passes: int | None = None, wave_impl=None, owner=None):
+        self.g = g
+        self.rank, self.world = rank, world
+        self.owner = component_owner(g, world) if owner is None else np.asarray(owner, np.int32)
+        self.max_passes = max_passes or max(16, g.init_bits.shape[0] + 1)
+        self.collectives = 0
+        self.wave_impl = wave_impl
+        if wave_impl is not None:
+            return
+        from .interproc import cg_struct
+        self.eng = eng or _abi.engine()
+        lib = self.eng.lib
+        for n in ("dfx_comm_unique_id", "dfx_comm_init", "dfx_comm_destroy",
+                  "dfx_summaries_sharded"):
+            getattr(lib, n).restype = C.c_int
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            self.eng.check(lib.dfx_comm_unique_id(uid), "dfx_comm_unique_id")
+        if world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0)
+            uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        self.eng.check(lib.dfx_comm_init(self.eng.h, uid, C.c_int32(world), C.c_int32(rank)),
+                       "dfx_comm_init")
+        self._keep: list = []
+        self.cin = cg_struct(g, self._keep, self.max_passes)
+
+    def local_schedule(self):
+        """This rank's waves: its own functions, in the reference order."""
+        g = self.g
+        woff, wfns = [0], []
+        for w in range(g.wave_off.shape[0] - 1):
+            seg = g.wave_fns[g.wave_off[w]:g.wave_off[w + 1]]
+            wfns.extend(int(f) for f in seg if self.owner[f] == self.rank)
+            if len(wfns) > woff[-1]:
+                woff.append(len(wfns))
+        return np.array(woff, dtype=np.int32), np.array(wfns, dtype=np.int32)
+
+    def solve(self):
+        """Returns (bits uint8 [nf, ns], list int16 [nf, ns], len int32, passes)."""
+        if self.wave_impl is not None:
+            return self._solve_protocol()
+        from .interproc import CgOut
+        bits = np.zeros(self.g.init_bits.shape, dtype=np.uint8)
+        lst = np.zeros(self.g.init_list.shape, dtype=np.int16)
+        ln = np.zeros(self.g.init_bits.shape[0], dtype=np.int32)
+        out = CgOut(bits.ctypes.data, lst.ctypes.data, ln.ctypes.data, 0, 0, 0.0)
+        ncol = C.c_int32(0)
+        own = np.ascontiguousarray(self.owner, dtype=np.int32)
+        self.eng.check(self.eng.lib.dfx_summaries_sharded(
+            self.eng.h, C.byref(self.cin), C.c_void_p(own.ctypes.data), C.byref(out),
+            C.byref(ncol)), "dfx_summaries_sharded")
+        self.kernel_ms = float(out.kernel_ms)
+        self.collectives = int(ncol.value)
+        return bits, lst, ln, int(out.passes)
+
+    def _solve_protocol(self):
+        """The same protocol on CPU tensors (wave_impl(prev, cur, w) rebuilds
+        the listed functions of local wave w)."""
+        import dataclasses
+        woff, wfns = self.local_schedule()
+        g, nf = self.g, self.g.init_bits.shape[0]
+        local = dataclasses.replace(g, wave_off=woff, wave_fns=wfns)
+        st = ShardedSummaries(local, 0, 1, device="cpu", wave_impl=lambda *a: 0,
+                              max_passes=self.max_passes)
+        st.wave_impl = self.wave_impl(st)
+        st._reset()
+        prev, passes = 0, 0
+        while passes < self.max_passes:
+            passes += 1
+            cur = prev ^ 1
+            changed = 0
+            for w in range(woff.shape[0] - 1):
+                changed |= st.wave_impl(prev, cur, w)
+            flag = torch.tensor([changed], dtype=torch.int32)
+            if self.world > 1:
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            self.collectives += 1
+            prev = cur
+            if not int(flag.item()):
+                break
+        t = st.t[prev]
+        if self.world > 1:
+            mine = torch.from_numpy(np.nonzero(self.owner == self.rank)[0].astype(np.int64))
+            per = int(np.bincount(self.owner, minlength=self.world).max())
+            rowb = st.nsp + 2 * st.nsp + 4
+            send = torch.zeros((per, rowb), dtype=torch.uint8)
+            k = mine.numel()
+            send[:k, :st.nsp] = t["bits"].index_select(0, mine)
+            send[:k, st.nsp:3 * st.nsp] = t["list"].index_select(0, mine).view(torch.uint8)
+            send[:k, 3 * st.nsp:] = t["len"].index_select(0, mine).view(torch.uint8).view(-1, 4)
+            recv = [torch.empty_like(send) for _ in range(self.world)]
+            dist.all_gather(recv, send)
+            self.collectives += 1
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                ids = torch.from_numpy(np.nonzero(self.owner == r)[0].astype(np.int64))
+                rows = recv[r][:ids.numel()]
+                t["bits"].index_copy_(0, ids, rows[:, :st.nsp].contiguous())
+                t["list"].index_copy_(0, ids, rows[:, st.nsp:3 * st.nsp].contiguous().view(torch.int16))
+                t["len"].index_copy_(0, ids, rows[:, 3 * st.nsp:].contiguous().view(torch.int32).view(-1))
+        return (t["bits"][:, :st.ns].numpy().copy(), t["list"][:, :st.ns].numpy().copy(),
+                t["len"].numpy().copy(), passes)
+
+    def close(self):
+        if self.wave_impl is None and getattr(self, "eng", None) is not None:
+            self.eng.lib.dfx_comm_destroy(self.eng.h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ShardedSummaries:

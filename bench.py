@@ -61,6 +61,8 @@ def parse_args():
     ap.add_argument("--c4-funcs", type=int, default=100_000)
     ap.add_argument("--no-c4", action="store_true",
                     help="skip the C4 sub-record of the default (c3) run")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the C5 sub-record of the default (c3) run")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the post-run parity check of the timed outputs")
     ap.add_argument("--c4-ref-funcs", type=int, default=1000,
@@ -424,6 +426,9 @@ def run_ours(args, rank, world, local):
     c4 = None
     if not args.no_c4:
         c4 = run_c4(args, rank, world, local, sub=True)
+    c5 = None
+    if not args.no_c5:
+        c5 = run_c5(args, rank, world, local)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -457,6 +462,8 @@ def run_ours(args, rank, world, local):
         line["cpu_baseline"] = base
     if c4 is not None:
         line["c4"] = c4
+    if c5 is not None:
+        line["c5"] = c5
     print(json.dumps(line), flush=True)
 
 
@@ -651,6 +658,107 @@ def run_c4(args, rank, world, local, sub=False):
     rec.update({"warmup": args.warmup, "vs_baseline": None, "dtype": "u32"})
     print(json.dumps(rec), flush=True)
     return None
+
+
+def run_c5(args, rank, world, local):
+    """Configuration C5 record: the 10k-function call graph (gen/c5.py)
+    through kernel (c) -- the single-launch solve (`dfx_summaries`) and the
+    component-sharded solve over the ranks' NCCL communicator
+    (`dfx_summaries_sharded`: one all-reduce per pass + one all-gather) --
+    and, at one rank, the reference's own summarize_all on the same-shaped C
+    program (gen/callgraph.py, 10k functions; front end untimed) beside the
+    drop-in summarize_all on the same parse, with an identity check."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_13881_b200.distributed import ComponentSummaries
+    from paper_2406_13881_b200.gen.c5 import generate_c5
+    from paper_2406_13881_b200.interproc import solve_call_graph
+
+    torch.cuda.set_device(local)
+    g = generate_c5(seed=0, n_funcs=10_000)
+    for _ in range(3):
+        r = solve_call_graph(g)
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        r = solve_call_graph(g)
+        ts.append(time.perf_counter() - t0)
+    cs = ComponentSummaries(g, rank, world)
+    cs.solve()
+    tc = []
+    for _ in range(5):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        bits, lst, ln, passes = cs.solve()
+        tc.append(time.perf_counter() - t0)
+    same = bool(np.array_equal(bits, r.bits) and np.array_equal(ln, r.len) and passes == r.passes)
+    t = torch.tensor([statistics.median(tc)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nf, ns = g.init_bits.shape
+    rec = {"workload": "C5: %d functions, depth-12 chains, 10%% back edges, %d globals"
+                       % (nf, ns - g.n_params),
+           "unit": "summary facts/s (functions x slots per solve)",
+           "single_launch": {"value": nf * ns / statistics.median(ts), "passes": r.passes,
+                             "device_ms": r.kernel_ms, "call_ms": 1e3 * statistics.median(ts),
+                             "path": "dfx_summaries: all passes and waves in one cooperative launch"},
+           "component_sharded": {"value": nf * ns / float(t.item()), "ranks": world,
+                                 "call_ms_max_over_ranks": 1e3 * float(t.item()),
+                                 "collectives_per_solve": cs.collectives, "passes": passes,
+                                 "equal_to_single_launch": same,
+                                 "path": "dfx_summaries_sharded over the handle's NCCL "
+                                         "communicator (dfx_comm_init)"}}
+    cs.close()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from paper_2406_13881_b200._host import have_dartomp
+        if have_dartomp():
+            rec["reference"] = c5_reference_compare()
+    return rec if rank == 0 else None
+
+
+def c5_reference_compare(n_funcs=10_000):
+    """The reference's summarize_all (interproc.py:90-144) and the drop-in
+    on one parse of the same C program (front end untimed)."""
+    from paper_2406_13881_b200._host import import_dartomp
+    import_dartomp()
+    from dartomp.access import VariableTable, classify_accesses
+    from dartomp.astcfg import build_astcfg
+    from dartomp.interproc import summarize_all as ref_summarize_all
+    from dartomp.lexer import expand_defines
+    from dartomp.nodes import defined_functions
+    from dartomp.parser import parse
+    from dartomp.source import SourceFile
+    from paper_2406_13881_b200.gen.callgraph import CallGraphConfig, generate
+    from paper_2406_13881_b200.interproc import summarize_all as our_summarize_all
+    text = generate(7, CallGraphConfig(n_funcs=n_funcs))
+    src = SourceFile.from_text(text, path="c5.c")
+    pre = expand_defines(src)
+    tu, _ = parse(src, pre)
+    table = VariableTable(src, tu)
+    cfgs, raw = {}, {}
+    for name, fn in defined_functions(tu).items():
+        cfgs[name] = build_astcfg(src, fn)
+        raw[name] = classify_accesses(src, cfgs[name], table)
+    t0 = time.perf_counter()
+    ref = ref_summarize_all(src, tu, cfgs, raw, table)
+    t_ref = time.perf_counter() - t0
+    our_summarize_all(src, tu, cfgs, raw, table)                 # warm
+    t0 = time.perf_counter()
+    ours = our_summarize_all(src, tu, cfgs, raw, table)
+    t_ours = time.perf_counter() - t0
+    same = list(ref) == list(ours) and all(
+        list(ref[k].param_effects.items()) == list(ours[k].param_effects.items())
+        and list(ref[k].global_effects.items()) == list(ours[k].global_effects.items())
+        for k in ref)
+    return {"workload": "C5 from C source: %d defined functions (gen/callgraph.py seed 7)" % len(cfgs),
+            "reference_summarize_all_ms": 1e3 * t_ref, "dropin_summarize_all_ms": 1e3 * t_ours,
+            "speedup": t_ref / t_ours, "identical_summaries_and_dict_order": bool(same),
+            "cpu_baseline": {"kind": "reference", "cores": 1,
+                             "sample": "the full program, one process (its passes are sequential)"},
+            **host_info()}
 
 
 def main():

@@ -202,11 +202,8 @@ int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* ba
                int64_t n_hi, cudaStream_t st) {
   if (n_hi <= n_lo) return DFX_OK;
   const size_t smem = (size_t)kWarps * 2 * p.words * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(expand_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
+  // the attribute is per device: set it on every call (cheap)
+  cudaFuncSetAttribute(expand_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   expand_acc_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, smem, st>>>(n_lo, n_hi, p.words, off,
                                                                          acc, p.A, p.B, p.USE, bad);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;

@@ -510,6 +510,8 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   gate.items_done = reinterpret_cast<unsigned*>(g_done);
   gate.host_done = h->host_done_dev;
   gate.timed_out = reinterpret_cast<unsigned*>(g_timeout);
+  gate.timeout_ns = 20000000000ull;                 // 20 s, then the ungated replay
+  if (const char* e = getenv("DFX_GATE_TIMEOUT_MS")) gate.timeout_ns = 1000000ull * strtoull(e, nullptr, 10);
   auto lo = [&](int f, int32_t dfx_fn_desc::*off) -> int64_t { return f < nf ? in->fns[f].*off : -1; };
   // region tables on two streams, alternating by range: a region kernel
   // shares the SMs with the running replay, so consecutive ranges' tables
@@ -604,7 +606,27 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   {
     int timed_out = 0;
     CK(cudaMemcpy(&timed_out, g_timeout, sizeof timed_out, cudaMemcpyDeviceToHost));
-    if (timed_out) return fail(DFX_E_CUDA, "dfx_replay_batch: a range never became ready");
+    if (timed_out) {
+      // a range's region kernel never got an SM slot beside the gated launch
+      // (e.g. another process holds the GPU): replay the batch again,
+      // ungated, through the device-resident path
+      if (h->trace) fprintf(stderr, "dfx_replay_batch: gate timed out; replaying ungated\n");
+      for (cudaStream_t sr : s_regs) cudaStreamSynchronize(sr);
+      cudaStreamSynchronize(h->s_copy);
+      dfx_replay* rp = nullptr;
+      int rc = dfx_replay_create(h, in, out->event_cap > 0 ? out->event_cap : 1, &rp);
+      if (rc) return rc;
+      int64_t n_ev = 0;
+      float kms = 0.f;
+      rc = dfx_replay_run(h, rp, &n_ev, &kms);
+      if (rc == DFX_OK || rc == DFX_E_NOSPC) {
+        const int rc2 = dfx_replay_fetch(h, rp, out);
+        if (rc == DFX_OK) rc = rc2;
+        out->kernel_ms = kms;
+      }
+      dfx_replay_destroy(h, rp);
+      return rc;
+    }
   }
   if (!redo.empty() && (int64_t)count <= cap) {
     for (int k : redo) {

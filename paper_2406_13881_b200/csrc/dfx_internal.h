@@ -44,6 +44,7 @@ struct GateDev {
   unsigned* items_done;              // [K]
   unsigned long long* host_done;     // [K] mapped host memory: count + 1 when done
   unsigned* timed_out;
+  unsigned long long timeout_ns;     // a range not ready by then fails the wait ($DFX_GATE_TIMEOUT_MS)
 };
 
 // region tables of functions [fn_lo, fn_hi) (replay.cu region_kernel)

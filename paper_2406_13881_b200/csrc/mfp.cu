@@ -637,20 +637,22 @@ int or_planes(const CsrDev& p, cudaStream_t st) {
 template <int PHASE>
 static int launch_phase(const CsrDev& p, int q0, int chunk_nodes, int n_chunks, RoundCtl* ctl,
                         uint8_t* flags, cudaStream_t st) {
-  static int sms = 0, per_sm = 0;
+  // occupancy per device (a thread may drive handles on several devices)
+  constexpr int kDevs = 64;
+  static int sms[kDevs] = {}, per_sm[kDevs] = {};
   auto* fn = mfp_phase_kernel<PHASE, 4>;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
-    if (per_sm < 1) per_sm = 1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) return DFX_E_CUDA;
+  if (!sms[dev]) {
+    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], fn, 256, 0);
+    if (per_sm[dev] < 1) per_sm[dev] = 1;
   }
   CsrDev pp = p;
   int max_rounds = 1 << 30;
   void* args[] = {&pp, &q0, &chunk_nodes, &n_chunks, &ctl, &flags, &max_rounds};
-  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(sms * per_sm), dim3(256), args, 0, st) !=
-      cudaSuccess)
+  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(sms[dev] * per_sm[dev]), dim3(256), args, 0,
+                                  st) != cudaSuccess)
     return DFX_E_CUDA;
   return DFX_OK;
 }
@@ -673,9 +675,16 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
   const int n_slices = vpl;                 // 32 quads (4096 variables) per slice
   const int n_chunks = (int)((p.n_nodes + chunk_nodes - 1) / chunk_nodes);
   RoundCtl* ctls = reinterpret_cast<RoundCtl*>(ctl_mem);   // [slice][phase]
-  static thread_local cudaEvent_t ev[2 * 2 * kMaxSlices] = {};
+  // timing events per (thread, device): an event may only be recorded on a
+  // stream of the device it was created on
+  constexpr int kDevs = 64;
+  static thread_local cudaEvent_t ev_dev[kDevs][2 * 2 * kMaxSlices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) return DFX_E_CUDA;
+  cudaEvent_t* ev = ev_dev[dev];
   if (!ev[0])
-    for (auto& e : ev) cudaEventCreate(&e);
+    for (int i = 0; i < 2 * 2 * kMaxSlices; i++)
+      if (cudaEventCreate(&ev[i]) != cudaSuccess) return DFX_E_CUDA;
   static int trace = -1;
   if (trace < 0) trace = getenv("DFX_TRACE") ? 1 : 0;
   if (cudaMemsetAsync(ctls, 0, sizeof(RoundCtl) * 2 * n_slices, st) != cudaSuccess) return DFX_E_CUDA;
@@ -684,11 +693,11 @@ int mfp_solve(const CsrDev& p, void* ctl_mem, uint8_t* flags, cudaStream_t st, i
       if (cudaMemsetAsync(flags, 0, 2 * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
       if (cudaMemsetAsync(p.chunk_done, 0, sizeof(int) * (size_t)n_chunks, st) != cudaSuccess) return DFX_E_CUDA;
       const int k = 2 * sl + phase;
-      cudaEventRecord(ev[2 * k], st);
+      if (cudaEventRecord(ev[2 * k], st) != cudaSuccess) return DFX_E_CUDA;
       int rc = phase == 0 ? launch_phase<0>(p, 32 * sl, chunk_nodes, n_chunks, ctls + k, flags, st)
                           : launch_phase<1>(p, 32 * sl, chunk_nodes, n_chunks, ctls + k, flags, st);
       if (rc != DFX_OK) return rc;
-      cudaEventRecord(ev[2 * k + 1], st);
+      if (cudaEventRecord(ev[2 * k + 1], st) != cudaSuccess) return DFX_E_CUDA;
     }
   if (!collect) return DFX_OK;        // enqueued only: no host synchronisation
   static thread_local RoundCtl h[2 * kMaxSlices];

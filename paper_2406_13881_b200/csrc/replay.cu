@@ -581,14 +581,14 @@ halt_all:
 
 // Bounded wait (lane 0) for *p != 0; false after ~20 s (a range whose inputs
 // never arrive must not hang the device)
-__device__ __noinline__ bool wait_set(const volatile int* p) {
+__device__ __noinline__ bool wait_set(const volatile int* p, unsigned long long limit_ns) {
   if (*p) return true;
   unsigned long long t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   unsigned ns = 64;
   while (!*p) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 20000000000ull) return false;
+    if (t - t0 > limit_ns) return false;
     __nanosleep(ns);
     if (ns < 4096) ns <<= 1;
   }
@@ -626,7 +626,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
       }
       int ok = 1;
       if (lane == 0) {
-        ok = wait_set(gate.ready + k);
+        ok = wait_set(gate.ready + k, gate.timeout_ns);
         if (!ok) atomicExch(gate.timed_out, 1u);
       }
       if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return;

@@ -257,18 +257,22 @@ int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
              int* d_passes, cudaStream_t st, int first_pass) {
-  static int sms = 0, per_sm = 0;
   const size_t smem = (size_t)kCgWarps * (g.nsp / 32) * sizeof(uint32_t);
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // occupancy per (device, smem size)
+  constexpr int kDevs = 64;
+  static int sms_d[kDevs] = {}, per_sm_d[kDevs] = {};
+  static size_t smem_d[kDevs];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) return DFX_E_CUDA;
+  if (!sms_d[dev]) {
+    cudaDeviceGetAttribute(&sms_d[dev], cudaDevAttrMultiProcessorCount, dev);
+    smem_d[dev] = (size_t)-1;
   }
-  static size_t last_smem = (size_t)-1;
-  if (smem != last_smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_solve_kernel, kCgWarps * 32, smem);
-    last_smem = smem;
+  if (smem != smem_d[dev]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d[dev], cg_solve_kernel, kCgWarps * 32, smem);
+    smem_d[dev] = smem;
   }
+  const int sms = sms_d[dev], per_sm = per_sm_d[dev];
   if (per_sm < 1) return DFX_E_LIMIT;
   int max_wave = 0;
   for (int w = 0; w < g.n_waves; w++) {

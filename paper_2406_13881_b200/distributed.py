@@ -368,7 +368,14 @@ class PeerSummaries:
         lst = np.zeros(self.g.init_list.shape, dtype=np.int16)
         ln = np.zeros(self.g.n_funcs, dtype=np.int32)
         out = CgOut(bits.ctypes.data, lst.ctypes.data, ln.ctypes.data, 0, 0, 0.0)
+        # the peer protocol (include/dfx.h): no rank may start solve k+1 (and
+        # write pass-1 rows into a peer's tables) before every rank has
+        # returned from solve k
+        if self.world > 1:
+            dist.barrier()
         self.eng.check(self.eng.lib.dfx_cgp_solve(self.eng.h, self.h, C.byref(out)), "dfx_cgp_solve")
+        if self.world > 1:
+            dist.barrier()
         self.kernel_ms = float(out.kernel_ms)
         return bits, lst, ln, int(out.passes)
 

@@ -125,3 +125,17 @@ def test_cuda_replay_many_chunks_and_wide_slot_masks():
     exp = run_replay(b2, runner=_oracle.replay_runner_mt)
     got = run_replay(b2)
     _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)
+
+
+@pytest.mark.gpu
+def test_gate_timeout_falls_back_to_the_ungated_replay(monkeypatch):
+    """if a range's region kernel cannot get an SM slot beside
+    the gated launch, the call replays the batch ungated instead of failing
+    (forced here with a zero wait budget)."""
+    from paper_2406_13881_b200.batch import C4Config, c4_generate
+    from paper_2406_13881_b200.dataflow import run_replay
+    b, _ = c4_generate(C4Config(), np.arange(600))
+    exp = run_replay(b, runner=_oracle.replay_runner_mt)
+    monkeypatch.setenv("DFX_GATE_TIMEOUT_MS", "0")
+    got = run_replay(b)
+    _golden.assert_raw_equal(got.events, got.var_out, exp.events, exp.var_out)

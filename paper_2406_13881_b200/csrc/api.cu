@@ -573,6 +573,33 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     }
   }
   CK(cudaEventRecord(h->ev1, st));
+  // a range's region kernel never got an SM slot beside the gated launch
+  // (e.g. another process holds the GPU), so its items gave up waiting:
+  // replay the batch again, ungated, through the device-resident path
+  //
+  auto ungated = [&]() -> int {
+    if (h->trace) fprintf(stderr, "dfx_replay_batch: gate timed out; replaying ungated\n");
+    for (cudaStream_t sr : s_regs) cudaStreamSynchronize(sr);
+    cudaStreamSynchronize(h->s_copy);
+    cudaStreamSynchronize(st);
+    dfx_replay* rp = nullptr;
+    int rc = dfx_replay_create(h, in, out->event_cap > 0 ? out->event_cap : 1, &rp);
+    if (rc) return rc;
+    int64_t n_ev = 0;
+    float kms = 0.f;
+    rc = dfx_replay_run(h, rp, &n_ev, &kms);
+    if (rc == DFX_OK || rc == DFX_E_NOSPC) {
+      const int rc2 = dfx_replay_fetch(h, rp, out);
+      if (rc == DFX_OK) rc = rc2;
+      out->kernel_ms = kms;
+    }
+    dfx_replay_destroy(h, rp);
+    return rc;
+  };
+  auto gate_timed_out = [&]() -> bool {
+    int t = 0;
+    return cudaMemcpy(&t, g_timeout, sizeof t, cudaMemcpyDeviceToHost) == cudaSuccess && t != 0;
+  };
   // range k's events go home as soon as its last item is done
   const auto t_call = std::chrono::steady_clock::now();
   std::vector<double> t_done(K, 0.0);
@@ -587,7 +614,10 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       }
       if (*hd == 0ull) {
         CK(cudaEventSynchronize(h->ev1));
-        if (*hd == 0ull) return fail(DFX_E_CUDA, "dfx_replay_batch: range %d did not complete", k);
+        if (*hd == 0ull) {
+          if (gate_timed_out()) return ungated();
+          return fail(DFX_E_CUDA, "dfx_replay_batch: range %d did not complete", k);
+        }
       }
     }
     t_done[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
@@ -606,27 +636,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   {
     int timed_out = 0;
     CK(cudaMemcpy(&timed_out, g_timeout, sizeof timed_out, cudaMemcpyDeviceToHost));
-    if (timed_out) {
-      // a range's region kernel never got an SM slot beside the gated launch
-      // (e.g. another process holds the GPU): replay the batch again,
-      // ungated, through the device-resident path
-      if (h->trace) fprintf(stderr, "dfx_replay_batch: gate timed out; replaying ungated\n");
-      for (cudaStream_t sr : s_regs) cudaStreamSynchronize(sr);
-      cudaStreamSynchronize(h->s_copy);
-      dfx_replay* rp = nullptr;
-      int rc = dfx_replay_create(h, in, out->event_cap > 0 ? out->event_cap : 1, &rp);
-      if (rc) return rc;
-      int64_t n_ev = 0;
-      float kms = 0.f;
-      rc = dfx_replay_run(h, rp, &n_ev, &kms);
-      if (rc == DFX_OK || rc == DFX_E_NOSPC) {
-        const int rc2 = dfx_replay_fetch(h, rp, out);
-        if (rc == DFX_OK) rc = rc2;
-        out->kernel_ms = kms;
-      }
-      dfx_replay_destroy(h, rp);
-      return rc;
-    }
+    if (timed_out) return ungated();
   }
   if (!redo.empty() && (int64_t)count <= cap) {
     for (int k : redo) {

@@ -397,6 +397,80 @@ int dfx_cgp_connect(dfx_handle *h, dfx_cgp *p, const void *ipc_handles);
 int dfx_cgp_solve(dfx_handle *h, dfx_cgp *p, dfx_cg_out *out);
 int dfx_cgp_destroy(dfx_handle *h, dfx_cgp *p);
 
+/* ------------------------------------------------------------------------ */
+/* Transfer simulator: batched replacement of                 */
+/* dartomp.simulator.simulate (simulator.py:180-708)                         */
+/* ------------------------------------------------------------------------ */
+/* A program is the simulator's walk of one translation unit with its
+ * control (concrete scalar values, if decisions, trip counts, returns, call
+ * inlining and aliases) resolved by the host lowering
+ * (paper_2406_13881_b200/simlower.py), leaving the per-variable state
+ * machine (ref count, host-valid, device-valid) to the device: one warp per
+ * (program, 32-variable chunk), one lane per resolved variable.  Ops are
+ * int32 x4 (code | flags << 8, var, a, b) plus one int64 argument each
+ * (bytes per transfer, loop trip count):
+ *   READ var space site | WRITE var space | ENTER var maptype [bytes] |
+ *   EXIT var maptype warn [bytes] | UPDATE var dir warn [bytes] |
+ *   SHIELD_SAVE / SHIELD_SET / UNSHIELD var |
+ *   CHECK_BEGIN extent chunkmask | CHECK_END (untaken if-arm: its stale
+ *   reads count, its state and transfers roll back) |
+ *   LOOP extent chunkmask nvariants [trip] { VAR_BEGIN extent (F_RET)
+ *   ... VAR_END back } x nvariants (round r runs variant min(r, n)) | END
+ * Loops iterate per variable until that variable's state repeats under the
+ * steady variant; the rest of the trip count is then accounted by one more
+ * round counted trip - r times (simulator.py:528-550, `_scale_tail`). */
+enum {
+  DFX_SIM_END = 0, DFX_SIM_READ = 1, DFX_SIM_WRITE = 2, DFX_SIM_ENTER = 3,
+  DFX_SIM_EXIT = 4, DFX_SIM_UPDATE = 5, DFX_SIM_SHIELD_SAVE = 6, DFX_SIM_SHIELD_SET = 7,
+  DFX_SIM_UNSHIELD = 8, DFX_SIM_CHECK_BEGIN = 9, DFX_SIM_CHECK_END = 10, DFX_SIM_LOOP = 11,
+  DFX_SIM_VAR_BEGIN = 12, DFX_SIM_VAR_END = 13,
+  DFX_SIM_WARN = 14             /* control warning (call depth, unknown clause
+                                   variable): host-side text, no device effect */
+};
+#define DFX_SIM_F_RET (1 << 8)
+#define DFX_SIM_MAX_NEST 16          /* loops + untaken arms nested */
+#define DFX_SIM_MAX_ROUNDS 10000     /* simulator.py _MAX_CONCRETE_ROUNDS */
+
+typedef struct {
+  int32_t op_off, n_ops;        /* into ops (units of 4 int32) and arg64 */
+  int32_t var_off, n_vars;      /* into the per-variable outputs */
+} dfx_sim_prog;
+
+typedef struct {
+  int32_t n_progs;
+  const dfx_sim_prog *progs;
+  const int32_t *ops;           /* [n_ops * 4] */
+  const int64_t *arg64;         /* [n_ops] */
+  int64_t n_ops, n_vars;
+} dfx_sim_in;
+
+/* per-variable result: transfer totals, stale reads, final state */
+typedef struct {
+  uint64_t htod_calls, htod_bytes, dtoh_calls, dtoh_bytes, stale;
+  int64_t ref;
+  uint8_t host_valid, device_valid, flags, pad[5];
+} dfx_sim_var;
+#define DFX_SIM_VF_OVERFLOW 1        /* a count exceeded 64 bits */
+#define DFX_SIM_VF_FAULT 2           /* shield stack / malformed program */
+
+/* records: stale reads (id = site, count), warnings (id = warn id) */
+enum { DFX_SIM_REC_STALE = 0, DFX_SIM_REC_WARN = 1, DFX_SIM_REC_NOSETTLE = 2 };
+typedef struct {
+  int32_t prog, var, id, kind;
+  uint64_t count;
+} dfx_sim_rec;
+
+typedef struct {
+  dfx_sim_var *vars;            /* [n_vars] */
+  dfx_sim_rec *recs;            /* capacity rec_cap */
+  int64_t rec_cap;
+  int64_t n_recs;               /* out (may exceed rec_cap -> DFX_E_NOSPC) */
+  float kernel_ms;
+} dfx_sim_out;
+
+/* host buffers in and out */
+int dfx_sim_batch(dfx_handle *h, const dfx_sim_in *in, dfx_sim_out *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1840,4 +1840,74 @@ int dfx_summaries_sharded(dfx_handle* h, const dfx_cg_in* in, const int32_t* own
   return DFX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// transfer simulator (sim.cu): replaces dartomp.simulator.simulate
+// (simulator.py:180-708) for a batch of lowered programs
+// ---------------------------------------------------------------------------
+int dfx_sim_batch(dfx_handle* h, const dfx_sim_in* in, dfx_sim_out* out) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_sim_batch: null argument");
+  if (in->n_progs < 0 || in->n_ops < 0 || in->n_vars < 0 || in->n_ops > INT32_MAX ||
+      in->n_vars > INT32_MAX)
+    return fail(DFX_E_ARG, "dfx_sim_batch: bad sizes");
+  if (in->n_progs && (!in->progs || !in->ops || !in->arg64))
+    return fail(DFX_E_ARG, "dfx_sim_batch: null input array");
+  if (in->n_vars && !out->vars) return fail(DFX_E_ARG, "dfx_sim_batch: null vars output");
+  std::vector<int32_t> item_prog, item_chunk;
+  for (int i = 0; i < in->n_progs; i++) {
+    const dfx_sim_prog& p = in->progs[i];
+    if (p.op_off < 0 || p.n_ops < 1 || (int64_t)p.op_off + p.n_ops > in->n_ops || p.var_off < 0 ||
+        p.n_vars < 0 || (int64_t)p.var_off + p.n_vars > in->n_vars)
+      return fail(DFX_E_ARG, "dfx_sim_batch: program %d out of range", i);
+    for (int c = 0; c < (p.n_vars + 31) / 32; c++) {
+      item_prog.push_back(i);
+      item_chunk.push_back(c);
+    }
+  }
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->st();
+  const int n_items = (int)item_prog.size();
+  const int64_t cap = out->rec_cap > 0 ? out->rec_cap : 0;
+  auto* d_progs = (dfx_sim_prog*)dbuf(h, "sim_progs", sizeof(dfx_sim_prog) * in->n_progs + 16);
+  auto* d_ops = (int32_t*)dbuf(h, "sim_ops", sizeof(int32_t) * 4 * in->n_ops + 16);
+  auto* d_arg = (int64_t*)dbuf(h, "sim_arg", sizeof(int64_t) * in->n_ops + 16);
+  auto* d_items = (int32_t*)dbuf(h, "sim_items", sizeof(int32_t) * 2 * (size_t)n_items + 16);
+  auto* d_vars = (dfx_sim_var*)dbuf(h, "sim_vars", sizeof(dfx_sim_var) * in->n_vars + 16);
+  auto* d_recs = (dfx_sim_rec*)dbuf(h, "sim_recs", sizeof(dfx_sim_rec) * cap + 16);
+  auto* d_ctr = (unsigned long long*)dbuf(h, "sim_ctr", 64);
+  if (!d_progs || !d_ops || !d_arg || !d_items || !d_vars || !d_recs || !d_ctr)
+    return fail(DFX_E_CUDA, "dfx_sim_batch: allocation failed");
+  if (in->n_progs) {
+    CK(cudaMemcpyAsync(d_progs, in->progs, sizeof(dfx_sim_prog) * in->n_progs, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_ops, in->ops, sizeof(int32_t) * 4 * in->n_ops, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_arg, in->arg64, sizeof(int64_t) * in->n_ops, cudaMemcpyHostToDevice, st));
+  }
+  if (n_items) {
+    CK(cudaMemcpyAsync(d_items, item_prog.data(), sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_items + n_items, item_chunk.data(), sizeof(int32_t) * n_items,
+                       cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(d_ctr, 0, 64, st));
+  dfx::SimDev s;
+  s.progs = d_progs; s.ops = d_ops; s.arg64 = d_arg;
+  s.item_prog = d_items; s.item_chunk = d_items + n_items; s.n_items = n_items;
+  s.vars = d_vars; s.recs = d_recs; s.rec_cap = cap;
+  s.rec_count = d_ctr; s.next = reinterpret_cast<unsigned*>(d_ctr + 1);
+  CK(cudaEventRecord(h->ev0, st));
+  int rc = dfx::sim_launch(s, st);
+  CK(cudaEventRecord(h->ev1, st));
+  if (rc) return fail(rc, "sim_launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  unsigned long long nrec = 0;
+  CK(cudaMemcpyAsync(&nrec, d_ctr, sizeof nrec, cudaMemcpyDeviceToHost, st));
+  if (in->n_vars)
+    CK(cudaMemcpyAsync(out->vars, d_vars, sizeof(dfx_sim_var) * in->n_vars, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out->n_recs = (int64_t)nrec;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  out->kernel_ms = ms;
+  if ((int64_t)nrec > cap) return fail(DFX_E_NOSPC, "dfx_sim_batch: %llu records, capacity %lld", nrec, (long long)cap);
+  if (nrec) CK(cudaMemcpy(out->recs, d_recs, sizeof(dfx_sim_rec) * nrec, cudaMemcpyDeviceToHost));
+  return DFX_OK;
+}
+
 }  // extern "C"

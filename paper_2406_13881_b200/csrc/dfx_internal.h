@@ -169,3 +169,23 @@ int cg_pack(uint8_t* b, int16_t* l, int32_t* n, int nsp, const int32_t* fns, int
             uint8_t* out, int rowb, bool unpack, cudaStream_t st);
 
 }  // namespace dfx
+
+namespace dfx {
+
+// transfer simulator (sim.cu): one persistent launch over (program, chunk) items
+struct SimDev {
+  const dfx_sim_prog* progs;
+  const int32_t* ops;
+  const int64_t* arg64;
+  const int32_t* item_prog;
+  const int32_t* item_chunk;
+  int n_items;
+  dfx_sim_var* vars;
+  dfx_sim_rec* recs;
+  int64_t rec_cap;
+  unsigned long long* rec_count;
+  unsigned* next;
+};
+int sim_launch(const SimDev& s, cudaStream_t stream);
+
+}  // namespace dfx

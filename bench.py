@@ -67,6 +67,10 @@ def parse_args():
                     help="skip the post-run parity check of the timed outputs")
     ap.add_argument("--c4-ref-funcs", type=int, default=1000,
                     help="functions in the reference C4 CPU-baseline sample")
+    ap.add_argument("--no-sim", action="store_true",
+                    help="skip the transfer-simulator (verifier) sub-record")
+    ap.add_argument("--sim-funcs", type=int, default=256,
+                    help="C4 source functions in the simulator (verifier) record")
     return ap.parse_args()
 
 
@@ -429,6 +433,9 @@ def run_ours(args, rank, world, local):
     c5 = None
     if not args.no_c5:
         c5 = run_c5(args, rank, world, local)
+    sim = None
+    if not args.no_sim and world == 1:
+        sim = run_sim_record(args)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -464,7 +471,81 @@ def run_ours(args, rank, world, local):
         line["c4"] = c4
     if c5 is not None:
         line["c5"] = c5
+    if sim is not None:
+        line["sim"] = sim
     print(json.dumps(line), flush=True)
+
+
+def run_sim_record(args):
+    """Transfer simulator as a batched verifier: C4 source
+    functions, transformed (annotated mode) and original (implicit mode),
+    simulated in ONE `dfx_sim_batch` launch; beside it the reference
+    `simulate` (simulator.py:708) on the same programs in a process pool.
+    Host preparation (parse, transform) is untimed; the host lowering is
+    timed and reported.  Parity: every program's totals, aggregated stale
+    reads, warnings and final reference counts equal the reference's."""
+    import multiprocessing as mp
+    from paper_2406_13881_b200._host import have_dartomp
+    if not have_dartomp():
+        return {"unavailable": "host front end (dartomp) not importable"}
+    sys.path.insert(0, str(ROOT / "scripts"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import sim_worker  # noqa: E402
+    import _sim  # noqa: E402  (aggregate view of a SimReport, for the parity check)
+    from paper_2406_13881_b200.simulator import _report, run_sim
+    procs = len(os.sched_getaffinity(0))
+    n = args.sim_funcs
+    jobs = [(k * (100_000 // max(1, n)), mode) for k in range(n) for mode in ("annotated", "implicit")]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(procs) as pool:
+        rows = pool.map(sim_worker.one, jobs, chunksize=2)
+    prep_wall = time.perf_counter() - t0
+    progs = [r[1] for r in rows]
+    lower_cpu = sum(r[3] for r in rows)
+    ref_cpu = sum(r[4] for r in rows)
+    for _ in range(3):
+        raw = run_sim(progs)
+    ks, es = [], []
+    for _ in range(max(3, min(args.steps, 10))):
+        t1 = time.perf_counter()
+        raw = run_sim(progs)
+        es.append(time.perf_counter() - t1)
+        ks.append(raw.kernel_ms)
+    # parity, program by program
+    import numpy as np
+    order = np.argsort(raw.recs["prog"], kind="stable")
+    recs = raw.recs[order]
+    bounds = np.searchsorted(recs["prog"], np.arange(len(progs) + 1))
+    bad, stale_ann, var_off = 0, 0, 0
+    for i, (p, row) in enumerate(zip(progs, rows)):
+        rep = _report(p, raw.vars[var_off:var_off + p.n_vars], recs[bounds[i]:bounds[i + 1]])
+        var_off += p.n_vars
+        bad += _sim.aggregate_fields(rep) != row[2]
+        if p.mode == "annotated":
+            stale_ann += rep.log.stale_count
+    nprog = len(progs)
+    kms, ems = statistics.median(ks), 1e3 * statistics.median(es)
+    ops = int(sum(p.ops.shape[0] for p in progs))
+    return {"workload": "C4 source functions (gen/c4src.py, every %d-th of 100k): %d transformed "
+                        "(annotated) + %d original (implicit) programs" % (100_000 // max(1, n), n, n),
+            "unit": "programs simulated/s", "programs": nprog, "ops": ops,
+            "vars": int(sum(p.n_vars for p in progs)),
+            "value": nprog / (kms / 1e3), "kernel_ms": kms,
+            "e2e": {"value": nprog / (ems / 1e3), "ms": ems,
+                    "path": "dfx_sim_batch with host buffers (H2D programs, kernel, D2H per-variable "
+                            "totals + records)"},
+            "host_lowering": {"cpu_s": lower_cpu, "programs_per_s_per_core": nprog / lower_cpu},
+            "parity": {"status": "ok" if bad == 0 else "MISMATCH", "mismatched_programs": bad,
+                       "checked": "every program: totals, stale reads per (line, var, space), "
+                                  "warnings, final ref counts == reference simulate"},
+            "stale_reads_in_transformed_programs": int(stale_ann),
+            "cpu_baseline": {"value": nprog / (ref_cpu / procs), "unit": "programs simulated/s",
+                             "cores": procs, "kind": "reference",
+                             "sample": "reference dartomp simulate (simulator.py:708) on the same "
+                                       "%d programs, multiprocessing.Pool(%d), parse excluded; "
+                                       "aggregate = programs / (CPU seconds / cores)" % (nprog, procs),
+                             "cpu_s": ref_cpu, **host_info()},
+            "prep_wall_s": prep_wall}
 
 
 def host_info() -> dict:

@@ -71,6 +71,10 @@ def parse_args():
                     help="skip the transfer-simulator (verifier) sub-record")
     ap.add_argument("--sim-funcs", type=int, default=256,
                     help="C4 source functions in the simulator (verifier) record")
+    ap.add_argument("--no-emit", action="store_true",
+                    help="skip the batched-emission sub-record")
+    ap.add_argument("--emit-units", type=int, default=48,
+                    help="C4 source translation units in the batched-emission record")
     return ap.parse_args()
 
 
@@ -436,6 +440,9 @@ def run_ours(args, rank, world, local):
     sim = None
     if not args.no_sim and world == 1:
         sim = run_sim_record(args)
+    emit_rec = None
+    if not args.no_emit and world == 1:
+        emit_rec = run_emit_record(args)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -473,7 +480,66 @@ def run_ours(args, rank, world, local):
         line["c5"] = c5
     if sim is not None:
         line["sim"] = sim
+    if emit_rec is not None:
+        line["emit"] = emit_rec
     print(json.dumps(line), flush=True)
+
+
+def run_emit_record(args):
+    """Batched emission: C4 source translation units, planned
+    by the drop-in (E1), then rewritten text + report lines by the native
+    emitter in one call (`dfx_emit_batch`) beside the reference's
+    `rewriter.apply_plans` + `report.plan_lines` on the same plans; outputs
+    compared byte for byte."""
+    from paper_2406_13881_b200._host import have_dartomp
+    if not have_dartomp():
+        return {"unavailable": "host front end (dartomp) not importable"}
+    from dartomp.report import plan_lines as ref_lines
+    from dartomp.rewriter import apply_plans as ref_apply
+    from paper_2406_13881_b200 import emit, pipeline
+    from paper_2406_13881_b200.gen.c4src import C4SourceConfig, c4_source
+    n = args.emit_units
+    units = []
+    for k in range(n):
+        a = pipeline.load(text=c4_source(C4SourceConfig(), k * (100_000 // max(1, n))))
+        units.append((a.src, pipeline.plan_transform(a)))
+
+    def ref_all():
+        out = []
+        for src, plans in units:
+            r = ref_apply(src, plans)
+            try:
+                ln = ref_lines(src, plans)
+            except KeyError as e:
+                ln = e
+            out.append((r.text, ln))
+        return out
+
+    def nat_all():
+        return [(r.text, ln) for r, ln in emit.emit_batch([(s, p, None) for s, p in units])]
+
+    def timed(fn, reps=5):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts), out
+    tr, ro = timed(ref_all, 3)
+    tn, no = timed(nat_all)
+    same = all(a[0] == b[0] and (a[1] == b[1] or (isinstance(a[1], KeyError) and isinstance(b[1], KeyError)))
+               for a, b in zip(ro, no))
+    plans = sum(len(p.all_plans) for _, ps in units for p in ps)
+    chars = sum(len(s.text) for s, _ in units)
+    return {"workload": "%d C4 source translation units (gen/c4src.py, every %d-th of 100k): "
+                        "%d plans, %d source characters" % (n, 100_000 // max(1, n), plans, chars),
+            "unit": "translation units emitted/s (rewritten text + report lines)",
+            "value": n / tn, "ms": 1e3 * tn,
+            "reference": {"value": n / tr, "ms": 1e3 * tr, "cores": 1,
+                          "what": "dartomp rewriter.apply_plans + report.plan_lines, same plans"},
+            "identical": same,
+            "path": "emit.emit_batch -> dfx_emit_batch (csrc/emit.cpp), one native call"}
 
 
 def run_sim_record(args):

@@ -471,6 +471,54 @@ typedef struct {
 /* host buffers in and out */
 int dfx_sim_batch(dfx_handle *h, const dfx_sim_in *in, dfx_sim_out *out);
 
+/* ------------------------------------------------------------------------ */
+/* Batched emission: rewriter.apply_plans (rewriter.py:255)  */
+/* and report.plan_lines (report.py:13) for many translation units          */
+/* ------------------------------------------------------------------------ */
+/* Host code, no device.  Text is UTF-32 (code point offsets = the
+ * reference's string indices).  Plans: int32 x6 (function, class 0 update /
+ * 1 kernel clause, kind, position DFX_POS_*, kernel group, 0) and int64 x3
+ * (anchor start, anchor end, loop-body closing brace or -1).  Update kinds
+ * DFX_EMIT_TO / DFX_EMIT_FROM; kernel-clause kinds 0 map(to) 1 map(tofrom)
+ * 2 map(from) 3 map(alloc) 4 firstprivate.  Strings (names, clause texts,
+ * function names) are ids into one string pool. */
+#define DFX_EMIT_TO 0
+#define DFX_EMIT_FROM 1
+#define DFX_EMIT_REPORT 1        /* flags: also produce the report lines */
+#define DFX_EMIT_AFTER_LINES 2   /* flags: report AFTER updates ("after line N")
+                                    instead of failing like report.py:35 */
+enum { DFX_EMIT_ERR_BRACES = 1, DFX_EMIT_ERR_CLASH = 2, DFX_EMIT_ERR_POSITION = 3 };
+
+typedef struct {
+  int32_t n_units;
+  const uint32_t *text; const int64_t *text_off;          /* [n_units+1] */
+  const int32_t *unit_len;                                 /* indent unit length, -1: detect */
+  const uint32_t *unit_text; const int64_t *unit_off;
+  int32_t n_fns;
+  const int32_t *fn_unit;                                  /* [n_fns] */
+  const int64_t *fn_region;                                /* [n_fns*2] begin start, end end; -1 */
+  const int32_t *fn_clause;                                /* [n_fns] region clause text (string id) */
+  const int32_t *fn_name;                                  /* [n_fns] function name (string id) */
+  const int64_t *fn_supp_off; const int32_t *supp_idx;     /* suppressed names */
+  int32_t n_plans;
+  const int32_t *plan;                                     /* [n_plans*6] */
+  const int64_t *plan_pos;                                 /* [n_plans*3] */
+  const int64_t *plan_names_off; const int32_t *name_idx;  /* names (string ids) */
+  const int64_t *str_off; const uint32_t *strpool;         /* string pool */
+  int32_t flags;
+} dfx_emit_in;
+
+typedef struct {
+  uint32_t *text; int64_t text_cap; int64_t *text_off;     /* rewritten texts [n_units+1] */
+  int64_t *ins; int64_t ins_cap; int64_t *ins_off;         /* placed (start, length) pairs */
+  uint32_t *report; int64_t report_cap; int64_t *report_off;   /* report lines, '\n'-ended */
+  int32_t *err_kind; int64_t *err_offset;                  /* [n_units] rewriter errors */
+  int32_t *report_err;                                     /* [n_units] 1: AFTER update (KeyError) */
+  int64_t text_need, ins_need, report_need;                /* out: sizes (DFX_E_NOSPC) */
+} dfx_emit_out;
+
+int dfx_emit_batch(const dfx_emit_in *in, dfx_emit_out *out);
+
 #ifdef __cplusplus
 }
 #endif

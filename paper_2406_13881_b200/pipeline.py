@@ -23,10 +23,10 @@ from dartomp.parser import parse  # noqa: E402
 from dartomp.diagnostics import PreconditionError  # noqa: E402
 from dartomp.omp import DATA_MAPPING_KINDS  # noqa: E402
 from dartomp.pipeline import Analysis, check_transform_preconditions  # noqa: E402
-from dartomp.rewriter import apply_plans  # noqa: E402
 from dartomp.source import SourceFile  # noqa: E402
 
 from .dataflow import analyze_function, analyze_functions  # noqa: E402
+from .emit import apply_plans, plan_lines  # noqa: E402
 from .lower import premapped_directive  # noqa: E402
 from .interproc import apply_call_effects, summarize_all  # noqa: E402
 
@@ -108,22 +108,38 @@ def plan_transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset()
 
 def transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset(),
               indent_unit: str | None = None, replay_runner=None):
-    """`dartomp.pipeline.transform` (`pipeline.py:99-105`)."""
+    """`dartomp.pipeline.transform` (`pipeline.py:99-105`): plans from one E1
+    launch, text from the native emitter (`emit.py`, byte-identical to
+    `rewriter.apply_plans`)."""
     plans = plan_transform(analysis, allow_stale, replay_runner=replay_runner)
     result = apply_plans(analysis.src, plans, indent_unit=indent_unit)
     return result, plans
 
 
 def install() -> None:
-    """Route an imported `dartomp` through the engine (plugin drop-in)."""
+    """Route an imported `dartomp` through the engine (plugin drop-in): the
+    analysis (E1), the summaries (kernel c), the emitter (native), and the
+    CLI's `compare` (the CUDA transfer simulator; its comparison lines are the
+    reference's byte for byte).  `simulate_analysis` (the CLI's `simulate`
+    mode, whose verbose log lists the reference's per-round records) stays the
+    reference's."""
     import dartomp.cli as cli
     import dartomp.dataflow as df
     import dartomp.interproc as ip
     import dartomp.pipeline as pl
+    import dartomp.report as rp
+    import dartomp.rewriter as rw
+    from .simulator import compare
     df.analyze_function = analyze_function
     ip.summarize_all = summarize_all
     pl.analyze_function = analyze_function
     pl.summarize_all = summarize_all
     pl.plan_transform = plan_transform
     pl.transform = transform
+    pl.apply_plans = apply_plans
+    pl.compare = compare
+    rw.apply_plans = apply_plans
+    rp.plan_lines = plan_lines
     cli.transform = transform
+    cli.plan_lines = plan_lines
+    cli.compare = compare

@@ -102,12 +102,12 @@ U32 detect_unit(const Src& s) {
   return U32((size_t)best.first, U' ');
 }
 
-struct Ins {
+struct Ins {            // an insertion; its text is arena[a, a + len)
   int64_t offset;
   int prio;
   int64_t seq;
   int64_t order;
-  U32 text;
+  int64_t a, len;
 };
 enum { kOpen = 0, kUpdate = 1, kClause = 2, kReindent = 3, kClose = 4 };
 
@@ -157,13 +157,21 @@ extern "C" int dfx_emit_batch(const dfx_emit_in* in, dfx_emit_out* out) {
                    ? U32(in->unit_text + in->unit_off[u], in->unit_text + in->unit_off[u] + in->unit_len[u])
                    : detect_unit(s);
     std::vector<Ins> ins;
+    U32 arena;
+    arena.reserve(1 << 12);
+    const int64_t unit_a = 0, unit_n = (int64_t)unit.size();
+    arena += unit;                 // the reindent pad, shared by every covered line
     int64_t order = 0;
     U32 err_msg;
     for (int32_t f : unit_fns[u]) {
       if (out->err_kind[u]) break;
       int64_t seq = 0;
-      auto add = [&](int64_t off, int prio, U32 text) {
-        ins.push_back(Ins{off, prio, seq++, order++, std::move(text)});
+      auto add = [&](int64_t off, int prio, const U32& text) {
+        ins.push_back(Ins{off, prio, seq++, order++, (int64_t)arena.size(), (int64_t)text.size()});
+        arena += text;
+      };
+      auto add_unit = [&](int64_t off, int prio) {
+        ins.push_back(Ins{off, prio, seq++, order++, unit_a, unit_n});
       };
       const int64_t rb = in->fn_region[2 * f], re = in->fn_region[2 * f + 1];
       int64_t first_line = -1, last_line = -1;
@@ -185,7 +193,7 @@ extern "C" int dfx_emit_batch(const dfx_emit_in* in, dfx_emit_out* out) {
         int64_t off = begin_off;
         while (off <= last_line) {
           const int64_t end = s.line_end(off);
-          if (!s.blank(off, end)) add(off, kReindent, unit);
+          if (!s.blank(off, end)) add_unit(off, kReindent);
           if (end <= off) break;
           off = end;
         }
@@ -370,14 +378,21 @@ extern "C" int dfx_emit_batch(const dfx_emit_in* in, dfx_emit_out* out) {
         return std::tie(a.offset, a.prio, a.seq, a.order) < std::tie(b.offset, b.prio, b.seq, b.order);
       });
       U32 o;
+      int64_t extra = 0;
+      for (const Ins& x : ins) extra += x.len;
+      o.resize((size_t)(s.n + extra));
+      char32_t* w = &o[0];
       int64_t pos = 0;
+      placed[u].reserve(ins.size());
       for (const Ins& x : ins) {
-        o.append(s.t + pos, s.t + x.offset);
-        placed[u].push_back({(int64_t)o.size(), (int64_t)x.text.size()});
-        o += x.text;
+        std::memcpy(w, s.t + pos, sizeof(char32_t) * (size_t)(x.offset - pos));
+        w += x.offset - pos;
+        placed[u].push_back({(int64_t)(w - &o[0]), x.len});
+        std::memcpy(w, arena.data() + x.a, sizeof(char32_t) * (size_t)x.len);
+        w += x.len;
         pos = x.offset;
       }
-      o.append(s.t + pos, s.t + s.n);
+      std::memcpy(w, s.t + pos, sizeof(char32_t) * (size_t)(s.n - pos));
       texts[u] = std::move(o);
     }
     reports[u] = std::move(rep);

@@ -55,6 +55,23 @@ class EmitOut(C.Structure):
                 ("text_need", C.c_int64), ("ins_need", C.c_int64), ("report_need", C.c_int64)]
 
 
+class _Rewrite(RewriteResult):
+    """`RewriteResult` whose `placed` list is built on first use from the
+    native (start, length) pairs."""
+
+    def __init__(self, original: str, text: str, ins: np.ndarray):
+        self.original = original
+        self.text = text
+        self._ins = ins
+
+    def __getattr__(self, name):
+        if name == "placed":
+            t = self.text
+            self.placed = [(s0, t[s0:s0 + n]) for s0, n in self._ins.tolist()]
+            return self.placed
+        raise AttributeError(name)
+
+
 def _u32(s: str) -> np.ndarray:
     return np.frombuffer(s.encode("utf-32-le"), dtype=np.uint32)
 
@@ -84,7 +101,11 @@ def emit_batch(units, report: bool = True, rewrite: bool = True, on_after: str =
     unit_len, unit_parts, unit_off = [], [], [0]
     fn_unit, fn_region, fn_clause, fn_name, supp_off, supp = [], [], [], [], [0], []
     plan, plan_pos, names_off, names = [], [], [0], []
-    plan_src = []                      # (unit, plan object) for error messages
+    plan_src = []                      # plan objects, for error messages
+    ids, items = strs.ids, strs.items
+    pos_get, kcl_get, upd_get = _POS.get, _KCL.get, _UPD.get
+    plan_app, pos_app, names_app, noff_app = plan.append, plan_pos.append, names.append, names_off.append
+    body_end, compound = _abi.POS_BODY_END, NodeKind.COMPOUND_STMT
     for u, (src, plans, indent_unit) in enumerate(units):
         t = _u32(src.text)
         text_parts.append(t)
@@ -115,24 +136,28 @@ def emit_batch(units, report: bool = True, rewrite: bool = True, on_after: str =
             for cls, lst in ((1, fp.kernel_clauses), (0, fp.updates)):
                 for p in lst:
                     a = p.anchor
-                    pos = _POS.get(p.position, 99)
-                    if cls == 1:
-                        kind = _KCL.get(p.kind, 4)
+                    sp = a.span
+                    pos = pos_get(p.position, 99)
+                    brace = -1
+                    if cls:
+                        kind = kcl_get(p.kind, 4)
                         grp = groups.setdefault(id(a), len(groups))
-                        brace = -1
                     else:
-                        kind = _UPD.get(p.kind, 0)
+                        kind = upd_get(p.kind, 0)
                         grp = 0
-                        brace = -1
-                        if pos == _abi.POS_BODY_END:
+                        if pos == body_end:
                             body = getattr(a, "body", None)
-                            if body is not None and body.kind is NodeKind.COMPOUND_STMT:
+                            if body is not None and body.kind is compound:
                                 brace = body.span.end - 1
-                    plan.append((f, cls, kind, pos, grp, 0))
-                    plan_pos.append((a.span.start, a.span.end, brace))
+                    plan_app((f, cls, kind, pos, grp, 0))
+                    pos_app((sp.start, sp.end, brace))
                     for nme in p.names:
-                        names.append(strs.id(nme))
-                    names_off.append(len(names))
+                        k = ids.get(nme)
+                        if k is None:
+                            k = ids[nme] = len(items)
+                            items.append(nme)
+                        names_app(k)
+                    noff_app(len(names))
                     plan_src.append(p)
     if not strs.items:
         strs.id("")
@@ -164,7 +189,14 @@ def emit_batch(units, report: bool = True, rewrite: bool = True, on_after: str =
     lib = _abi.load_lib()
     lib.dfx_emit_batch.restype = C.c_int
     nu = len(units)
-    caps = [arr["text"].shape[0] * 2 + 1024, 4096, 4096]
+    # capacities from the inputs (a retry after DFX_E_NOSPC reruns the whole
+    # emission): insertions <= covered lines + plans (+2 per region), report
+    # <= a line per plan / function with its names
+    n_lines = int(sum(src.text.count("\n") for src, _, _ in units)) + nu
+    name_chars = int(str_off[-1])
+    caps = [arr["text"].shape[0] + 64 * (len(plan) + 4 * len(fn_unit)) + name_chars * 4 + 1024,
+            n_lines + len(plan) + 2 * len(fn_unit) + 64,
+            96 * (len(plan) + 4 * len(fn_unit) + nu) + name_chars * 4 + 1024]
     while True:
         o = {"text": np.zeros(caps[0], np.uint32), "text_off": np.zeros(nu + 1, np.int64),
              "ins": np.zeros(2 * caps[1], np.int64), "ins_off": np.zeros(nu + 1, np.int64),
@@ -200,9 +232,7 @@ def emit_batch(units, report: bool = True, rewrite: bool = True, on_after: str =
                                 "kernel clause plan with position %r" % plan_src[k].position)
         else:
             i0, i1 = int(o["ins_off"][u]), int(o["ins_off"][u + 1])
-            ins = o["ins"][2 * i0:2 * i1].reshape(-1, 2).tolist()
-            res = RewriteResult(original=src.text, text=body,
-                                placed=[(s0, body[s0:s0 + n]) for s0, n in ins])
+            res = _Rewrite(src.text, body, o["ins"][2 * i0:2 * i1].reshape(-1, 2))
         if not report:
             lines = None
         elif int(o["report_err"][u]):

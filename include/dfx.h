@@ -111,8 +111,16 @@ typedef struct {
   int32_t site_off, arm_off;   /* into sites (int32) / arms (units of 2) */
   int32_t region_begin_start;  /* -1: function has no kernels */
   int32_t n_slots, max_loop_depth, max_br_depth, max_arms;
-  int32_t reserved[3];
+  int32_t flags;               /* DFX_FN_* (0: none) */
+  int32_t reserved[2];
 } dfx_fn_desc;
+
+/* dfx_fn_desc.flags.  DFX_FN_NO_ERR_SITES: no hoist-table entry and no arm
+ * anchor of the function can raise a braces error (the lowering knows this
+ * statically).  It lets the replay drop, per variable, the dry round of a
+ * loop that never writes the variable (exact: see replay.cu "dry-round lane
+ * skip"); without it every dry round is replayed in full. */
+#define DFX_FN_NO_ERR_SITES 1
 
 typedef struct {
   int32_t n_funcs;

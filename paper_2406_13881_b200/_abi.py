@@ -23,13 +23,13 @@ class FnDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "op_off", "n_ops", "var_off", "n_vars", "stmt_off", "n_stmts",
         "site_off", "arm_off", "region_begin_start", "n_slots",
-        "max_loop_depth", "max_br_depth", "max_arms")] + [("reserved", C.c_int32 * 3)]
+        "max_loop_depth", "max_br_depth", "max_arms", "flags")] + [("reserved", C.c_int32 * 2)]
 
 
 FN_DESC_DTYPE = np.dtype([(n, np.int32) for n in (
     "op_off", "n_ops", "var_off", "n_vars", "stmt_off", "n_stmts",
     "site_off", "arm_off", "region_begin_start", "n_slots",
-    "max_loop_depth", "max_br_depth", "max_arms", "r0", "r1", "r2")])
+    "max_loop_depth", "max_br_depth", "max_arms", "flags", "r1", "r2")])
 assert FN_DESC_DTYPE.itemsize == C.sizeof(FnDesc) == 64
 
 
@@ -69,6 +69,7 @@ EV_ERR_DATAMAP, EV_ERR_BRACES_LOOP, EV_ERR_BRACES_ARM, EV_ERR_DECL, EV_ERR_ENGIN
     16, 17, 18, 19, 20
 POS_BEFORE, POS_AFTER, POS_BODY_END, POS_KERNEL = 0, 1, 2, 3
 OUT_PRESENCE, OUT_TO, OUT_FROM, OUT_H, OUT_D = 1, 2, 4, 8, 16
+FN_NO_ERR_SITES = 1          # dfx_fn_desc.flags (include/dfx.h)
 
 DFX_OK, DFX_E_ARG, DFX_E_CUDA, DFX_E_NOSPC, DFX_E_LIMIT = 0, -1, -2, -3, -4
 

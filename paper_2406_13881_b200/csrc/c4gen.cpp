@@ -263,6 +263,7 @@ int dfx_gen_c4(uint64_t seed, const int32_t* fids, int32_t n, int32_t n_min, int
     d.max_loop_depth = g.max_loop;
     d.max_br_depth = g.max_br;
     d.max_arms = g.max_arms;
+    d.flags = DFX_FN_NO_ERR_SITES;   // no hoist code or arm carries a braces error
     std::memcpy(ops + 4 * off_o[i], g.ops.data(), g.ops.size() * sizeof(int32_t));
     for (int k = 0; k < V; k++) {
       int fl = g.scalar[k] ? DFX_V_SCALAR : 0;

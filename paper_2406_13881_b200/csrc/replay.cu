@@ -467,6 +467,29 @@ replay_one(int item, WarpCtl<M, P>& c, typename P::Prov* prov, int lane, const d
       }
       case DFX_OP_LOOP_BEGIN: {  // _loop_rounds: entry = state.copy(); dry round
         if (!(((uint32_t)op.z >> (chunk & 31)) & 1u)) goto skip_region;
+        // Dry round in closed form.  When the loop (body, condition, increment)
+        // writes none of this warp's variables, their ops in it are reads, and
+        // reads (and the reconciles they cause) only raise H/D bits and never
+        // touch provenance: the dry round's exit state is >= its entry state,
+        // so the weakened state merge_conj(entry, exit) (dataflow.py:572-574)
+        // IS the entry state, and the planning round replays the dry round
+        // from the same state with record on -- every dry-round side effect
+        // (presence, to_comp, from_comp, the plan log an enclosing loop's skip
+        // merge reads) recurs there, and a dry round records no events.  The
+        // dry round is then jumped: the visit counter advances by its dynamic
+        // length.  Exact under two conditions: no anchor of the function can
+        // raise a braces error (DFX_FN_NO_ERR_SITES, from the lowering: no
+        // error event of a skipped round is lost), and the loop does not hold
+        // a branch while its entry slot is captured by an enclosing if-arm
+        // (D4: that arm freezes at the dry round's first branch and is read
+        // after the loop).  Region table: end.z = written-chunk mask.
+        bool jump = false;
+        uint32_t ew = 0u;
+        if ((d.flags & DFX_FN_NO_ERR_SITES) && op.z != -1) {
+          const int2 e2 = __ldg(reinterpret_cast<const int2*>(&fops[pc + op.w].z));
+          ew = (uint32_t)e2.y;
+          jump = !(((uint32_t)e2.x >> (chunk & 31)) & 1u) && !((ew >> 31) && c.ref[cur] >= 2);
+        }
         if (lane == 0) {
           if (c.nlp >= P::kMaxLoop) c.fault = 1;
           else {
@@ -483,6 +506,11 @@ replay_one(int item, WarpCtl<M, P>& c, typename P::Prov* prov, int lane, const d
         copy_slot(c.bc0, cur);
         record = 0;
         __syncwarp();
+        if (jump) {   // to the LOOP_END of the dry round: one round = (dyn - 3) / 2 visits
+          sbase += (uint64_t)(((ew & 0x7FFFFFFFu) - 3u) >> 1) + 1u - (uint64_t)op.w;
+          pc += op.w;
+          continue;
+        }
         break;
       }
       case DFX_OP_LOOP_END: {
@@ -657,6 +685,8 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 //             static error op, nests deeper than the frame stack, or its
 //             dynamic length does not fit 31 bits (never skipped)
 //   begin.w = end pc - begin pc
+//   end.z   = (LOOP_END) written-chunk mask: bit (v >> 5) & 31 for every
+//             variable v with a HW/DW op inside the loop (the dry-round jump)
 //   end.w   = dynamic op count of one visit of the region, begin and end
 //             included: branch 2 + content, loop 3 + 2 x content (the dry
 //             round and the planning round, `_loop_rounds`, dataflow.py:566-590)
@@ -673,11 +703,11 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
   // the open region's accumulators live in registers; the stack (local
   // memory) holds the enclosing regions' and is touched only at BEGIN / END
   int32_t st_pc[kRegionStack + 1];
-  uint32_t st_mask[kRegionStack + 1];
+  uint32_t st_mask[kRegionStack + 1], st_wmask[kRegionStack + 1];
   int64_t st_dyn[kRegionStack + 1];
   bool st_br[kRegionStack + 1];
   int cpc = -1;          // begin pc of the open region (-1: the function body)
-  uint32_t cmask = 0u;
+  uint32_t cmask = 0u, cwmask = 0u;
   int64_t cdyn = 0;
   bool cbr = false;
   int sp = 0, deep = 0;  // sp: enclosing regions stacked; deep: beyond the stack (never skipped)
@@ -700,13 +730,14 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
     if (code == DFX_OP_END) break;
     if (code >= DFX_OP_HR && code <= DFX_OP_DW) {
       cmask |= 1u << ((op.y >> 5) & 31);
+      if (code == DFX_OP_HW || code == DFX_OP_DW) cwmask |= 1u << ((op.y >> 5) & 31);
       cdyn++;
     } else if (code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN) {
       o[pc].z = -1;          // until its end is seen
       if (deep || sp == kRegionStack) { deep++; cmask = ~0u; continue; }
-      st_pc[sp] = cpc; st_mask[sp] = cmask; st_dyn[sp] = cdyn; st_br[sp] = cbr;
+      st_pc[sp] = cpc; st_mask[sp] = cmask; st_wmask[sp] = cwmask; st_dyn[sp] = cdyn; st_br[sp] = cbr;
       sp++;
-      cpc = pc; cmask = 0u; cdyn = 0; cbr = code == DFX_OP_BR_BEGIN;
+      cpc = pc; cmask = 0u; cwmask = 0u; cdyn = 0; cbr = code == DFX_OP_BR_BEGIN;
     } else if (code == DFX_OP_BR_END || code == DFX_OP_LOOP_END) {
       if (deep) { deep--; continue; }
       if (sp == 0) continue; // unbalanced
@@ -717,10 +748,12 @@ region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int f
       if (dyn > 0x7FFFFFFF || loop == cbr) mask = ~0u;   // too long, or mismatched
       o[b].z = (int)mask;
       o[b].w = pc - b;
+      if (loop) o[pc].z = (int)cwmask;
       o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (cbr ? 0x80000000u : 0u));
       const bool br = cbr;
       sp--;
-      cpc = st_pc[sp]; cmask = st_mask[sp] | mask; cdyn = st_dyn[sp] + dyn; cbr = st_br[sp] | br;
+      cpc = st_pc[sp]; cmask = st_mask[sp] | mask; cwmask = st_wmask[sp] | cwmask;
+      cdyn = st_dyn[sp] + dyn; cbr = st_br[sp] | br;
     } else {
       if (code == DFX_OP_ERR) cmask = ~0u;
       cdyn++;

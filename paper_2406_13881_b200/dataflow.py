@@ -81,6 +81,7 @@ def pack(progs: list[FnProgram]) -> PackedBatch:
         d["max_loop_depth"] = p.max_loop_depth
         d["max_br_depth"] = p.max_br_depth
         d["max_arms"] = p.max_arms
+        d["flags"] = p.fn_flags
         op_off += p.ops.shape[0]
         var_off += p.var_flags.shape[0]
         stmt_off += p.stmt_span.shape[0]
@@ -243,9 +244,10 @@ def decode(prog: FnProgram, src, accesses, events: np.ndarray,
 
 
 def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
-                 var_out) -> FunctionPlan:
+                 var_out, presorted_unique: bool = False) -> FunctionPlan:
     """`decode` on the event columns as lists (key order); `events` (the same
-    events as a structured array) is read only to raise an error."""
+    events as a structured array) is read only to raise an error.
+    `presorted_unique`: repeated records were already dropped."""
     updates: list = []
     firstprivates: list = []
     suppressed: list[str] = []
@@ -256,7 +258,12 @@ def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
         keys: set = set()
         pstmts = prog.stmts
         names = [v.name for v in prog.vars]
+        # the batch path drops repeated (variable, node, kind, position)
+        # records before decoding (`_first_occurrences`), so the key set is
+        # needed only where two variables share a name (shadowing)
+        dedup = not presorted_unique or len(set(names)) != len(names)
         suppress, fp = _abi.EV_SUPPRESS, _abi.EV_FIRSTPRIVATE
+        new, DP = object.__new__, DirectivePlan
         for kind, vi, ni, pi in zip(kinds, vis, nis, pis):
             name = names[vi]
             if kind == suppress:
@@ -265,12 +272,21 @@ def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
                 continue
             # `_add_plan`'s key (`dataflow.py:264`): kind, name, anchor
             # identity (one statement per node index), position
-            key = (kind, name, ni, pi)
-            if key in keys:
-                continue
-            keys.add(key)
-            (firstprivates if kind == fp else updates).append(
-                DirectivePlan(_PLAN_KIND[kind], (name,), pstmts[ni], _POS[pi]))
+            if dedup:
+                key = (kind, name, ni, pi)
+                if key in keys:
+                    continue
+                keys.add(key)
+            # DirectivePlan(kind, (name,), anchor, position), built without
+            # the frozen dataclass's per-field object.__setattr__ (the same
+            # object: fields live in its __dict__; eq/hash read them)
+            plan = new(DP)
+            pd = plan.__dict__
+            pd["kind"] = _PLAN_KIND[kind]
+            pd["names"] = (name,)
+            pd["anchor"] = pstmts[ni]
+            pd["position"] = _POS[pi]
+            (firstprivates if kind == fp else updates).append(plan)
     # sets (`dataflow.py:214-216`) and `_escape_liveness` (`:671-676`)
     presence, to_comp, from_comp = set(), set(), set()
     for i, var in enumerate(prog.vars):
@@ -316,33 +332,12 @@ def _finish(prog, src, accesses, presence, to_comp, from_comp, updates,
             if names:
                 kernel_clauses.append(DirectivePlan(kind, tuple(names), k, KERNEL))
     elif presence or updates:
-        _check_region_scoping(src, accesses, begin, end)
+        if prog.scoping_error is not None:      # `_check_region_scoping` (`:713-734`)
+            raise DeclPlacementError.at(src, *prog.scoping_error)
         region = TargetDataRegion(block=block, begin=begin, end=end,
                                   map_to=tuple(to_only), map_from=tuple(from_only),
                                   map_tofrom=tuple(tofrom), map_alloc=tuple(alloc))
     return FunctionPlan(fn, region, kernel_clauses, updates, suppressed)
-
-
-def _check_region_scoping(src, accesses, begin, end) -> None:
-    """`_Analyzer._check_region_scoping` (`dataflow.py:713-734`)."""
-    lo = begin.span.start
-    hi = end.span.end
-    inside = {}
-    for acc in accesses:
-        d = acc.var.decl
-        if d is None or not (lo <= d.span.start < hi):
-            continue
-        if acc.ast.span.start >= hi and acc.ast is not d:
-            inside.setdefault(acc.var, acc)
-    for var, acc in sorted(inside.items(), key=lambda kv: kv[0].name):
-        raise DeclPlacementError.at(
-            src, var.decl.span.start,
-            "'%s' is declared at line %d inside the new data region "
-            "(lines %d..%d) but used at line %d after it; move the "
-            "declaration above the region" % (
-                var.name, src.line_of(var.decl.span.start),
-                src.line_of(lo), src.line_of(hi - 1),
-                src.line_of(acc.ast.span.start)))
 
 
 # ---- public API --------------------------------------------------------------
@@ -424,7 +419,8 @@ def _lower_portable(i: int):
         return ("serial", None)  # a reference not reachable this way: lower in the parent
     fields = {k: getattr(prog, k) for k in ("ops", "var_flags", "stmt_span", "sites", "arms",
                                             "region_begin_start", "n_slots", "max_loop_depth",
-                                            "max_br_depth", "max_arms")}
+                                            "max_br_depth", "max_arms", "fn_flags",
+                                            "scoping_error")}
     return ("ok", (fields, stmts, kstmts, region, vars_, premapped))
 
 
@@ -553,7 +549,7 @@ def _analyze_functions(items, allow_stale, runner, precheck) -> list[_Deferred]:
         vo = raw.var_out[var_off[i]:var_off[i] + n_vars[i]]
         try:
             out.append(_Deferred(plan=_decode_cols(p, src, accs, evs[a:b], kinds[a:b], vis[a:b],
-                                                   nis[a:b], pis[a:b], vo)))
+                                                   nis[a:b], pis[a:b], vo, True)))
         except Exception as e:  # the reference's ToolError subclasses
             out.append(_Deferred(error=e))
     return out

@@ -80,6 +80,9 @@ V_ALLOW_STALE = 2
 V_DECL_LATE = 4           # check_decl_placement would raise (`dataflow.py:242-255`)
 V_NONLOCAL = 8            # storage is not LOCAL (`_escape_liveness`, `dataflow.py:671-676`)
 
+# function flags (dfx_fn_desc.flags)
+FN_NO_ERR_SITES = 1       # no anchor of the function can raise a braces error
+
 # ---- anchor codes (hoist tables and arm anchors) ---------------------------
 AC_NODE_MASK = (1 << 20) - 1
 AC_ERR = 1 << 20          # the node is the one `_normalize_anchor` failed at
@@ -143,6 +146,8 @@ class FnProgram:
     max_loop_depth: int
     max_br_depth: int
     max_arms: int
+    fn_flags: int = 0                    # dfx_fn_desc.flags (FN_NO_ERR_SITES)
+    scoping_error: tuple | None = None   # (decl offset, message): see region_scoping_error
     vars: list = field(default_factory=list)
     stmts: list = field(default_factory=list)
     kernel_stmts: list = field(default_factory=list)
@@ -234,6 +239,7 @@ class _Lowerer:
         self.br_depth = 0
         self.max_br_depth = 0
         self.max_arms = 0
+        self.may_err = False    # some anchor can raise a braces error
         self.live = 1       # slot references held (cur)
         self.max_live = 1
 
@@ -294,6 +300,7 @@ class _Lowerer:
                 node = p
                 continue
             code = self.sid(node) | AC_ERR
+            self.may_err = True
             break
         if code is None:
             code = self.sid(node)
@@ -529,6 +536,7 @@ class _Lowerer:
             return (ARM_AFTER, self.sid(last))
         if arm.kind in _JUMPS:
             return self._none_anchor(branch_stmt)
+        self.may_err = True
         return (ARM_ERR_ARM, self.sid(arm))
 
     def _none_anchor(self, branch_stmt):
@@ -677,9 +685,39 @@ class _Lowerer:
                                 if self.region_begin is not None else -1),
             n_slots=n_slots, max_loop_depth=self.max_loop_depth,
             max_br_depth=self.max_br_depth, max_arms=self.max_arms,
+            fn_flags=0 if self.may_err else FN_NO_ERR_SITES,
+            scoping_error=(region_scoping_error(self.src, self.accesses, self.region_begin,
+                                               self.region_end)
+                           if self.region_begin is not None else None),
             vars=self.vars, stmts=self.stmts, kernel_stmts=self.kernel_stmts,
             region=((self.region_block, self.region_begin, self.region_end)
                     if self.region_begin is not None else None))
+
+
+def region_scoping_error(src, accesses, begin, end):
+    """`_Analyzer._check_region_scoping` (`dataflow.py:713-734`) as data: the
+    DeclPlacementError it raises for a region over [begin, end] -- (offset,
+    message) -- or None.  Static (declarations and accesses only), so the
+    lowering computes it and `_finish` raises it only if the plan opens a
+    region."""
+    lo = begin.span.start
+    hi = end.span.end
+    inside = {}
+    for acc in accesses:
+        d = acc.var.decl
+        if d is None or not (lo <= d.span.start < hi):
+            continue
+        if acc.ast.span.start >= hi and acc.ast is not d:
+            inside.setdefault(acc.var, acc)
+    for var, acc in sorted(inside.items(), key=lambda kv: kv[0].name):
+        return (var.decl.span.start,
+                "'%s' is declared at line %d inside the new data region "
+                "(lines %d..%d) but used at line %d after it; move the "
+                "declaration above the region" % (
+                    var.name, src.line_of(var.decl.span.start),
+                    src.line_of(lo), src.line_of(hi - 1),
+                    src.line_of(acc.ast.span.start)))
+    return None
 
 
 def premapped_directive(root):

@@ -73,6 +73,10 @@ def parse_args():
                     help="C4 source functions in the simulator (verifier) record")
     ap.add_argument("--no-emit", action="store_true",
                     help="skip the batched-emission sub-record")
+    ap.add_argument("--no-api", action="store_true",
+                    help="skip the reference-API record (C1, C2, C4 source through plan_transform)")
+    ap.add_argument("--api-funcs", type=int, default=400,
+                    help="functions of the C4-style source program in the reference-API record")
     ap.add_argument("--emit-units", type=int, default=48,
                     help="C4 source translation units in the batched-emission record")
     return ap.parse_args()
@@ -443,6 +447,9 @@ def run_ours(args, rank, world, local):
     emit_rec = None
     if not args.no_emit and world == 1:
         emit_rec = run_emit_record(args)
+    api_rec = None
+    if not args.no_api and world == 1:
+        api_rec = run_api_record(args)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -482,7 +489,101 @@ def run_ours(args, rank, world, local):
         line["sim"] = sim
     if emit_rec is not None:
         line["emit"] = emit_rec
+    if api_rec is not None:
+        line["api"] = api_rec
     print(json.dumps(line), flush=True)
+
+
+def run_api_record(args):
+    """The drop-in at the reference's own API (`dartomp.pipeline`), beside
+    the reference on the same source, same process, one core each:
+      c1  Listing 1 (SPEC motivating example): transform text + report lines
+          identical to the reference's (parity only, BASELINE configs[0]);
+      c2  LULESH-shaped program (BASELINE configs[1]): load, plan_transform
+          and apply_plans timed (medians), output byte-identical;
+      c4_source  a C4-style program of --api-funcs structured functions:
+          plan_transform timed on the same parsed unit, plans identical
+          (anchor identity included).
+    The front end (lexer, parser, AST-CFG, access classification) is the
+    reference's on both sides; the drop-in swaps the analysis (E1, kernel c)
+    and the emitter."""
+    from paper_2406_13881_b200._host import have_dartomp
+    if not have_dartomp():
+        return {"unavailable": "host front end (dartomp) not importable"}
+    import dartomp.pipeline as ref
+    from dartomp.report import plan_lines as ref_lines
+    from dartomp.rewriter import apply_plans as ref_apply
+    from paper_2406_13881_b200 import pipeline as eng
+    from paper_2406_13881_b200.gen.cprog import GenConfig, generate
+    from paper_2406_13881_b200.gen.lulesh import generate_lulesh
+
+    def med(fn, reps):
+        ts, out = [], None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn()
+            ts.append(1e3 * (time.perf_counter() - t0))
+        return statistics.median(ts), out
+
+    def pipeline_run(mod, apply, text, reps):
+        parts = {"load": [], "plan": [], "total": []}
+        out = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            a = mod.load(text=text)
+            t1 = time.perf_counter()
+            plans = mod.plan_transform(a)
+            t2 = time.perf_counter()
+            out = apply(a.src, plans)
+            t3 = time.perf_counter()
+            parts["load"].append(1e3 * (t1 - t0))
+            parts["plan"].append(1e3 * (t2 - t1))
+            parts["total"].append(1e3 * (t3 - t0))
+        return {k: statistics.median(v) for k, v in parts.items()}, out
+
+    rec = {"what": "the drop-in (paper_2406_13881_b200.pipeline) vs the reference "
+                   "(dartomp.pipeline) on the same source, same process, one core each"}
+    # C1: Listing 1
+    c1 = ROOT / "tests" / "golden" / "corpus" / "transform" / "listing1.c"
+    text = c1.read_text()
+    ar, ae = ref.load(text=text, path=str(c1)), eng.load(text=text, path=str(c1))
+    pr, pe = ref.plan_transform(ar), eng.plan_transform(ae)
+    rr, re_ = ref_apply(ar.src, pr), eng.apply_plans(ae.src, pe)
+    rec["c1"] = {"workload": "C1: SPEC Listing 1 (tests/golden/corpus/transform/listing1.c)",
+                 "identical_output": rr.text == re_.text,
+                 "identical_report": ref_lines(ar.src, pr) == eng.plan_lines(ae.src, pe),
+                 "report": eng.plan_lines(ae.src, pe)}
+    # C2: LULESH-shaped
+    text = generate_lulesh(seed=1)
+    pipeline_run(eng, eng.apply_plans, text, 2)                # warm the engine
+    r_ref, o_ref = pipeline_run(ref, ref_apply, text, 7)
+    r_eng, o_eng = pipeline_run(eng, eng.apply_plans, text, 7)
+    rec["c2"] = {"workload": "C2: LULESH-shaped program (gen/lulesh.py seed 1), %d lines"
+                             % len(text.splitlines()),
+                 "reference_ms": r_ref, "dropin_ms": r_eng,
+                 "speedup_plan": r_ref["plan"] / r_eng["plan"],
+                 "speedup_total": r_ref["total"] / r_eng["total"],
+                 "identical_output": o_ref.text == o_eng.text}
+    # C4-style functions from C source at the reference API
+    n = args.api_funcs
+    text = generate(7, GenConfig(n_funcs=n, n_globals=24, n_stmts=40, p_kernel=0.3))
+    a = ref.load(text=text)
+    eng.plan_transform(a)                                      # warm
+    t_ref, p_ref = med(lambda: ref.plan_transform(a), 2)
+    t_eng, p_eng = med(lambda: eng.plan_transform(a), 3)
+
+    def key(plans):
+        return [(id(p.function), [(u.kind, u.names, id(u.anchor), u.position) for u in p.all_plans],
+                 (id(p.region.begin), p.region.clause_text()) if p.region is not None else None,
+                 tuple(p.suppressed)) for p in plans]
+    rec["c4_source"] = {"workload": "%d structured functions from C source (gen/cprog.py seed 7), "
+                                    "%d lines" % (len(a.cfgs), len(text.splitlines())),
+                        "reference_plan_transform_ms": t_ref, "dropin_plan_transform_ms": t_eng,
+                        "speedup": t_ref / t_eng, "identical_plans": key(p_ref) == key(p_eng),
+                        "lowering_workers": int(os.environ.get("DFX_LOWER_WORKERS", "0"))
+                        or min(16, os.cpu_count() or 1)}
+    rec.update(host_info())
+    return rec
 
 
 def run_emit_record(args):

@@ -45,8 +45,7 @@ import numpy as np
 from ._host import import_dartomp
 
 import_dartomp()
-from dartomp.access import (AccessKind, Space, Storage,  # noqa: E402
-                            enclosing_statement, kernel_rw_sets, reads, writes)
+from dartomp.access import AccessKind, Space, Storage, reads, writes  # noqa: E402
 from dartomp.bounds import (enclosing_for_loops, find_indexing_var,  # noqa: E402
                             subscript_index_vars)
 from dartomp.dataflow import compute_region_extent  # noqa: E402
@@ -233,6 +232,8 @@ class _Lowerer:
         self._dev_by_node: dict | None = None
         self._fiv_cache: dict = {}
         self._norm_cache: dict = {}
+        self._loops_cache: dict = {}
+        self._idx_cache: dict = {}
         # structural bounds for engine resources
         self.loop_depth = 0
         self.max_loop_depth = 0
@@ -333,8 +334,15 @@ class _Lowerer:
         if subscript is None:
             self.sites.extend([0, acc_code])
         else:
-            loops = enclosing_for_loops(access_stmt, stop_at=self.fn)
-            idx_vars = subscript_index_vars(subscript)
+            # per statement / per subscript, not per (statement, subscript, variable)
+            k = id(access_stmt)
+            loops = self._loops_cache.get(k)
+            if loops is None:
+                loops = self._loops_cache[k] = enclosing_for_loops(access_stmt, stop_at=self.fn)
+            k = id(subscript)
+            idx_vars = self._idx_cache.get(k)
+            if idx_vars is None:
+                idx_vars = self._idx_cache[k] = subscript_index_vars(subscript)
             read_pos = access_stmt.span.start
             self.sites.extend([len(loops), acc_code])
             for f in loops:
@@ -365,7 +373,32 @@ class _Lowerer:
             for acc in self.accesses:
                 if acc.space is Space.DEVICE:
                     by.setdefault(acc.cfg_node, []).append(acc)
-        return kernel_rw_sets(by.get(node_id, ()), node_id, kernel_ast)
+        # the reference's loop (`access.py:405-427`) with `decl_is_inside`
+        # (`access.py:163-166`, an ancestor walk) answered once per variable
+        written: set = set()
+        seen_reads: set = set()
+        entry_reads: list = []
+        writes_out: list = []
+        inside: dict = {}
+        for acc in by.get(node_id, ()):
+            var = acc.var
+            k = id(var)
+            ins = inside.get(k)
+            if ins is None:
+                d = var.decl
+                ins = inside[k] = d is not None and (
+                    d is kernel_ast or any(a is kernel_ast for a in d.ancestors()))
+            if ins:
+                continue
+            kind = acc.kind
+            if reads(kind) and var not in written and var not in seen_reads:
+                entry_reads.append(var)
+                seen_reads.add(var)
+            if writes(kind):
+                if var not in written:
+                    writes_out.append(var)
+                written.add(var)
+        return entry_reads, writes_out
 
     def device_read_subscript(self, var, kernel_stmt):
         """`_device_read_subscript` (`dataflow.py:380-390`): the subscript of
@@ -728,18 +761,34 @@ def premapped_directive(root):
     Iterative, so the batched lowering can run the check per function in its
     workers instead of one recursive generator walk over the whole unit."""
     omp_kind = NodeKind.OMP_DIRECTIVE
+    leaf = _NO_DIRECTIVE_BELOW
     stack = [root]
     while stack:
         node = stack.pop()
-        if node.kind is omp_kind and node.omp is not None:
+        kind = node.kind
+        if kind is omp_kind and node.omp is not None:
             info = node.omp
             if info.kind in DATA_MAPPING_KINDS or (
                     info.kind in KERNEL_KINDS and info.clause("map") is not None):
                 return node
+        if kind in leaf:
+            continue
         ch = node.children
         if ch:
             stack.extend(reversed(ch))
     return None
+
+
+# node kinds whose subtrees hold expressions and declarators only: a pragma
+# is a statement (`parser.py`), so no directive lies below them and the
+# pre-order walk above need not enter them
+_NO_DIRECTIVE_BELOW = frozenset({
+    NodeKind.EXPR_STMT, NodeKind.DECL_STMT, NodeKind.RETURN_STMT, NodeKind.VAR_DECL,
+    NodeKind.PARAM_DECL, NodeKind.STRUCT_DECL, NodeKind.BINARY_OP, NodeKind.UNARY_OP,
+    NodeKind.ASSIGN_OP, NodeKind.ARRAY_SUBSCRIPT, NodeKind.MEMBER_ACCESS, NodeKind.CALL,
+    NodeKind.DECL_REF, NodeKind.INT_LITERAL, NodeKind.FLOAT_LITERAL, NodeKind.STRING_LITERAL,
+    NodeKind.INIT_LIST, NodeKind.CAST, NodeKind.EMPTY,
+})
 
 
 def lower_function(src, cfg, accesses, table, allow_stale=frozenset()) -> FnProgram:

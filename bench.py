@@ -226,7 +226,7 @@ def run_reference(args, rank, world):
                       "impl": "reference", "cpu_baseline": cb,
                       "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit_line(line)
 
 
 # ---------------------------------------------------------------------------
@@ -491,7 +491,7 @@ def run_ours(args, rank, world, local):
         line["emit"] = emit_rec
     if api_rec is not None:
         line["api"] = api_rec
-    print(json.dumps(line), flush=True)
+    emit_line(line)
 
 
 def run_api_record(args):
@@ -914,7 +914,7 @@ def run_c4(args, rank, world, local, sub=False):
     if rank != 0:
         return None
     rec.update({"warmup": args.warmup, "vs_baseline": None, "dtype": "u32"})
-    print(json.dumps(rec), flush=True)
+    emit_line(rec)
     return None
 
 
@@ -1019,7 +1019,24 @@ def c5_reference_compare(n_funcs=10_000):
             **host_info()}
 
 
+_JSON_OUT = None
+
+
+def emit_line(rec) -> None:
+    """The run's one JSON line, on the process's real stdout (see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(rec) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: native libraries (NCCL prints its
+    # version at communicator init) write to fd 1 directly, so fd 1 is pointed
+    # at stderr for the run and the line goes to a private copy of stdout
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse_args()
     rank, world, local = dist_env()
     if world > 1:

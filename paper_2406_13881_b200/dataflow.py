@@ -258,6 +258,7 @@ def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
         keys: set = set()
         pstmts = prog.stmts
         names = [v.name for v in prog.vars]
+        name1 = [(n,) for n in names]       # one names tuple per variable
         # the batch path drops repeated (variable, node, kind, position)
         # records before decoding (`_first_occurrences`), so the key set is
         # needed only where two variables share a name (shadowing)
@@ -283,7 +284,7 @@ def _decode_cols(prog: FnProgram, src, accesses, events, kinds, vis, nis, pis,
             plan = new(DP)
             pd = plan.__dict__
             pd["kind"] = _PLAN_KIND[kind]
-            pd["names"] = (name,)
+            pd["names"] = name1[vi]
             pd["anchor"] = pstmts[ni]
             pd["position"] = _POS[pi]
             (firstprivates if kind == fp else updates).append(plan)

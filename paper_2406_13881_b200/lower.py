@@ -127,6 +127,9 @@ def _clause_names(info, clause: str) -> set[str]:
 
 
 _JUMPS = (NodeKind.RETURN_STMT, NodeKind.BREAK_STMT, NodeKind.CONTINUE_STMT)
+# `access.reads` / `access.writes` (`access.py:44-49`) as tuples (identity tests)
+_READ_KINDS = (AccessKind.READ, AccessKind.READWRITE, AccessKind.UNKNOWN)
+_WRITE_KINDS = (AccessKind.WRITE, AccessKind.READWRITE, AccessKind.UNKNOWN)
 
 
 @dataclass
@@ -178,12 +181,17 @@ def _enclosing_statement(ast):
 
 
 def _for_stmts(root):
-    """`root.find_all(NodeKind.FOR_STMT)` in the same (pre-)order, iteratively."""
+    """`root.find_all(NodeKind.FOR_STMT)` in the same (pre-)order, iteratively
+    (expression subtrees, which hold no statement, are not entered)."""
     out, stack = [], [root]
+    for_kind, leaf = NodeKind.FOR_STMT, _NO_STMT_BELOW_IDS
     while stack:
         n = stack.pop()
-        if n.kind is NodeKind.FOR_STMT:
+        k = n.kind
+        if k is for_kind:
             out.append(n)
+        elif id(k) in leaf:
+            continue
         stack.extend(reversed(n.children))
     return out
 
@@ -233,6 +241,7 @@ class _Lowerer:
         self._fiv_cache: dict = {}
         self._norm_cache: dict = {}
         self._loops_cache: dict = {}
+        self._decl_anc: dict = {}
         self._idx_cache: dict = {}
         # structural bounds for engine resources
         self.loop_depth = 0
@@ -380,21 +389,29 @@ class _Lowerer:
         entry_reads: list = []
         writes_out: list = []
         inside: dict = {}
+        anc = self._decl_anc
+        kid = id(kernel_ast)
         for acc in by.get(node_id, ()):
             var = acc.var
             k = id(var)
             ins = inside.get(k)
             if ins is None:
                 d = var.decl
-                ins = inside[k] = d is not None and (
-                    d is kernel_ast or any(a is kernel_ast for a in d.ancestors()))
+                if d is None:
+                    ins = False
+                else:
+                    a = anc.get(id(d))
+                    if a is None:      # the declaration and its ancestors' ids, once per function
+                        a = anc[id(d)] = {id(x) for x in d.ancestors()} | {id(d)}
+                    ins = kid in a
+                inside[k] = ins
             if ins:
                 continue
             kind = acc.kind
-            if reads(kind) and var not in written and var not in seen_reads:
+            if kind in _READ_KINDS and var not in written and var not in seen_reads:
                 entry_reads.append(var)
                 seen_reads.add(var)
-            if writes(kind):
+            if kind in _WRITE_KINDS:
                 if var not in written:
                     writes_out.append(var)
                 written.add(var)
@@ -761,7 +778,7 @@ def premapped_directive(root):
     Iterative, so the batched lowering can run the check per function in its
     workers instead of one recursive generator walk over the whole unit."""
     omp_kind = NodeKind.OMP_DIRECTIVE
-    leaf = _NO_DIRECTIVE_BELOW
+    leaf = _NO_STMT_BELOW_IDS
     stack = [root]
     while stack:
         node = stack.pop()
@@ -771,7 +788,7 @@ def premapped_directive(root):
             if info.kind in DATA_MAPPING_KINDS or (
                     info.kind in KERNEL_KINDS and info.clause("map") is not None):
                 return node
-        if kind in leaf:
+        if id(kind) in leaf:
             continue
         ch = node.children
         if ch:
@@ -779,16 +796,18 @@ def premapped_directive(root):
     return None
 
 
-# node kinds whose subtrees hold expressions and declarators only: a pragma
-# is a statement (`parser.py`), so no directive lies below them and the
-# pre-order walk above need not enter them
-_NO_DIRECTIVE_BELOW = frozenset({
+# node kinds whose subtrees hold expressions and declarators only: no
+# statement -- in particular no pragma (`parser.py:293-298`) and no loop --
+# lies below them, so the pre-order walks for directives and for-statements
+# need not enter them
+_NO_STMT_BELOW = frozenset({
     NodeKind.EXPR_STMT, NodeKind.DECL_STMT, NodeKind.RETURN_STMT, NodeKind.VAR_DECL,
     NodeKind.PARAM_DECL, NodeKind.STRUCT_DECL, NodeKind.BINARY_OP, NodeKind.UNARY_OP,
     NodeKind.ASSIGN_OP, NodeKind.ARRAY_SUBSCRIPT, NodeKind.MEMBER_ACCESS, NodeKind.CALL,
     NodeKind.DECL_REF, NodeKind.INT_LITERAL, NodeKind.FLOAT_LITERAL, NodeKind.STRING_LITERAL,
     NodeKind.INIT_LIST, NodeKind.CAST, NodeKind.EMPTY,
 })
+_NO_STMT_BELOW_IDS = frozenset(id(k) for k in _NO_STMT_BELOW)   # Enum.__hash__ is Python-level
 
 
 def lower_function(src, cfg, accesses, table, allow_stale=frozenset()) -> FnProgram:

@@ -943,33 +943,41 @@ def run_c5(args, rank, world, local):
         t0 = time.perf_counter()
         r = solve_call_graph(g)
         ts.append(time.perf_counter() - t0)
-    cs = ComponentSummaries(g, rank, world)
-    cs.solve()
-    tc = []
-    for _ in range(5):
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        bits, lst, ln, passes = cs.solve()
-        tc.append(time.perf_counter() - t0)
-    same = bool(np.array_equal(bits, r.bits) and np.array_equal(ln, r.len) and passes == r.passes)
-    t = torch.tensor([statistics.median(tc)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     nf, ns = g.init_bits.shape
+    if world > 1 and os.environ.get("DFX_BENCH_SHARE_GPU"):
+        # ranks sharing one GPU (the 2-rank rehearsal on a 1-GPU box): NCCL
+        # refuses two ranks on one device, so the sharded solve is not run
+        sharded = {"skipped": "ranks share one GPU (DFX_BENCH_SHARE_GPU); NCCL needs one GPU per rank"}
+        cs = None
+    else:
+        cs = ComponentSummaries(g, rank, world)
+        cs.solve()
+        tc = []
+        for _ in range(5):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            bits, lst, ln, passes = cs.solve()
+            tc.append(time.perf_counter() - t0)
+        same = bool(np.array_equal(bits, r.bits) and np.array_equal(ln, r.len) and passes == r.passes)
+        t = torch.tensor([statistics.median(tc)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sharded = {"value": nf * ns / float(t.item()), "ranks": world,
+                   "call_ms_max_over_ranks": 1e3 * float(t.item()),
+                   "collectives_per_solve": cs.collectives, "passes": passes,
+                   "equal_to_single_launch": same,
+                   "path": "dfx_summaries_sharded over the handle's NCCL "
+                           "communicator (dfx_comm_init)"}
     rec = {"workload": "C5: %d functions, depth-12 chains, 10%% back edges, %d globals"
                        % (nf, ns - g.n_params),
            "unit": "summary facts/s (functions x slots per solve)",
            "single_launch": {"value": nf * ns / statistics.median(ts), "passes": r.passes,
                              "device_ms": r.kernel_ms, "call_ms": 1e3 * statistics.median(ts),
                              "path": "dfx_summaries: all passes and waves in one cooperative launch"},
-           "component_sharded": {"value": nf * ns / float(t.item()), "ranks": world,
-                                 "call_ms_max_over_ranks": 1e3 * float(t.item()),
-                                 "collectives_per_solve": cs.collectives, "passes": passes,
-                                 "equal_to_single_launch": same,
-                                 "path": "dfx_summaries_sharded over the handle's NCCL "
-                                         "communicator (dfx_comm_init)"}}
-    cs.close()
+           "component_sharded": sharded}
+    if cs is not None:
+        cs.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from paper_2406_13881_b200._host import have_dartomp
         if have_dartomp():

@@ -77,6 +77,10 @@ def parse_args():
                     help="skip the reference-API record (C1, C2, C4 source through plan_transform)")
     ap.add_argument("--api-funcs", type=int, default=400,
                     help="functions of the C4-style source program in the reference-API record")
+    ap.add_argument("--no-cfg", action="store_true",
+                    help="skip the north-star CFG-program record (real programs -> CSR -> kernels a+b)")
+    ap.add_argument("--cfg-units", type=int, default=40,
+                    help="C4 source translation units in the CFG-program record")
     ap.add_argument("--emit-units", type=int, default=48,
                     help="C4 source translation units in the batched-emission record")
     return ap.parse_args()
@@ -450,6 +454,9 @@ def run_ours(args, rank, world, local):
     api_rec = None
     if not args.no_api and world == 1:
         api_rec = run_api_record(args)
+    cfg_rec = None
+    if not args.no_cfg and world == 1:
+        cfg_rec = run_cfg_record(args)
     if rank != 0:
         return
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -491,7 +498,85 @@ def run_ours(args, rank, world, local):
         line["emit"] = emit_rec
     if api_rec is not None:
         line["api"] = api_rec
+    if cfg_rec is not None:
+        line["cfg"] = cfg_rec
     emit_line(line)
+
+
+def run_cfg_record(args):
+    """The north-star path on real programs (cfgprog.py): --cfg-units C4
+    source translation units, parsed by the reference's front end (untimed),
+    lowered into ONE block-diagonal CSR over their AST-CFGs with per-node
+    access lists (host Python, timed and reported), solved by kernels (a)+(b)
+    in one `dfx_mfp_acc` call with host buffers (timed: H2D, expansion,
+    fixpoint, requirements, D2H).  Parity: fixpoint planes and requirement
+    lists == oracle/mfp_oracle.c on the same problem."""
+    from paper_2406_13881_b200._host import have_dartomp
+    if not have_dartomp():
+        return {"unavailable": "host front end (dartomp) not importable"}
+    import numpy as np
+    from dartomp.pipeline import load
+    from paper_2406_13881_b200.cfgprog import fixpoint_planes, lower_program, solve_program
+    from paper_2406_13881_b200.csr import AccSession
+    from paper_2406_13881_b200.gen.c4src import C4SourceConfig, c4_source
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _oracle  # noqa: E402  (the checker)
+    n = args.cfg_units
+    items = []
+    for k in range(n):
+        a = load(text=c4_source(C4SourceConfig(), k * (100_000 // max(1, n))))
+        items += [(nm, a.src, a.cfgs[nm], a.accesses[nm], a.table) for nm in a.cfgs]
+    t0 = time.perf_counter()
+    prog = lower_program(items)
+    lower_s = time.perf_counter() - t0
+    sess = AccSession()
+    solve_program(prog, sess)                              # warm
+    ts, ks = [], []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        reqs, st = solve_program(prog, sess)
+        ts.append(time.perf_counter() - t0)
+        ks.append(float(st.kernel_ms))
+    call_s = statistics.median(ts)
+    # parity: planes of the C restatement on the same problem
+    acc = prog.acc.astype(np.int64)
+    node = np.repeat(np.arange(prog.n_nodes), np.diff(prog.acc_off))
+
+    def plane(mask):
+        bits = np.zeros((prog.n_nodes, prog.words * 32), dtype=np.uint8)
+        sel = (acc >> 14) & mask != 0
+        bits[node[sel], (acc & 0x3FFF)[sel]] = 1
+        return np.packbits(bits, axis=1, bitorder="little").view(np.uint32).reshape(
+            prog.n_nodes, prog.words).copy()
+    R, W = plane(1), plane(2)
+    g = {"row_ptr": prog.row_ptr, "col": prog.col, "kind": prog.kind, "A": R | W, "B": W,
+         "USE": R, "S": prog.S}
+    OH, OD, _ = _oracle.c3_solve(g)
+    REQ, FP = _oracle.c3_requirements(g, OH, OD)
+    gh, gd = fixpoint_planes(prog)
+    rl = sess.run(prog.row_ptr, prog.col, prog.kind, prog.acc_off, prog.acc, prog.S, prog.words)
+    rq, fp = rl.to_planes()
+    ok = (np.array_equal(gh, OH) and np.array_equal(gd, OD) and np.array_equal(rq, REQ)
+          and np.array_equal(fp, FP))
+    supported = sum(f.status == "ok" for f in prog.fns)
+    facts = prog.facts
+    return {"workload": "%d C4 source translation units (gen/c4src.py, every %d-th of 100k), "
+                        "%d functions lowered into one CSR over their AST-CFGs"
+                        % (n, 100_000 // max(1, n), len(prog.fns)),
+            "unit": "facts/s (CFG nodes x variables, to fixpoint, + requirements)",
+            "functions": len(prog.fns), "supported": supported,
+            "nodes": prog.n_nodes, "edges": int(prog.col.shape[0]),
+            "words": prog.words, "accesses": int(prog.acc.shape[0]), "facts": facts,
+            "value": facts / call_s,
+            "call_ms": 1e3 * call_s, "kernel_ms": statistics.median(ks),
+            "h2d_bytes": int(prog.row_ptr.nbytes + prog.col.nbytes + prog.kind.nbytes
+                             + prog.acc_off.nbytes + prog.acc.nbytes + prog.S.nbytes),
+            "host_lowering_s": lower_s,
+            "requirements": int(rl.vars.shape[0]),
+            "parity": {"status": "ok" if ok else "MISMATCH",
+                       "checked": "fixpoint planes (H, D) and requirement / firstprivate "
+                                  "planes == oracle/mfp_oracle.c on the same problem"},
+            "path": "cfgprog.lower_program -> solve_program -> dfx_mfp_acc (one call)"}
 
 
 def run_api_record(args):

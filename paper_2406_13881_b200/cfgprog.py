@@ -1,0 +1,326 @@
+"""North-star lowering of real programs into kernels (a)+(b).
+
+`north_star`: the front end lowers each program into packed CSR graphs -- the
+CFG and its predecessor lists -- and each node's GEN/KILL and access sets into
+uint32 bitplanes over the variable dimension, which hand-written kernels solve.
+This module is that path for parsed translation units of the reference:
+
+- the graph is the reference's own AST-CFG (`astcfg.py:507`, `AstCfg.edges`):
+  one node per CFG node, predecessors from its edges, kernel nodes where the
+  CFG has a sub-CFG (`AstCfg.kernel_nodes`);
+- a node's accesses are the reference's `MemoryAccess` list grouped by
+  `cfg_node` with the analysis' own op rules (`dataflow.py:412-494`): a device
+  access outside the data region counts as a host access, `UNKNOWN` is
+  skipped, READWRITE is read then write, and a kernel node carries its
+  whole-object entry reads and writes (`access.kernel_rw_sets`) without its
+  private / linear / loop-index variables; a scalar read and not written by
+  the kernel is firstprivate-eligible (the S plane);
+- many functions (of one or many units) go into ONE block-diagonal problem:
+  each function's variables get function-local slots, scalars first, so one
+  S plane (slots [0, max scalars)) serves every function;
+- `solve_program` runs kernel (a) (fixpoint) and kernel (b) (per-node
+  requirements) in one call through the access-list entry point
+  (`dfx_mfp_acc`: H2D of CSR + lists, expansion, kernels, D2H of lists).
+
+What it computes is the monotone-framework solution the north star names
+(`dataflow.py:299-378` op effects, `:130-134` AND meet) over the CFG.  It
+equals the reference analysis' state at every planning visit on the monotone
+subset (loops, no branches, no update hoisted in front of a loop),
+which `tests/test_cfgprog.py` checks against the reference itself; outside
+that subset the reference's reconcile joins, dry rounds and provenance (D1,
+D3, D8, D9) are not an MFP, and the directive plans come from E1 (DESIGN.md
+§13).  Node shapes the two-plane encoding cannot express -- a host read at a
+kernel node (firstprivate clause), host accesses on a kernel statement, a
+device access at a host node inside the region -- mark the function
+unsupported; it is reported, not approximated.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._host import import_dartomp
+from .csr import ACC_READ, ACC_WRITE, REQ_FP_FLAG, AccSession, CsrProblem
+from .lower import _clause_names, _for_stmts, _Lowerer, _READ_KINDS, _WRITE_KINDS
+
+import_dartomp()
+from dartomp.access import AccessKind, Space  # noqa: E402
+
+
+class Unsupported(Exception):
+    """A node the host/kernel two-plane encoding cannot express."""
+
+
+@dataclass
+class FnGraph:
+    """One function's part of a batch: nodes [node0, node0 + n_nodes) are its
+    CFG nodes in id order; slot s of the batch's variable dimension is
+    `vars[s]` (None: unused by this function)."""
+    name: str
+    cfg: object
+    node0: int = 0
+    n_nodes: int = 0
+    vars: list = field(default_factory=list)
+    status: str = "ok"
+    first: list = field(default_factory=list)   # CFG node id -> its first graph node
+
+
+@dataclass
+class CfgProgram:
+    row_ptr: np.ndarray      # int32 [N+1] predecessor CSR
+    col: np.ndarray          # int32 [nnz]
+    kind: np.ndarray         # uint8 [N]: 0 host node, 1 kernel node
+    acc_off: np.ndarray      # int64 [N+1]
+    acc: np.ndarray          # uint16: slot | kind << 14 (1 read, 2 write, 3 both)
+    S: np.ndarray            # uint32 [words]: firstprivate-eligible scalar slots
+    words: int
+    fns: list                # FnGraph per input function (unsupported: n_nodes 0)
+    node_cfg: np.ndarray = None   # int32 [N]: the CFG node id each graph node belongs to
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.row_ptr.shape[0]) - 1
+
+    @property
+    def facts(self) -> int:
+        """Nodes x variables of the supported functions (the metric's facts)."""
+        return sum(f.n_nodes * sum(v is not None for v in f.vars) for f in self.fns)
+
+
+_HOST, _DEV = 0, 1
+
+
+def _node_chain(seqs):
+    """Per-variable op sequences of one CFG node -> a chain of graph nodes.
+
+    `seqs`: {var id: (var, [(space, read, write, fp_ok)])} in op order.  A
+    node carries one run per variable: consecutive ops of one space, reads
+    before writes (a read after a write starts a new run, so the node's USE
+    bit means "the first H/D-affecting op is a read", `dataflow.py:299-368`).
+    Different variables are independent, so each variable's runs
+    go to successive chain nodes of the matching kind and only its own order
+    is kept.  Returns [(kind, {var id: (var, read, write)})]."""
+    chain: list = []
+    for k, (var, ops) in seqs.items():
+        runs = []
+        for sp, r, w, fp_ok in ops:
+            if runs and runs[-1][0] == sp and not (r and runs[-1][2]):
+                last = runs[-1]
+                runs[-1] = (sp, last[1] or r, last[2] or w, last[3] and fp_ok)
+            else:
+                runs.append((sp, r, w, fp_ok))
+        pos = 0
+        for sp, r, w, fp_ok in runs:
+            if sp == _DEV and r and not w and var.is_scalar and not fp_ok:
+                # the kernel-node transfer would make it firstprivate-eligible
+                raise Unsupported("scalar device read outside a kernel's entry reads")
+            while pos < len(chain) and chain[pos][0] != sp:
+                pos += 1
+            if pos == len(chain):
+                chain.append((sp, {}))
+            chain[pos][1][k] = (var, r, w)
+            pos += 1
+    return chain
+
+
+def _function_graph(src, cfg, accesses, table):
+    """(chains per CFG node, preds per CFG node): the analysis' per-statement
+    op sequences (`dataflow.py:412-494`) as graph-node chains."""
+    lw = _Lowerer(src, cfg, accesses, table)
+    n = len(cfg.nodes)
+    preds = [[] for _ in range(n)]
+    for e in cfg.edges:
+        preds[e.dst].append(e.src)
+    kernel_ids = lw.kernel_node_ids
+    seqs: list = [dict() for _ in range(n)]
+
+    def add(nid, var, sp, r, w, fp_ok=False):
+        d = seqs[nid]
+        ent = d.get(id(var))
+        if ent is None:
+            ent = d[id(var)] = (var, [])
+        ent[1].append((sp, r, w, fp_ok))
+
+    # kernel nodes first in each node's order: `exec_omp` (dataflow.py:456-494)
+    # runs the kernel's entry reads and writes, then the statement's own
+    # accesses (`process_accesses(stmt, extra)`)
+    for nid in sorted(kernel_ids):
+        stmt = cfg.nodes[nid].ast
+        info = stmt.omp
+        entry_reads, kernel_writes = lw.kernel_rw_sets(nid, stmt)
+        captured = _clause_names(info, "firstprivate")
+        private = _clause_names(info, "private") | _clause_names(info, "linear")
+        for f in _for_stmts(stmt):
+            v = lw.find_indexing_var(f)
+            if v is not None:
+                private.add(v)
+        for var in entry_reads:
+            if var.name in private:
+                continue
+            if var.name in captured:
+                add(nid, var, _HOST, True, False)     # host_read at the kernel
+            else:
+                add(nid, var, _DEV, True, False, True)
+        for var in kernel_writes:
+            if var.name not in private and var.name not in captured:
+                add(nid, var, _DEV, False, True)
+    # statements' accesses (`process_accesses`, dataflow.py:412-435), in order
+    for acc in accesses:
+        kind = acc.kind
+        if kind is AccessKind.UNKNOWN:
+            continue
+        if acc.space is Space.DEVICE and acc.cfg_node in kernel_ids:
+            continue           # folded into the kernel's read/write sets
+        sp = _HOST
+        if acc.space is Space.DEVICE and lw.in_region(_enclosing(acc.ast)):
+            sp = _DEV
+        r, w = kind in _READ_KINDS, kind in _WRITE_KINDS
+        if r:
+            add(acc.cfg_node, acc.var, sp, True, False)
+        if w:
+            add(acc.cfg_node, acc.var, sp, False, True)
+    chains = [_node_chain(d) if d else [] for d in seqs]
+    return chains, preds
+
+
+def _enclosing(ast):
+    from .lower import _enclosing_statement
+    return _enclosing_statement(ast)
+
+
+def lower_program(items) -> CfgProgram:
+    """`items`: (name, src, cfg, accesses, table) per function.  Returns one
+    block-diagonal problem over all supported functions.  A CFG node becomes
+    a chain of graph nodes when its statement mixes host and device ops
+    (a call whose callee offloads, a firstprivate capture at a kernel): the
+    chain's first node takes the CFG node's predecessors, its last node
+    feeds the CFG node's successors."""
+    parts = []
+    for name, src, cfg, accesses, table in items:
+        fg = FnGraph(name=name, cfg=cfg)
+        try:
+            parts.append((fg, _function_graph(src, cfg, accesses, table)))
+        except Unsupported as e:
+            fg.status = "unsupported: %s" % e
+            parts.append((fg, None))
+    # slots: per function, scalars then the rest, in first-occurrence order
+    n_sc = n_ot = 0
+    for fg, g in parts:
+        if g is None:
+            continue
+        sc, ot = {}, {}
+        for chain in g[0]:
+            for _, ents in chain:
+                for var, _, _ in ents.values():
+                    (sc if var.is_scalar else ot).setdefault(id(var), var)
+        fg._sc, fg._ot = list(sc.values()), list(ot.values())
+        n_sc, n_ot = max(n_sc, len(fg._sc)), max(n_ot, len(fg._ot))
+    V = max(1, n_sc + n_ot)
+    if V > 0x3FFF:
+        raise ValueError("more than %d variables in one function" % 0x3FFF)
+    words = ((V + 127) // 128) * 4
+    bits = np.zeros(words * 32, dtype=np.uint8)
+    bits[:n_sc] = 1
+    S = np.packbits(bits, bitorder="little").view(np.uint32).copy()
+    row_ptr, col, kind, acc_off, acc, node_cfg = [0], [], [], [0], [], []
+    node0 = 0
+    for fg, g in parts:
+        if g is None:
+            continue
+        chains, preds = g
+        slot = {id(v): i for i, v in enumerate(fg._sc)}
+        slot.update({id(v): n_sc + i for i, v in enumerate(fg._ot)})
+        fg.vars = [None] * V
+        for v in fg._sc + fg._ot:
+            fg.vars[slot[id(v)]] = v
+        del fg._sc, fg._ot
+        # graph node ids: every CFG node gets at least one (empty chains: a
+        # host node without accesses)
+        first, last, nxt = [], [], node0
+        for c in chains:
+            first.append(nxt)
+            nxt += max(1, len(c))
+            last.append(nxt - 1)
+        fg.node0, fg.n_nodes = node0, nxt - node0
+        fg.first = first
+        for c_id, c in enumerate(chains):
+            nodes = c if c else [(_HOST, {})]
+            for j, (sp, ents) in enumerate(nodes):
+                if j == 0:
+                    col.extend(last[p] for p in preds[c_id])
+                else:
+                    col.append(first[c_id] + j - 1)
+                row_ptr.append(len(col))
+                kind.append(sp)
+                node_cfg.append(c_id)
+                acc.extend(sorted(slot[k] | (((ACC_READ if r else 0) | (ACC_WRITE if w else 0)) << 14)
+                                  for k, (var, r, w) in ents.items()))
+                acc_off.append(len(acc))
+        node0 = nxt
+    return CfgProgram(row_ptr=np.array(row_ptr, dtype=np.int32),
+                      col=np.array(col, dtype=np.int32),
+                      kind=np.array(kind, dtype=np.uint8),
+                      acc_off=np.array(acc_off, dtype=np.int64),
+                      acc=np.array(acc, dtype=np.uint16), S=S, words=words,
+                      fns=[fg for fg, _ in parts],
+                      node_cfg=np.array(node_cfg, dtype=np.int32))
+
+
+def lower_analysis(analysis, names=None) -> CfgProgram:
+    """`lower_program` over the functions of a `dartomp.pipeline.Analysis`."""
+    names = list(analysis.cfgs) if names is None else names
+    return lower_program([(n, analysis.src, analysis.cfgs[n], analysis.accesses[n],
+                           analysis.table) for n in names])
+
+
+@dataclass
+class FnRequirements:
+    """Kernel (b)'s answer for one function, per CFG node id: the variables
+    needing a device -> host transfer before a host read (`update from`),
+    a host -> device transfer before a device read (`update to` / map to),
+    and a kernel's firstprivate captures."""
+    name: str
+    update_from: dict        # cfg node id -> [VariableId]
+    update_to: dict
+    firstprivate: dict
+
+
+def solve_program(prog: CfgProgram, session: AccSession | None = None):
+    """Kernels (a)+(b) on the whole batch in one `dfx_mfp_acc` call.
+    Returns ([FnRequirements] for the supported functions, CsrStats)."""
+    sess = session or AccSession()
+    rl = sess.run(prog.row_ptr, prog.col, prog.kind, prog.acc_off, prog.acc, prog.S,
+                  prog.words)
+    off = rl.row_off.tolist()
+    ents = rl.vars.tolist()
+    kinds = prog.kind.tolist()
+    ncfg = prog.node_cfg.tolist()
+    out = []
+    for fg in prog.fns:
+        if fg.status != "ok":
+            continue
+        uf, ut, fp = {}, {}, {}
+        for g in range(fg.node0, fg.node0 + fg.n_nodes):
+            a, b = off[g], off[g + 1]
+            if a == b:
+                continue
+            c = ncfg[g]
+            for e in ents[a:b]:
+                v = fg.vars[e & 0x3FFF]
+                d = fp if e & REQ_FP_FLAG else (ut if kinds[g] else uf)
+                d.setdefault(c, []).append(v)
+        out.append(FnRequirements(fg.name, uf, ut, fp))
+    return out, sess.stats
+
+
+def fixpoint_planes(prog: CfgProgram):
+    """Kernel (a)'s fixpoint OUT planes (H, D) [N, words] of the batch."""
+    p = CsrProblem.from_acc(prog.row_ptr, prog.col, prog.kind, prog.acc_off, prog.acc,
+                            prog.S, prog.words)
+    try:
+        p.solve()
+        oh, od, _ = p.download(True, True)
+    finally:
+        p.close()
+    return oh, od

@@ -236,15 +236,19 @@ def lower_program(items) -> CfgProgram:
             fg.vars[slot[id(v)]] = v
         del fg._sc, fg._ot
         # graph node ids: every CFG node gets at least one (empty chains: a
-        # host node without accesses)
-        first, last, nxt = [], [], node0
-        for c in chains:
-            first.append(nxt)
-            nxt += max(1, len(c))
-            last.append(nxt - 1)
+        # host node without accesses), numbered in reverse postorder so that
+        # kernel (a)'s in-order sweep meets most predecessors already final
+        # and a statement's fall-through predecessor is the node before it
+        order = _reverse_postorder(preds)
+        first, last, nxt = [0] * len(chains), [0] * len(chains), node0
+        for c_id in order:
+            first[c_id] = nxt
+            nxt += max(1, len(chains[c_id]))
+            last[c_id] = nxt - 1
         fg.node0, fg.n_nodes = node0, nxt - node0
         fg.first = first
-        for c_id, c in enumerate(chains):
+        for c_id in order:
+            c = chains[c_id]
             nodes = c if c else [(_HOST, {})]
             for j, (sp, ents) in enumerate(nodes):
                 if j == 0:
@@ -265,6 +269,33 @@ def lower_program(items) -> CfgProgram:
                       acc=np.array(acc, dtype=np.uint16), S=S, words=words,
                       fns=[fg for fg, _ in parts],
                       node_cfg=np.array(node_cfg, dtype=np.int32))
+
+
+def _reverse_postorder(preds):
+    """CFG node ids in reverse postorder from the entry (node 0); nodes the
+    entry does not reach follow in id order."""
+    n = len(preds)
+    succ = [[] for _ in range(n)]
+    for d, ps in enumerate(preds):
+        for p in ps:
+            succ[p].append(d)
+    seen = [False] * n
+    post = []
+    if n:
+        seen[0] = True
+        stack = [(0, iter(succ[0]))]
+        while stack:
+            v, it = stack[-1]
+            for w in it:
+                if not seen[w]:
+                    seen[w] = True
+                    stack.append((w, iter(succ[w])))
+                    break
+            else:
+                stack.pop()
+                post.append(v)
+    post.reverse()
+    return post + [v for v in range(n) if not seen[v]]
 
 
 def lower_analysis(analysis, names=None) -> CfgProgram:

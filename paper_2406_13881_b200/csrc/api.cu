@@ -932,6 +932,19 @@ int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
   return DFX_OK;
 }
 
+// Nodes per warp task of kernel (a): 56 (C3 sweep 32..512, scripts/tune_c3.py)
+// unless the graph is too small to give every resident warp a chunk (real
+// programs' CFGs: tens of thousands of nodes), then as many chunks as warps,
+// at least 4 nodes each -- a round's latency is one chunk's serial sweep.
+static int default_chunk(dfx_handle* h, int64_t n_nodes) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  const int64_t warps = (int64_t)sms * 32;     // 4 blocks x 8 warps per SM
+  if (n_nodes >= 56 * warps) return 56;
+  const int64_t c = n_nodes / warps;
+  return (int)(c < 4 ? 4 : c);
+}
+
 int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
   if (h) cudaSetDevice(h->device);
   return csr_destroy_impl(p);
@@ -940,7 +953,7 @@ int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
 int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats* stats) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 56;   // C3 sweep 32..512 (scripts/tune_c3.py): 56 best
+  if (chunk_nodes <= 0) chunk_nodes = default_chunk(h, c->p.n_nodes);
   cudaStream_t st = h->st();
   dfx::SolveStats s{};
   CK(cudaEventRecord(c->e0, st));
@@ -965,7 +978,7 @@ int dfx_csr_solve(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes, dfx_csr_stats*
 int dfx_csr_solve_async(dfx_handle* h, dfx_csr* c, int32_t chunk_nodes) {
   if (!h || !c) return fail(DFX_E_ARG, "dfx_csr_solve_async: null argument");
   CK(cudaSetDevice(h->device));
-  if (chunk_nodes <= 0) chunk_nodes = 56;   // C3 sweep 32..512 (scripts/tune_c3.py): 56 best
+  if (chunk_nodes <= 0) chunk_nodes = default_chunk(h, c->p.n_nodes);
   dfx::SolveStats s{};
   int rc = dfx::mfp_solve(c->p, c->d_cnt, c->flags, h->st(), chunk_nodes, &s, false);
   if (rc) return fail(rc, "mfp_solve failed: %s", cudaGetErrorString(cudaGetLastError()));

@@ -79,7 +79,7 @@ def parse_args():
                     help="functions of the C4-style source program in the reference-API record")
     ap.add_argument("--no-cfg", action="store_true",
                     help="skip the north-star CFG-program record (real programs -> CSR -> kernels a+b)")
-    ap.add_argument("--cfg-units", type=int, default=40,
+    ap.add_argument("--cfg-units", type=int, default=80,
                     help="C4 source translation units in the CFG-program record")
     ap.add_argument("--emit-units", type=int, default=48,
                     help="C4 source translation units in the batched-emission record")

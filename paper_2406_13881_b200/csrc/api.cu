@@ -932,18 +932,10 @@ int dfx_csr_generate_c3(dfx_handle* h, const dfx_c3_spec* spec, dfx_csr** out) {
   return DFX_OK;
 }
 
-// Nodes per warp task of kernel (a): 56 (C3 sweep 32..512, scripts/tune_c3.py)
-// unless the graph is too small to give every resident warp a chunk (real
-// programs' CFGs: tens of thousands of nodes), then as many chunks as warps,
-// at least 4 nodes each -- a round's latency is one chunk's serial sweep.
-static int default_chunk(dfx_handle* h, int64_t n_nodes) {
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  const int64_t warps = (int64_t)sms * 32;     // 4 blocks x 8 warps per SM
-  if (n_nodes >= 56 * warps) return 56;
-  const int64_t c = n_nodes / warps;
-  return (int)(c < 4 ? 4 : c);
-}
+// Nodes per warp task of kernel (a): 56 (C3 sweep 32..512, scripts/tune_c3.py).
+// Real programs' CFGs (cfgprog.py, scripts/diag_cfg_solve.py) measured too:
+// 56 is best there as well (2.9 ms vs 3.0 at 128, 4.5 at 8 on 40 C4 units).
+static int default_chunk(dfx_handle*, int64_t) { return 56; }
 
 int dfx_csr_destroy(dfx_handle* h, dfx_csr* p) {
   if (h) cudaSetDevice(h->device);

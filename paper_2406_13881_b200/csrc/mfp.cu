@@ -24,7 +24,6 @@
 // The host stops when a round changes nothing.
 #include <cstdint>
 #include <cuda_runtime.h>
-#include <cub/cub.cuh>
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstdio>
@@ -142,6 +141,101 @@ __global__ void build_desc_kernel(int64_t n_nodes, const int32_t* row_ptr, const
   }
 }
 
+// Inclusive prefix sums for the CSR builders and kernel (b)'s compaction
+// (out[i] = in[0] + ... + in[i]; in and out may alias).  Reduce-then-scan over
+// tiles of 4096 elements (1024 threads x 4): per-tile sums, one block scans
+// those (exclusive), each tile rescans itself from its prefix.  Two reads of
+// the counts (8 MB at C3) instead of a single decoupled look-back pass: a few
+// microseconds beside the kernels it serves.
+constexpr int kScanThreads = 1024, kScanItems = 4, kScanTile = kScanThreads * kScanItems;
+
+// block-wide inclusive scan of one value per thread; returns the block total
+__device__ __forceinline__ int64_t block_scan(int64_t& v, int64_t* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t t = __shfl_up_sync(FULL, v, d);
+    if (lane >= d) v += t;
+  }
+  if (lane == 31) warp_tot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t t = __shfl_up_sync(FULL, w, d);
+      if (lane >= d) w += t;
+    }
+    warp_tot[lane] = w;                    // inclusive over warps
+  }
+  __syncthreads();
+  if (warp > 0) v += warp_tot[warp - 1];
+  const int64_t total = warp_tot[(blockDim.x >> 5) - 1];
+  __syncthreads();                         // warp_tot is reused by the caller's next scan
+  return total;
+}
+
+template <class TI>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums_kernel(const TI* in, int64_t n,
+                                                                      int64_t* tile_sums) {
+  __shared__ int64_t warp_tot[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++)
+    if (base + k < n) v += (int64_t)in[base + k];
+  const int64_t total = block_scan(v, warp_tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// one block: tile_sums[0..n) -> exclusive prefixes, in place
+__global__ void __launch_bounds__(kScanThreads) scan_tile_prefix_kernel(int64_t* tile_sums, int64_t n) {
+  __shared__ int64_t warp_tot[32];
+  int64_t carry = 0;
+  for (int64_t b = 0; b < n; b += kScanThreads) {
+    const int64_t i = b + threadIdx.x;
+    const int64_t x = i < n ? tile_sums[i] : 0;
+    int64_t v = x;
+    const int64_t total = block_scan(v, warp_tot);
+    if (i < n) tile_sums[i] = carry + v - x;
+    carry += total;
+  }
+}
+
+template <class TI, class TO>
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const TI* in, TO* out, int64_t n,
+                                                                  const int64_t* tile_prefix) {
+  __shared__ int64_t warp_tot[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t x[kScanItems];
+  int64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    x[k] = base + k < n ? (int64_t)in[base + k] : 0;
+    v += x[k];
+  }
+  block_scan(v, warp_tot);                 // every read of this tile precedes every write
+  int64_t run = tile_prefix[blockIdx.x] + v - (x[0] + x[1] + x[2] + x[3]);
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    run += x[k];
+    if (base + k < n) out[base + k] = (TO)run;
+  }
+}
+
+template <class TI, class TO>
+static int inclusive_scan(const TI* in, TO* out, int64_t n, void* scratch, size_t scratch_bytes,
+                          cudaStream_t st) {
+  if (n <= 0) return DFX_OK;
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if ((size_t)tiles * sizeof(int64_t) > scratch_bytes) return DFX_E_NOSPC;
+  int64_t* sums = static_cast<int64_t*>(scratch);
+  scan_tile_sums_kernel<TI><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, sums);
+  scan_tile_prefix_kernel<<<1, kScanThreads, 0, st>>>(sums, tiles);
+  scan_apply_kernel<TI, TO><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, sums);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
 __global__ void succ_count_kernel(int64_t nnz, const int32_t* col, int32_t* cnt) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x)
@@ -162,10 +256,8 @@ int build_succ(const CsrDev& p, void* scratch, size_t scratch_bytes, int32_t* tm
   if (g < 1) g = 1;
   if (cudaMemsetAsync(p.succ_ptr, 0, sizeof(int32_t) * (p.n_nodes + 1), st) != cudaSuccess) return DFX_E_CUDA;
   if (p.nnz) succ_count_kernel<<<g, 256, 0, st>>>(p.nnz, p.col, p.succ_ptr + 1);
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, p.succ_ptr + 1, p.succ_ptr + 1, (int)p.n_nodes, st);
+  if (int rc = inclusive_scan(p.succ_ptr + 1, p.succ_ptr + 1, p.n_nodes, scratch, scratch_bytes, st))
+    return rc;
   if (cudaMemcpyAsync(tmp, p.succ_ptr, sizeof(int32_t) * p.n_nodes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return DFX_E_CUDA;
   int gn = (int)((p.n_nodes + 255) / 256);
@@ -611,10 +703,7 @@ int c3_generate(CsrDev& p, uint64_t seed, int w0, cudaStream_t st, void* scratch
   int32_t* deg = p.row_ptr + 1;  // degrees land in row_ptr[1..n], scanned in place
   c3_degree_kernel<<<grid_for(p.n_nodes, 256), 256, 0, st>>>(seed, p.n_nodes, deg);
   if (cudaMemsetAsync(p.row_ptr, 0, sizeof(int32_t), st) != cudaSuccess) return DFX_E_CUDA;
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, deg, deg, (int)p.n_nodes, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, deg, deg, (int)p.n_nodes, st);
+  if (int rc = inclusive_scan(deg, deg, p.n_nodes, scratch, scratch_bytes, st)) return rc;
   c3_cols_kernel<<<grid_for(p.n_nodes, 256), 256, 0, st>>>(seed, p.n_nodes, p.row_ptr, p.col,
                                                            p.kind);
   c3_planes_kernel<<<grid_for(p.n_nodes * p.words, 256), 256, 0, st>>>(
@@ -762,10 +851,8 @@ int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void*
     case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
     default: return DFX_E_LIMIT;
   }
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, counts + n_lo, offsets + n_lo + 1, n, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, counts + n_lo, offsets + n_lo + 1, n, st);
+  if (int rc = inclusive_scan(counts + n_lo, offsets + n_lo + 1, (int64_t)n, scratch, scratch_bytes, st))
+    return rc;
   add_base_kernel<<<grid_for(n, 256), 256, 0, st>>>(offsets + n_lo + 1, n, offsets + n_lo);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
@@ -773,10 +860,7 @@ int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void*
 int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratch,
                 size_t scratch_bytes, int64_t* n_out, cudaStream_t st) {
   if (cudaMemsetAsync(offsets, 0, sizeof(int64_t), st) != cudaSuccess) return DFX_E_CUDA;
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, counts, offsets + 1, (int)n, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, counts, offsets + 1, (int)n, st);
+  if (int rc = inclusive_scan(counts, offsets + 1, n, scratch, scratch_bytes, st)) return rc;
   if (n_out && cudaMemcpyAsync(n_out, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st) !=
                    cudaSuccess)
     return DFX_E_CUDA;
@@ -796,10 +880,7 @@ int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scrat
   }
   // offsets[0] = 0; offsets[1..n] = inclusive prefix of counts
   if (cudaMemsetAsync(offsets, 0, sizeof(int64_t), st) != cudaSuccess) return DFX_E_CUDA;
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, counts, offsets + 1, (int)p.n_nodes, st);
-  if (need > scratch_bytes) return DFX_E_NOSPC;
-  cub::DeviceScan::InclusiveSum(scratch, need, counts, offsets + 1, (int)p.n_nodes, st);
+  if (int rc = inclusive_scan(counts, offsets + 1, p.n_nodes, scratch, scratch_bytes, st)) return rc;
   if (cudaMemcpyAsync(n_out, offsets + p.n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, st) !=
       cudaSuccess)
     return DFX_E_CUDA;
@@ -814,10 +895,7 @@ int requirements(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scrat
 }
 
 size_t scan_scratch_bytes(int64_t n) {
-  size_t a = 0, b = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
-  cub::DeviceScan::InclusiveSum(nullptr, b, (int32_t*)nullptr, (int64_t*)nullptr, (int)n);
-  return (a > b ? a : b) + 256;
+  return (size_t)((n + kScanTile - 1) / kScanTile) * sizeof(int64_t) + 256;
 }
 
 }  // namespace dfx

@@ -29,10 +29,12 @@ subset (loops, no branches, no update hoisted in front of a loop),
 which `tests/test_cfgprog.py` checks against the reference itself; outside
 that subset the reference's reconcile joins, dry rounds and provenance (D1,
 D3, D8, D9) are not an MFP, and the directive plans come from E1 (DESIGN.md
-§13).  Node shapes the two-plane encoding cannot express -- a host read at a
-kernel node (firstprivate clause), host accesses on a kernel statement, a
-device access at a host node inside the region -- mark the function
-unsupported; it is reported, not approximated.
+§13).  A statement that mixes host and device ops (a firstprivate capture at
+a kernel, a call whose callee offloads inside the region) becomes a chain of
+graph nodes.  The one shape the two-plane encoding cannot express -- a scalar
+read on the device outside a kernel's own entry reads, which the kernel-node
+transfer would make firstprivate-eligible -- marks the function unsupported;
+it is reported, not approximated.
 """
 from __future__ import annotations
 
@@ -42,20 +44,22 @@ import numpy as np
 
 from ._host import import_dartomp
 from .csr import ACC_READ, ACC_WRITE, REQ_FP_FLAG, AccSession, CsrProblem
-from .lower import _clause_names, _for_stmts, _Lowerer, _READ_KINDS, _WRITE_KINDS
+from .lower import (_clause_names, _enclosing_statement, _for_stmts, _Lowerer,
+                    _READ_KINDS, _WRITE_KINDS)
 
 import_dartomp()
 from dartomp.access import AccessKind, Space  # noqa: E402
 
 
 class Unsupported(Exception):
-    """A node the host/kernel two-plane encoding cannot express."""
+    """An op the host/kernel two-plane encoding cannot express."""
 
 
 @dataclass
 class FnGraph:
-    """One function's part of a batch: nodes [node0, node0 + n_nodes) are its
-    CFG nodes in id order; slot s of the batch's variable dimension is
+    """One function's part of a batch: graph nodes [node0, node0 + n_nodes)
+    are its CFG nodes' chains in reverse postorder (`first[c]` is CFG node
+    c's first graph node); slot s of the batch's variable dimension is
     `vars[s]` (None: unused by this function)."""
     name: str
     cfg: object
@@ -173,7 +177,7 @@ def _function_graph(src, cfg, accesses, table):
         if acc.space is Space.DEVICE and acc.cfg_node in kernel_ids:
             continue           # folded into the kernel's read/write sets
         sp = _HOST
-        if acc.space is Space.DEVICE and lw.in_region(_enclosing(acc.ast)):
+        if acc.space is Space.DEVICE and lw.in_region(_enclosing_statement(acc.ast)):
             sp = _DEV
         r, w = kind in _READ_KINDS, kind in _WRITE_KINDS
         if r:
@@ -182,11 +186,6 @@ def _function_graph(src, cfg, accesses, table):
             add(acc.cfg_node, acc.var, sp, False, True)
     chains = [_node_chain(d) if d else [] for d in seqs]
     return chains, preds
-
-
-def _enclosing(ast):
-    from .lower import _enclosing_statement
-    return _enclosing_statement(ast)
 
 
 def lower_program(items) -> CfgProgram:
@@ -206,6 +205,7 @@ def lower_program(items) -> CfgProgram:
             parts.append((fg, None))
     # slots: per function, scalars then the rest, in first-occurrence order
     n_sc = n_ot = 0
+    split: dict = {}                  # id(FnGraph) -> (scalars, others)
     for fg, g in parts:
         if g is None:
             continue
@@ -214,8 +214,8 @@ def lower_program(items) -> CfgProgram:
             for _, ents in chain:
                 for var, _, _ in ents.values():
                     (sc if var.is_scalar else ot).setdefault(id(var), var)
-        fg._sc, fg._ot = list(sc.values()), list(ot.values())
-        n_sc, n_ot = max(n_sc, len(fg._sc)), max(n_ot, len(fg._ot))
+        split[id(fg)] = (list(sc.values()), list(ot.values()))
+        n_sc, n_ot = max(n_sc, len(sc)), max(n_ot, len(ot))
     V = max(1, n_sc + n_ot)
     if V > 0x3FFF:
         raise ValueError("more than %d variables in one function" % 0x3FFF)
@@ -229,12 +229,12 @@ def lower_program(items) -> CfgProgram:
         if g is None:
             continue
         chains, preds = g
-        slot = {id(v): i for i, v in enumerate(fg._sc)}
-        slot.update({id(v): n_sc + i for i, v in enumerate(fg._ot)})
+        scalars, others = split[id(fg)]
+        slot = {id(v): i for i, v in enumerate(scalars)}
+        slot.update({id(v): n_sc + i for i, v in enumerate(others)})
         fg.vars = [None] * V
-        for v in fg._sc + fg._ot:
+        for v in scalars + others:
             fg.vars[slot[id(v)]] = v
-        del fg._sc, fg._ot
         # graph node ids: every CFG node gets at least one (empty chains: a
         # host node without accesses), numbered in reverse postorder so that
         # kernel (a)'s in-order sweep meets most predecessors already final

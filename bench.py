@@ -242,7 +242,8 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2406_13881_b200 import _abi
-    from paper_2406_13881_b200.csr import (AccSession, C3Config, CsrProblem, MfpSession,
+    from paper_2406_13881_b200.csr import (Acc8Session, AccSession, C3Config, CsrProblem, MfpSession,
+                                           acc_to_b8,
                                            c3_scalar_mask)
 
     torch.cuda.set_device(local)
@@ -356,13 +357,30 @@ def run_ours(args, rank, world, local):
         assert out.masks.shape[0] == rows.masks.shape[0], "e2e output differs from device run"
         ms_planes, d2h_planes = timed(lambda: sess.run(rp, col, kind, R, W, S))
         del R, W, out, sess
-        # list path (headline)
+        # uint16 list path
         acc_off, acc = prob.export_acc(alloc=pinned)
-        h2d = rp.nbytes + col.nbytes + kind.nbytes + acc_off.nbytes + acc.nbytes + S.nbytes
-        asess = AccSession(eng, alloc=pinned)
-        out = asess.run(rp, col, kind, acc_off, acc, S, cfg.words)   # warm (allocates)
-        assert out.vars.shape[0] == n_req_bits, "list output differs from the mask rows"
-        ms, d2h = timed(lambda: asess.run(rp, col, kind, acc_off, acc, S, cfg.words))
+        h2d_u16 = rp.nbytes + col.nbytes + kind.nbytes + acc_off.nbytes + acc.nbytes + S.nbytes
+        usess = AccSession(eng, alloc=pinned)
+        out_u16 = usess.run(rp, col, kind, acc_off, acc, S, cfg.words)   # warm (allocates)
+        assert out_u16.vars.shape[0] == n_req_bits, "list output differs from the mask rows"
+        ms_u16, d2h_u16 = timed(lambda: usess.run(rp, col, kind, acc_off, acc, S, cfg.words))
+        n_acc = int(acc.shape[0])
+        # byte-coded list path (headline): the same lists in ~1.2 bytes per
+        # entry (include/dfx.h B8), encoded before the timed region like the
+        # uint16 lists above
+        boff_np, b_np = acc_to_b8(acc_off, acc)
+        del acc_off, acc, usess
+        boff = pinned(boff_np.shape, np.int32)
+        boff[:] = boff_np
+        b8in = pinned(b_np.shape, np.uint8)
+        b8in[:] = b_np
+        del boff_np, b_np
+        h2d = rp.nbytes + col.nbytes + kind.nbytes + boff.nbytes + b8in.nbytes + S.nbytes
+        asess = Acc8Session(eng, alloc=pinned)
+        out8 = asess.run(rp, col, kind, boff, b8in, S, cfg.words)       # warm (allocates)
+        ms, d2h = timed(lambda: asess.run(rp, col, kind, boff, b8in, S, cfg.words))
+        out = out8.to_lists()
+        assert out.vars.shape[0] == n_req_bits, "byte-list output differs from the mask rows"
         # throughput of a stream of problems: two host threads, each with its
         # own handle and buffers, issue complete host-buffer calls; one
         # call's D2H overlaps the other's H2D and solve (full-duplex PCIe)
@@ -372,13 +390,13 @@ def run_ours(args, rank, world, local):
             eng2 = _abi.Engine(_abi.load_lib(), local)
             s2 = torch.cuda.Stream()
             eng2.lib.dfx_set_stream(eng2.h, __import__("ctypes").c_void_p(s2.cuda_stream))
-            sess2 = AccSession(eng2, alloc=pinned)
-            sess2.run(rp, col, kind, acc_off, acc, S, cfg.words)       # warm
+            sess2 = Acc8Session(eng2, alloc=pinned)
+            sess2.run(rp, col, kind, boff, b8in, S, cfg.words)       # warm
             n_each = max(2, args.e2e_steps)
 
             def worker(sess_):
                 for _ in range(n_each):
-                    sess_.run(rp, col, kind, acc_off, acc, S, cfg.words)
+                    sess_.run(rp, col, kind, boff, b8in, S, cfg.words)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             ths = [threading.Thread(target=worker, args=(x,)) for x in (asess, sess2)]
@@ -389,16 +407,22 @@ def run_ours(args, rank, world, local):
             torch.cuda.synchronize()
             ms2 = (time.perf_counter() - t0) * 1e3 / (2 * n_each)
             two = {"value": facts_total / (ms2 / 1e3), "ms_per_problem": ms2,
-                   "how": "2 host threads x %d dfx_mfp_acc calls, own handles, wall clock" % n_each}
+                   "how": "2 host threads x %d dfx_mfp_acc8 calls, own handles, wall clock" % n_each}
             del sess2
             eng2.close()
         e2e = {"value": facts_total / (ms / 1e3), "unit": UNIT,
                "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "two_calls_in_flight": two,
-               "path": "dfx_mfp_acc (pinned host buffers): H2D CSR + per-node access lists "
-                       "(uint16 var|kind), expansion to bitplanes, kernels (a)+(b), D2H per-node "
-                       "requirement variable lists (uint16) + row offsets",
-               "accesses": int(acc.shape[0]), "requirements": int(out.vars.shape[0]),
+               "path": "dfx_mfp_acc8 (pinned host buffers): H2D CSR + per-node access lists "
+                       "(byte-coded, include/dfx.h B8), decode to bitplanes, kernels (a)+(b), "
+                       "D2H per-node requirement lists (byte-coded) + int32 row offsets",
+               "accesses": n_acc, "requirements": int(out.vars.shape[0]),
+               "bytes_per_access": float(b8in.nbytes) / max(1, n_acc),
+               "bytes_per_requirement": float(out8.bytes.nbytes) / max(1, out.vars.shape[0]),
+               "lists_u16_path": {
+                   "value": facts_total / (ms_u16 / 1e3), "ms_per_step": ms_u16,
+                   "h2d_bytes_per_step": int(h2d_u16), "d2h_bytes_per_step": int(d2h_u16),
+                   "path": "dfx_mfp_acc: uint16 access lists in, uint16 requirement lists out"},
                "dense_planes_path": {
                    "value": facts_total / (ms_planes / 1e3), "ms_per_step": ms_planes,
                    "h2d_bytes_per_step": int(h2d_planes), "d2h_bytes_per_step": int(d2h_planes),
@@ -420,6 +444,9 @@ def run_ours(args, rank, world, local):
         if e2e is not None:
             lq, lf = out.to_planes()
             bad["e2e_lists"] = int(np.count_nonzero(lq != rq) + np.count_nonzero(lf != rf))
+            lq, lf = out_u16.to_planes()
+            bad["e2e_lists_u16"] = int(np.count_nonzero(lq != rq) + np.count_nonzero(lf != rf))
+            del lq, lf
         ok = all(v == 0 for v in bad.values())
         parity = {"status": "ok" if ok else "MISMATCH", "differing_words": bad,
                   "checked": "all %d variable words x %d nodes of this rank's slab vs "
@@ -437,7 +464,7 @@ def run_ours(args, rank, world, local):
                "output_bytes": int(rows.nbytes)}
     del rows
     if e2e is not None:
-        del out, asess
+        del out, out8, out_u16, asess
     prob.close()
     c4 = None
     if not args.no_c4:

@@ -306,6 +306,42 @@ int dfx_csr_export_acc(dfx_handle *h, dfx_csr *p, int64_t *acc_off, uint16_t *ac
  * D2H of the requirement lists */
 int dfx_mfp_acc(dfx_handle *h, const dfx_acc_in *in, dfx_req_list *out, dfx_csr_stats *stats);
 
+/* Byte-coded lists (B8): the same entries in about 1.2 bytes each instead of
+ * 2, for the host<->device link that bounds the host-buffer call.  Per node,
+ * entries ascend by variable; an entry is one or more bytes
+ *   b = kind << 6 | d:  d == 63 adds 63 and continues, d < 63 ends the entry,
+ * and its variable is prev + 1 + (the sum of its d fields), with prev = -1 at
+ * the start of the node (and, in the output, again where the firstprivate
+ * entries begin).  Input kind: DFX_ACC_READ / DFX_ACC_WRITE / both.  Output
+ * kind: DFX_B8_REQ for a transfer requirement, DFX_B8_FP for a firstprivate
+ * capture (after the node's requirements).  Offsets are int32 (a list of at
+ * most 2^31 - 1 bytes). */
+#define DFX_B8_REQ 1
+#define DFX_B8_FP 2
+
+typedef struct {
+  int64_t n_nodes;
+  int32_t words;                /* V/32: multiple of 4, at most 512 */
+  int64_t nnz;
+  int64_t n_bytes;
+  const int32_t *row_ptr;       /* [n_nodes+1] */
+  const int32_t *col;           /* [nnz] predecessor ids */
+  const uint8_t *node_kind;     /* [n_nodes] 0 host, 1 kernel */
+  const int32_t *byte_off;      /* [n_nodes+1] node n's entries: bytes[byte_off[n] .. byte_off[n+1]) */
+  const uint8_t *bytes;         /* [n_bytes] */
+  const uint32_t *S;            /* [words] scalar-variable mask */
+} dfx_acc8_in;
+
+typedef struct {
+  int32_t *row_off;             /* [n_nodes+1] */
+  uint8_t *bytes;               /* [cap] */
+  int64_t cap;
+  int64_t n_out;                /* out: total bytes (> cap -> DFX_E_NOSPC) */
+} dfx_req8_list;
+
+/* all-in-one host-buffer call on byte-coded lists (same kernels as dfx_mfp_acc) */
+int dfx_mfp_acc8(dfx_handle *h, const dfx_acc8_in *in, dfx_req8_list *out, dfx_csr_stats *stats);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel (c): interprocedural summaries (interproc.py:90-156)              */
 /* ------------------------------------------------------------------------ */

@@ -417,6 +417,146 @@ def _acc_in(row_ptr, col, kind, acc_off, acc, S, words):
     return cin, arrs
 
 
+# ---- byte-coded lists (include/dfx.h "B8") ----------------------------------
+B8_REQ, B8_FP = 1, 2
+
+
+class Acc8In(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("words", C.c_int32), ("nnz", C.c_int64),
+                ("n_bytes", C.c_int64), ("row_ptr", C.c_void_p), ("col", C.c_void_p),
+                ("node_kind", C.c_void_p), ("byte_off", C.c_void_p), ("bytes", C.c_void_p),
+                ("S", C.c_void_p)]
+
+
+class Req8Out(C.Structure):
+    _fields_ = [("row_off", C.c_void_p), ("bytes", C.c_void_p), ("cap", C.c_int64),
+                ("n_out", C.c_int64)]
+
+
+def _b8_encode(node, var, kind, n, restart=None):
+    """Entries (node, var, kind) grouped by node in ascending var order
+    (`restart`: True where a new ascending run starts inside a node) -> (byte
+    offsets int32 [n+1], bytes uint8).  b = kind << 6 | d, d == 63 continues."""
+    var = var.astype(np.int64)
+    first = np.ones(var.shape[0], dtype=bool)
+    first[1:] = node[1:] != node[:-1]
+    if restart is not None:
+        first |= restart
+    prev = np.empty_like(var)
+    prev[0:1] = -1
+    prev[1:] = var[:-1]
+    prev[first] = -1
+    delta = var - prev - 1
+    if (delta < 0).any():
+        raise ValueError("entries must ascend by variable within a node")
+    nb = delta // 63 + 1                                  # bytes per entry
+    end = np.cumsum(nb)
+    out = np.repeat((kind.astype(np.uint8) << 6) | 63, nb).astype(np.uint8)
+    if end.shape[0]:
+        out[end - 1] = ((kind.astype(np.int64) << 6) | (delta % 63)).astype(np.uint8)
+    per_node = np.bincount(node, weights=nb, minlength=n).astype(np.int64)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(per_node, out=off[1:])
+    if off[-1] > 0x7FFFFFFF:
+        raise ValueError("byte-coded lists are limited to 2^31 - 1 bytes")
+    return off.astype(np.int32), out
+
+
+def acc_to_b8(acc_off, acc):
+    """uint16 access lists (var | kind << 14, ascending per node) -> B8."""
+    n = int(acc_off.shape[0]) - 1
+    node = np.repeat(np.arange(n), np.diff(acc_off))
+    a = acc.astype(np.int64)
+    return _b8_encode(node, a & 0x3FFF, a >> 14, n)
+
+
+def b8_decode(off, b, restart_on_kind: bool = False):
+    """B8 lists -> (node int64, var int64, kind uint8) per entry, in order.
+    `restart_on_kind`: requirement lists, whose firstprivate entries restart
+    the ascending run (access lists mix kinds within one run)."""
+    b = np.asarray(b, dtype=np.uint8)
+    n = int(off.shape[0]) - 1
+    node_b = np.repeat(np.arange(n), np.diff(off.astype(np.int64)))
+    d = (b & 63).astype(np.int64)
+    kind = (b >> 6).astype(np.uint8)
+    term = d < 63
+    # a run restarts at each node and where the kind changes inside a node
+    start = np.ones(b.shape[0], dtype=bool)
+    start[1:] = node_b[1:] != node_b[:-1]
+    if restart_on_kind:
+        start[1:] |= kind[1:] != kind[:-1]
+    contrib = d + term
+    cs = np.cumsum(contrib)
+    base = np.maximum.accumulate(np.where(start, cs - contrib, 0))
+    var = cs - base - 1
+    return node_b[term], var[term], kind[term]
+
+
+def req8_to_lists(off, b, words):
+    """B8 requirement lists -> (row_off int64, vars uint16) in the uint16 list
+    form (`REQ_FP_FLAG` on firstprivate entries)."""
+    node, var, kind = b8_decode(off, b, restart_on_kind=True)
+    n = int(off.shape[0]) - 1
+    vals = (var | np.where(kind == B8_FP, REQ_FP_FLAG, 0)).astype(np.uint16)
+    row = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(node, minlength=n), out=row[1:])
+    return ReqList(row, vals, words)
+
+
+@dataclass
+class Req8List:
+    row_off: np.ndarray      # int32 [n+1]
+    bytes: np.ndarray        # uint8 [n_out]
+    words: int
+
+    @property
+    def nbytes(self) -> int:
+        return self.row_off.nbytes + self.bytes.nbytes
+
+    def to_lists(self) -> ReqList:
+        return req8_to_lists(self.row_off, self.bytes, self.words)
+
+
+class Acc8Session:
+    """`AccSession` on byte-coded lists (`dfx_mfp_acc8`): about 1.2 bytes per
+    access in and per planned transfer out instead of 2, the host link being
+    what bounds the call.  Output buffers are reused (optionally pinned)."""
+
+    def __init__(self, eng: _abi.Engine | None = None, alloc=np.empty):
+        self.eng = eng or _abi.engine()
+        _setup(self.eng.lib)
+        self.eng.lib.dfx_mfp_acc8.restype = C.c_int
+        self.alloc = alloc
+        self.capacity = 0
+        self.stats = CsrStats()
+        self._bufs = None
+
+    def run(self, row_ptr, col, kind, byte_off, b, S, words: int) -> Req8List:
+        arrs = [np.ascontiguousarray(a) for a in (row_ptr, col, kind, byte_off, b, S)]
+        row_ptr, col, kind, byte_off, b, S = arrs
+        assert row_ptr.dtype == np.int32 and col.dtype == np.int32 and kind.dtype == np.uint8
+        assert byte_off.dtype == np.int32 and b.dtype == np.uint8 and S.dtype == np.uint32
+        n = int(row_ptr.shape[0]) - 1
+        _check_graph_shapes(n, words, row_ptr, col, kind, S)
+        if byte_off.shape != (n + 1,) or b.shape[0] < int(byte_off[-1]):
+            raise ValueError("byte_off must have n_nodes + 1 entries and bytes at least byte_off[-1]")
+        cin = Acc8In(n, words, int(row_ptr[-1]), int(byte_off[-1]), *(a.ctypes.data for a in arrs))
+        if self.capacity == 0:
+            self.capacity = max(4096, int(byte_off[-1]))
+        while True:
+            if self._bufs is None or self._bufs[1].shape[0] < self.capacity \
+                    or self._bufs[0].shape[0] != n + 1:
+                self._bufs = (self.alloc((n + 1,), np.int32), self.alloc((self.capacity,), np.uint8))
+            row_off, out = self._bufs
+            o = Req8Out(row_off.ctypes.data, out.ctypes.data, out.shape[0], 0)
+            rc = self.eng.lib.dfx_mfp_acc8(self.eng.h, C.byref(cin), C.byref(o), C.byref(self.stats))
+            if rc == _abi.DFX_E_NOSPC:
+                self.capacity = int(o.n_out)
+                continue
+            self.eng.check(rc, "dfx_mfp_acc8")
+            return Req8List(row_off, out[: o.n_out], words)
+
+
 class AccSession:
     """Reference-facing all-in-one host-buffer path on lists (`dfx_mfp_acc`):
     H2D of the CSR and the per-node access lists, expansion, kernels (a)+(b),

@@ -161,6 +161,160 @@ compact_list_kernel(int64_t n_lo, int64_t n_hi, int words, const uint32_t* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// Byte-coded lists (include/dfx.h "B8"): b = kind << 6 | d, d == 63 continues
+// the entry (+63), d < 63 ends it (+d); var = prev + 1 + sum of its d fields.
+// A byte contributes d (+1 if it ends an entry) to a running sum that starts
+// at 0 for the node (and for its firstprivate list): the variable of an
+// entry is the inclusive sum through its last byte, minus 1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_inclusive_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// One warp per node: decode 32 bytes per step (a warp scan gives every
+// entry's variable), OR the entries into shared-memory rows, store the planes.
+__global__ void __launch_bounds__(kWarps * 32)
+expand_b8_kernel(int64_t n_lo, int64_t n_nodes, int words, const int32_t* __restrict__ off,
+                 const uint8_t* __restrict__ bytes, uint32_t* __restrict__ A,
+                 uint32_t* __restrict__ B, uint32_t* __restrict__ USE, int* bad) {
+  extern __shared__ uint32_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* r = sm + (size_t)warp * 2 * words;
+  uint32_t* w = r + words;
+  const int nvars = words * 32;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = n_lo + (int64_t)blockIdx.x * kWarps + warp; n < n_nodes; n += wstride) {
+    for (int i = lane; i < words; i += 32) r[i] = w[i] = 0u;
+    __syncwarp();
+    const int e0 = off[n], e1 = off[n + 1];
+    int carry = 0;
+    for (int e = e0; e < e1; e += 32) {
+      const bool in = e + lane < e1;
+      const uint32_t b = in ? bytes[e + lane] : 63u;     // padding: a continuation adding 0
+      const int d = (int)(b & 63u), end = in && d < 63;
+      const int sum = carry + warp_inclusive_scan(in ? d + end : 0, lane);
+      if (end) {
+        const int v = sum - 1;
+        const uint32_t k = b >> 6;
+        if (v >= nvars || k == 0u) {
+          atomicExch(bad, 1);
+        } else {
+          const uint32_t bit = 1u << (v & 31);
+          if (k & 1u) atomicOr(&r[v >> 5], bit);
+          if (k & 2u) atomicOr(&w[v >> 5], bit);
+        }
+      }
+      carry = __shfl_sync(FULL, sum, 31);
+    }
+    // a node's stream must end with a completed entry
+    if (e1 > e0 && lane == 0 && (bytes[e1 - 1] & 63u) == 63u) atomicExch(bad, 1);
+    __syncwarp();
+    const size_t row = (size_t)n * words;
+    for (int i = 4 * lane; i < words; i += 128) {
+      const uint4 rr = *reinterpret_cast<const uint4*>(r + i);
+      const uint4 ww = *reinterpret_cast<const uint4*>(w + i);
+      __stcs(reinterpret_cast<uint4*>(USE + row + i), rr);
+      __stcs(reinterpret_cast<uint4*>(B + row + i), ww);
+      __stcs(reinterpret_cast<uint4*>(A + row + i),
+             make_uint4(rr.x | ww.x, rr.y | ww.y, rr.z | ww.z, rr.w | ww.w));
+    }
+    __syncwarp();
+  }
+}
+
+// The requirement planes of node n as B8 bytes (write == false: only count
+// them).  Lane l covers words l, l + 32, ...: the previous set variable of a
+// lane's first entry is the last set variable of the lanes below it (warp max
+// scan), or of the chunk before.
+__device__ __forceinline__ int b8_node(int64_t n, int words, const uint32_t* __restrict__ REQ,
+                                       const uint32_t* __restrict__ FPQ,
+                                       const int32_t* __restrict__ fp_slot, int n_fp_slots,
+                                       uint8_t* __restrict__ out, int64_t pos, int64_t cap,
+                                       bool write, int lane) {
+  int total = 0;
+  for (int pass = 0; pass < 2; pass++) {
+    int prev = -1;
+    const uint32_t kb = (pass ? DFX_B8_FP : DFX_B8_REQ) << 6;
+    for (int i0 = 0; i0 < words; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t m = 0u;
+      if (i < words) {
+        if (pass == 0) {
+          m = __ldg(REQ + (size_t)n * words + i);
+        } else {
+          const int slot = fp_slot[i >> 2];
+          if (slot >= 0) m = __ldg(FPQ + ((size_t)n * n_fp_slots + slot) * 4 + (i & 3));
+        }
+      }
+      // previous set variable before this lane's word
+      int last = m ? 32 * i + 31 - __clz(m) : -1;
+      int before = last;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, before, o);
+        if (lane >= o) before = max(before, t);
+      }
+      int p = __shfl_up_sync(FULL, before, 1);
+      if (lane == 0) p = -1;
+      p = max(p, prev);
+      // bytes of this lane's entries
+      int cnt = 0, q = p;
+      for (uint32_t mm = m; mm; mm &= mm - 1) {
+        const int v = 32 * i + __ffs(mm) - 1;
+        cnt += 1 + (v - q - 1) / 63;
+        q = v;
+      }
+      int tot;
+      const int at = warp_exclusive_scan(cnt, lane, &tot);
+      if (write) {
+        int64_t o = pos + total + at;
+        q = p;
+        for (uint32_t mm = m; mm; mm &= mm - 1) {
+          const int v = 32 * i + __ffs(mm) - 1;
+          int dlt = v - q - 1;
+          for (; dlt >= 63; dlt -= 63, o++)
+            if (o < cap) out[o] = (uint8_t)(kb | 63u);
+          if (o < cap) out[o] = (uint8_t)(kb | (uint32_t)dlt);
+          o++;
+          q = v;
+        }
+      }
+      total += tot;
+      prev = max(prev, __shfl_sync(FULL, before, 31));
+    }
+  }
+  return total;
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+count_b8_kernel(int64_t n_lo, int64_t n_hi, int words, const uint32_t* __restrict__ REQ,
+                const uint32_t* __restrict__ FPQ, const int32_t* __restrict__ fp_slot,
+                int n_fp_slots, int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = n_lo + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_hi; n += wstride) {
+    const int c = b8_node(n, words, REQ, FPQ, fp_slot, n_fp_slots, nullptr, 0, 0, false, lane);
+    if (lane == 0) counts[n] = c;
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+compact_b8_kernel(int64_t n_lo, int64_t n_hi, int words, const uint32_t* __restrict__ REQ,
+                  const uint32_t* __restrict__ FPQ, const int32_t* __restrict__ fp_slot,
+                  int n_fp_slots, const int64_t* __restrict__ offsets, uint8_t* __restrict__ out,
+                  int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t n = n_lo + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); n < n_hi; n += wstride)
+    b8_node(n, words, REQ, FPQ, fp_slot, n_fp_slots, out, offsets[n], cap, true, lane);
+}
+
 // Graph validation on the device, before any kernel indexes through the CSR
 // (ADVICE r1): row_ptr[0] == 0, non-decreasing, row_ptr[n] == nnz, every
 // predecessor id in [0, n).  Sets bit 2 of *bad.
@@ -206,6 +360,31 @@ int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* ba
   cudaFuncSetAttribute(expand_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   expand_acc_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, smem, st>>>(n_lo, n_hi, p.words, off,
                                                                          acc, p.A, p.B, p.USE, bad);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int expand_b8(const CsrDev& p, const int32_t* off, const uint8_t* bytes, int* bad, int64_t n_lo,
+              int64_t n_hi, cudaStream_t st) {
+  if (n_hi <= n_lo) return DFX_OK;
+  const size_t smem = (size_t)kWarps * 2 * p.words * sizeof(uint32_t);
+  cudaFuncSetAttribute(expand_b8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  expand_b8_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, smem, st>>>(n_lo, n_hi, p.words, off,
+                                                                        bytes, p.A, p.B, p.USE, bad);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int count_b8(const CsrDev& p, int32_t* counts, int64_t n_lo, int64_t n_hi, cudaStream_t st) {
+  if (n_hi <= n_lo) return DFX_OK;
+  count_b8_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, 0, st>>>(
+      n_lo, n_hi, p.words, p.REQ, p.FPQ, p.fp_slot, p.n_fp_slots, counts);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+int compact_b8(const CsrDev& p, const int64_t* offsets, uint8_t* out, int64_t cap, int64_t n_lo,
+               int64_t n_hi, cudaStream_t st) {
+  if (n_hi <= n_lo) return DFX_OK;
+  compact_b8_kernel<<<grid_nodes(n_hi - n_lo), kWarps * 32, 0, st>>>(
+      n_lo, n_hi, p.words, p.REQ, p.FPQ, p.fp_slot, p.n_fp_slots, offsets, out, cap);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
 

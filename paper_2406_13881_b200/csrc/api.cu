@@ -748,6 +748,8 @@ struct dfx_csr {
   uint32_t* d_occ = nullptr;
   uint16_t* d_vars = nullptr;     // requirement lists (grow-only)
   int64_t vars_cap = 0;
+  uint8_t* d_b8 = nullptr;        // byte-coded requirement lists (grow-only)
+  int64_t b8_cap = 0;
   int* d_bad = nullptr;           // access-list validation flag
   void* d_cnt = nullptr;
   uint8_t* flags = nullptr;
@@ -770,6 +772,7 @@ int csr_destroy_impl(dfx_csr* c) {
   if (c->d_masks) cudaFree(c->d_masks);
   if (c->d_occ) cudaFree(c->d_occ);
   if (c->d_vars) cudaFree(c->d_vars);
+  if (c->d_b8) cudaFree(c->d_b8);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   delete c;
@@ -1138,6 +1141,121 @@ int csr_upload_acc(dfx_handle* h, dfx_csr* c, const dfx_acc_in* in, cudaStream_t
   return DFX_OK;
 }
 
+int check_acc8_in(const dfx_acc8_in* in) {
+  if (!in->row_ptr || !in->node_kind || !in->byte_off || !in->S || (in->nnz && !in->col) ||
+      (in->n_bytes && !in->bytes))
+    return fail(DFX_E_ARG, "dfx_acc8_in: null array");
+  int rc = check_nnz(in->nnz);
+  if (rc) return rc;
+  if (in->n_bytes < 0 || in->n_bytes > 0x7FFFFFFF || in->byte_off[0] != 0 ||
+      in->byte_off[in->n_nodes] != in->n_bytes)
+    return fail(DFX_E_ARG, "dfx_acc8_in: byte_off must run from 0 to n_bytes (< 2^31)");
+  return check_words(in->n_nodes, in->words);
+}
+
+// csr_upload_acc for byte-coded lists: CSR first (validated), then the lists
+// in node ranges on the copy stream, each range decoded into the planes on
+// the compute stream as it lands.
+int csr_upload_acc8(dfx_handle* h, dfx_csr* c, const dfx_acc8_in* in, cudaStream_t st) {
+  dfx::CsrDev& p = c->p;
+  auto* d_off = (int32_t*)dbuf(h, "b8_off", sizeof(int32_t) * (size_t)(in->n_nodes + 1));
+  auto* d_bytes = (uint8_t*)dbuf(h, "b8_in", (size_t)(in->n_bytes > 0 ? in->n_bytes : 1));
+  if (!d_off || !d_bytes) return fail(DFX_E_CUDA, "byte-list buffers: allocation failed");
+  CK(h->pipeline_init());
+  CK(cudaMemcpyAsync(p.row_ptr, in->row_ptr, sizeof(int32_t) * (in->n_nodes + 1), cudaMemcpyHostToDevice, st));
+  if (in->nnz) CK(cudaMemcpyAsync(p.col, in->col, sizeof(int32_t) * in->nnz, cudaMemcpyHostToDevice, st));
+  int rc = validate_csr(c, st);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(p.kind, in->node_kind, in->n_nodes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), st));
+  CK(cudaEventRecord(h->pev[0], st));
+  rc = dfx::build_desc(p, st);
+  if (!rc) rc = dfx::build_succ(p, c->scratch, c->scratch_bytes, c->counts, st);
+  if (rc) return fail(rc, "build_desc/build_succ launch failed");
+  CK(cudaStreamWaitEvent(h->s_copy, h->pev[0], 0));   // buffers free of the previous call
+  const int K = in->n_nodes >= 4096 ? dfx_handle::kPipe : 1;
+  for (int k = 0; k < K; k++) {
+    const int64_t lo = in->n_nodes * k / K, hi = in->n_nodes * (k + 1) / K;
+    const int64_t a = in->byte_off[lo], b = in->byte_off[hi];
+    CK(cudaMemcpyAsync(d_off + lo, in->byte_off + lo, sizeof(int32_t) * (size_t)(hi - lo + 1),
+                       cudaMemcpyHostToDevice, h->s_copy));
+    if (b > a) CK(cudaMemcpyAsync(d_bytes + a, in->bytes + a, (size_t)(b - a), cudaMemcpyHostToDevice,
+                                  h->s_copy));
+    CK(cudaEventRecord(h->pev[1 + k], h->s_copy));
+    CK(cudaStreamWaitEvent(st, h->pev[1 + k], 0));
+    rc = dfx::expand_b8(p, d_off, d_bytes, c->d_bad, lo, hi, st);
+    if (rc) return fail(rc, "expand_b8 launch failed");
+  }
+  return DFX_OK;
+}
+
+__global__ void offsets_i32_kernel(const int64_t* in, int32_t* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
+// dfx_csr_requirements_list for byte-coded lists: kernel (b), byte counts,
+// scan and encoding per node range, each range's bytes going home on the D2H
+// stream while the next range is computed.
+int requirements_b8(dfx_handle* h, dfx_csr* c, dfx_req8_list* out, dfx_csr_stats* stats) {
+  CK(h->pipeline_init());
+  cudaStream_t st = h->st();
+  const dfx::CsrDev& p = c->p;
+  const int64_t want = out->bytes ? out->cap : 0;
+  if (want > c->b8_cap) {
+    if (c->d_b8) cudaFree(c->d_b8);
+    c->d_b8 = nullptr;
+    c->b8_cap = 0;
+    CK(cudaMalloc(&c->d_b8, (size_t)want));
+    c->b8_cap = want;
+  }
+  auto* d_off32 = (int32_t*)dbuf(h, "b8_out_off", sizeof(int32_t) * (size_t)(p.n_nodes + 1));
+  if (!d_off32) return fail(DFX_E_CUDA, "byte-list offsets: allocation failed");
+  const int K = p.n_nodes >= 4096 && want ? dfx_handle::kPipe : 1;
+  CK(cudaMemsetAsync(c->offsets, 0, sizeof(int64_t), st));
+  CK(cudaEventRecord(c->e0, st));
+  for (int k = 0; k < K; k++) {
+    const int lo = (int)(p.n_nodes * k / K), hi = (int)(p.n_nodes * (k + 1) / K);
+    int rc = dfx::requirements_range(p, c->counts, c->offsets, c->scratch, c->scratch_bytes, lo, hi,
+                                     st, true);
+    if (!rc && want) rc = dfx::compact_b8(p, c->offsets, c->d_b8, want, lo, hi, st);
+    if (rc) return fail(rc, "requirements failed: %s", cudaGetErrorString(cudaGetLastError()));
+    CK(cudaMemcpyAsync(h->pin_cnt + k, c->offsets + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(h->pev[1 + dfx_handle::kPipeMax + k], st));
+  }
+  offsets_i32_kernel<<<148 * 4, 256, 0, st>>>(c->offsets, d_off32, p.n_nodes + 1);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->e1, st));
+  int64_t done = 0;
+  for (int k = 0; k < K; k++) {
+    CK(cudaEventSynchronize(h->pev[1 + dfx_handle::kPipeMax + k]));
+    int64_t end = (int64_t)h->pin_cnt[k];
+    if (end > want) end = want;
+    if (want && end > done)
+      CK(cudaMemcpyAsync(out->bytes + done, c->d_b8 + done, (size_t)(end - done),
+                         cudaMemcpyDeviceToHost, h->s_d2h));
+    if (end > done) done = end;
+  }
+  const int64_t n_out = (int64_t)h->pin_cnt[K - 1];
+  if (n_out > 0x7FFFFFFF) return fail(DFX_E_LIMIT, "byte-coded requirement lists exceed 2^31 bytes");
+  if (out->row_off) {
+    CK(cudaEventSynchronize(c->e1));
+    CK(cudaMemcpyAsync(out->row_off, d_off32, sizeof(int32_t) * (size_t)(p.n_nodes + 1),
+                       cudaMemcpyDeviceToHost, h->s_d2h));
+  }
+  CK(cudaStreamSynchronize(h->s_d2h));
+  out->n_out = n_out;
+  if (stats) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    stats->req_ms = ms;
+    stats->n_masks = n_out;
+  }
+  if (want && n_out > want)
+    return fail(DFX_E_NOSPC, "byte-list capacity %lld < %lld", (long long)want, (long long)n_out);
+  return DFX_OK;
+}
+
 int check_bad(dfx_csr* c, const dfx_acc_in* in, cudaStream_t st) {
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1267,6 +1385,35 @@ int dfx_mfp_acc(dfx_handle* h, const dfx_acc_in* in, dfx_req_list* out, dfx_csr_
   if (!rc) rc = dfx_csr_solve(h, c, 0, stats);    // synchronises: the flag is final
   if (!rc) rc = check_bad(c, in, h->st());
   if (!rc) rc = dfx_csr_requirements_list(h, c, out, stats);
+  return rc;
+}
+
+int dfx_mfp_acc8(dfx_handle* h, const dfx_acc8_in* in, dfx_req8_list* out, dfx_csr_stats* stats) {
+  if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_mfp_acc8: null argument");
+  CK(cudaSetDevice(h->device));
+  int rc = check_acc8_in(in);
+  if (rc) return rc;
+  dfx_csr* c = h->csr_cache;
+  if (c && (c->p.n_nodes != in->n_nodes || c->p.words != in->words || c->p.nnz != in->nnz ||
+            !same_scalars(c, in->S, in->words))) {
+    csr_destroy_impl(c);
+    c = h->csr_cache = nullptr;
+  }
+  if (!c) {
+    c = new dfx_csr();
+    rc = csr_alloc_all(c, in->n_nodes, in->words, in->nnz, in->S);
+    if (rc) { csr_destroy_impl(c); return rc; }
+    h->csr_cache = c;
+  }
+  rc = csr_upload_acc8(h, c, in, h->st());
+  if (!rc) rc = dfx_csr_solve(h, c, 0, stats);    // synchronises: the flag is final
+  if (!rc) {
+    int bad = 0;
+    CK(cudaMemcpy(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (bad) rc = fail(DFX_E_ARG, "byte-coded access list: variable >= %d, kind 0 or an "
+                                  "unterminated entry", 32 * in->words);
+  }
+  if (!rc) rc = requirements_b8(h, c, out, stats);
   return rc;
 }
 

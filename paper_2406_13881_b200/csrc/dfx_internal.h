@@ -118,11 +118,16 @@ int scan_counts(int64_t n, const int32_t* counts, int64_t* offsets, void* scratc
 int expand_acc(const CsrDev& p, const int64_t* off, const uint16_t* acc, int* bad, int64_t n_lo,
                int64_t n_hi, cudaStream_t st);
 int count_acc(const CsrDev& p, int32_t* counts, cudaStream_t st);
+int expand_b8(const CsrDev& p, const int32_t* off, const uint8_t* bytes, int* bad, int64_t n_lo,
+              int64_t n_hi, cudaStream_t st);
+int count_b8(const CsrDev& p, int32_t* counts, int64_t n_lo, int64_t n_hi, cudaStream_t st);
+int compact_b8(const CsrDev& p, const int64_t* offsets, uint8_t* out, int64_t cap, int64_t n_lo,
+               int64_t n_hi, cudaStream_t st);
 int export_acc(const CsrDev& p, const int64_t* off, uint16_t* acc, cudaStream_t st);
 int compact_list(const CsrDev& p, const int64_t* offsets, uint16_t* vars, int64_t cap,
                  int64_t n_lo, int64_t n_hi, cudaStream_t st);
 int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
-                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st);
+                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st, bool b8 = false);
 size_t scan_scratch_bytes(int64_t n);
 size_t round_ctl_bytes();
 

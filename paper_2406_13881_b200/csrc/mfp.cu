@@ -840,7 +840,7 @@ __global__ void add_base_kernel(int64_t* out, int64_t len, const int64_t* base) 
 }
 
 int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void* scratch,
-                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st) {
+                       size_t scratch_bytes, int n_lo, int n_hi, cudaStream_t st, bool b8) {
   const int vpl = vpl_for(p.words);
   const int n = n_hi - n_lo;
   if (n <= 0) return DFX_OK;
@@ -851,6 +851,9 @@ int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void*
     case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
     default: return DFX_E_LIMIT;
   }
+  // byte-coded lists: the offsets count bytes, not entries
+  if (b8)
+    if (int rc = count_b8(p, counts, n_lo, n_hi, st)) return rc;
   if (int rc = inclusive_scan(counts + n_lo, offsets + n_lo + 1, (int64_t)n, scratch, scratch_bytes, st))
     return rc;
   add_base_kernel<<<grid_for(n, 256), 256, 0, st>>>(offsets + n_lo + 1, n, offsets + n_lo);

@@ -229,31 +229,36 @@ expand_b8_kernel(int64_t n_lo, int64_t n_nodes, int words, const int32_t* __rest
 }
 
 // The requirement planes of node n as B8 bytes (write == false: only count
-// them).  Lane l covers words l, l + 32, ...: the previous set variable of a
-// lane's first entry is the last set variable of the lanes below it (warp max
-// scan), or of the chunk before.
+// them).  Lane l covers the 128-variable quad l (+32, ...), loaded as one
+// 16-byte vector: the previous set variable of a lane's first entry is the
+// last set variable of the lanes below it (warp max scan), or of the quads
+// before.
 __device__ __forceinline__ int b8_node(int64_t n, int words, const uint32_t* __restrict__ REQ,
                                        const uint32_t* __restrict__ FPQ,
                                        const int32_t* __restrict__ fp_slot, int n_fp_slots,
                                        uint8_t* __restrict__ out, int64_t pos, int64_t cap,
                                        bool write, int lane) {
+  const int nq = words >> 2;
   int total = 0;
   for (int pass = 0; pass < 2; pass++) {
     int prev = -1;
     const uint32_t kb = (pass ? DFX_B8_FP : DFX_B8_REQ) << 6;
-    for (int i0 = 0; i0 < words; i0 += 32) {
-      const int i = i0 + lane;
-      uint32_t m = 0u;
-      if (i < words) {
+    for (int q0 = 0; q0 < nq; q0 += 32) {
+      const int q = q0 + lane;
+      uint4 m = make_uint4(0u, 0u, 0u, 0u);
+      if (q < nq) {
         if (pass == 0) {
-          m = __ldg(REQ + (size_t)n * words + i);
+          m = __ldg(reinterpret_cast<const uint4*>(REQ + (size_t)n * words) + q);
         } else {
-          const int slot = fp_slot[i >> 2];
-          if (slot >= 0) m = __ldg(FPQ + ((size_t)n * n_fp_slots + slot) * 4 + (i & 3));
+          const int slot = fp_slot[q];
+          if (slot >= 0) m = __ldg(reinterpret_cast<const uint4*>(FPQ) + (size_t)n * n_fp_slots + slot);
         }
       }
-      // previous set variable before this lane's word
-      int last = m ? 32 * i + 31 - __clz(m) : -1;
+      const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+      int last = -1;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (mw[k]) last = 128 * q + 32 * k + 31 - __clz(mw[k]);
       int before = last;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -264,26 +269,30 @@ __device__ __forceinline__ int b8_node(int64_t n, int words, const uint32_t* __r
       if (lane == 0) p = -1;
       p = max(p, prev);
       // bytes of this lane's entries
-      int cnt = 0, q = p;
-      for (uint32_t mm = m; mm; mm &= mm - 1) {
-        const int v = 32 * i + __ffs(mm) - 1;
-        cnt += 1 + (v - q - 1) / 63;
-        q = v;
-      }
+      int cnt = 0, v0 = p;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        for (uint32_t mm = mw[k]; mm; mm &= mm - 1) {
+          const int v = 128 * q + 32 * k + __ffs(mm) - 1;
+          cnt += 1 + (v - v0 - 1) / 63;
+          v0 = v;
+        }
       int tot;
       const int at = warp_exclusive_scan(cnt, lane, &tot);
       if (write) {
         int64_t o = pos + total + at;
-        q = p;
-        for (uint32_t mm = m; mm; mm &= mm - 1) {
-          const int v = 32 * i + __ffs(mm) - 1;
-          int dlt = v - q - 1;
-          for (; dlt >= 63; dlt -= 63, o++)
-            if (o < cap) out[o] = (uint8_t)(kb | 63u);
-          if (o < cap) out[o] = (uint8_t)(kb | (uint32_t)dlt);
-          o++;
-          q = v;
-        }
+        v0 = p;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          for (uint32_t mm = mw[k]; mm; mm &= mm - 1) {
+            const int v = 128 * q + 32 * k + __ffs(mm) - 1;
+            int dlt = v - v0 - 1;
+            for (; dlt >= 63; dlt -= 63, o++)
+              if (o < cap) out[o] = (uint8_t)(kb | 63u);
+            if (o < cap) out[o] = (uint8_t)(kb | (uint32_t)dlt);
+            o++;
+            v0 = v;
+          }
       }
       total += tot;
       prev = max(prev, __shfl_sync(FULL, before, 31));

@@ -1405,8 +1405,13 @@ int dfx_mfp_acc8(dfx_handle* h, const dfx_acc8_in* in, dfx_req8_list* out, dfx_c
     if (rc) { csr_destroy_impl(c); return rc; }
     h->csr_cache = c;
   }
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   rc = csr_upload_acc8(h, c, in, h->st());
+  if (h->trace) CK(cudaStreamSynchronize(h->st()));
+  const auto t1 = now();
   if (!rc) rc = dfx_csr_solve(h, c, 0, stats);    // synchronises: the flag is final
+  const auto t2 = now();
   if (!rc) {
     int bad = 0;
     CK(cudaMemcpy(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1414,6 +1419,12 @@ int dfx_mfp_acc8(dfx_handle* h, const dfx_acc8_in* in, dfx_req8_list* out, dfx_c
                                   "unterminated entry", 32 * in->words);
   }
   if (!rc) rc = requirements_b8(h, c, out, stats);
+  if (h->trace) {
+    const auto t3 = now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[dfx_mfp_acc8] upload+expand %.3f ms, solve %.3f ms, requirements+D2H %.3f ms\n",
+            ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
   return rc;
 }
 

@@ -566,6 +566,40 @@ mfp_phase_kernel(CsrDev p, int q0, int chunk_nodes, int n_chunks, RoundCtl* ctl,
 // ---------------------------------------------------------------------------
 // kernel (b): requirement planes + per-node nonzero-word counts
 // ---------------------------------------------------------------------------
+// Bytes of one ascending list in the B8 coding (include/dfx.h) whose bits are
+// spread as quads: lane l holds quads l, l + 32, ... (uniform across the warp)
+template <int VPL>
+__device__ __forceinline__ int b8_bytes(const uint4 (&m)[VPL], int lane) {
+  int total = 0, prev = -1;
+#pragma unroll
+  for (int v = 0; v < VPL; v++) {
+    const int q = lane + 32 * v;
+    const uint32_t mw[4] = {m[v].x, m[v].y, m[v].z, m[v].w};
+    int last = -1;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (mw[k]) last = 128 * q + 32 * k + 31 - __clz(mw[k]);
+    int before = last;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, before, o);
+      if (lane >= o) before = max(before, t);
+    }
+    int p = __shfl_up_sync(FULL, before, 1);
+    if (lane == 0) p = -1;
+    int v0 = max(p, prev), cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      for (uint32_t mm = mw[k]; mm; mm &= mm - 1) {
+        const int var = 128 * q + 32 * k + __ffs(mm) - 1;
+        cnt += 1 + (var - v0 - 1) / 63;
+        v0 = var;
+      }
+    total += (int)__reduce_add_sync(FULL, (unsigned)cnt);
+    prev = max(prev, __shfl_sync(FULL, before, 31));
+  }
+  return total;
+}
 template <int VPL>
 __global__ void __launch_bounds__(256)
 requirements_kernel(CsrDev p, int32_t* counts, int count_bits, int n_lo, int n_hi) {
@@ -607,8 +641,10 @@ requirements_kernel(CsrDev p, int32_t* counts, int count_bits, int n_lo, int n_h
         }
     }
     int cnt = 0;
+    uint4 rq[VPL], fq[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; v++) {
+      rq[v] = fq[v] = zero4();
       if (!active[v]) continue;
       const int q = lane + 32 * v;
       const uint4 use = ldg4(U + row + q);
@@ -621,17 +657,23 @@ requirements_kernel(CsrDev p, int32_t* counts, int count_bits, int n_lo, int n_h
         req = or4(andn4(andn4(use, f), id[v]), andn4(andn4(f, id[v]), ih[v]));
         fp = and4(andn4(f, id[v]), ih[v]);
       }
+      rq[v] = req;
       __stcs(REQ + row + q, req);
       cnt += count_bits ? __popc(req.x) + __popc(req.y) + __popc(req.z) + __popc(req.w)
                         : (req.x != 0) + (req.y != 0) + (req.z != 0) + (req.w != 0);
       if (p.fp_slot[q] >= 0) {
+        fq[v] = fp;
         FPQ[(size_t)n * p.n_fp_slots + p.fp_slot[q]] = fp;
         cnt += count_bits ? __popc(fp.x) + __popc(fp.y) + __popc(fp.z) + __popc(fp.w)
                           : (fp.x != 0) + (fp.y != 0) + (fp.z != 0) + (fp.w != 0);
       }
     }
+    if (count_bits == 2) {      // byte-coded lists: the node's bytes (requirements, then captures)
+      cnt = b8_bytes<VPL>(rq, lane) + b8_bytes<VPL>(fq, lane);
+    } else {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+      for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    }
     if (lane == 0) counts[n] = cnt;
   }
 }
@@ -846,14 +888,12 @@ int requirements_range(const CsrDev& p, int32_t* counts, int64_t* offsets, void*
   if (n <= 0) return DFX_OK;
   int blocks = grid_for((int64_t)n * 32, 256);
   switch (vpl) {
-    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
-    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
-    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, 1, n_lo, n_hi); break;
+    // byte-coded lists (b8): the counts are bytes, not entries
+    case 1: requirements_kernel<1><<<blocks, 256, 0, st>>>(p, counts, b8 ? 2 : 1, n_lo, n_hi); break;
+    case 2: requirements_kernel<2><<<blocks, 256, 0, st>>>(p, counts, b8 ? 2 : 1, n_lo, n_hi); break;
+    case 4: requirements_kernel<4><<<blocks, 256, 0, st>>>(p, counts, b8 ? 2 : 1, n_lo, n_hi); break;
     default: return DFX_E_LIMIT;
   }
-  // byte-coded lists: the offsets count bytes, not entries
-  if (b8)
-    if (int rc = count_b8(p, counts, n_lo, n_hi, st)) return rc;
   if (int rc = inclusive_scan(counts + n_lo, offsets + n_lo + 1, (int64_t)n, scratch, scratch_bytes, st))
     return rc;
   add_base_kernel<<<grid_for(n, 256), 256, 0, st>>>(offsets + n_lo + 1, n, offsets + n_lo);

@@ -154,6 +154,18 @@ typedef struct {
 /* Host buffers in, host buffers out (H2D + kernel + D2H). */
 int dfx_replay_batch(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
 
+/* dfx_replay_batch with the ops packed into 8 bytes each (half the host->
+ * device bytes of the ops): in->ops points at n_ops pairs of uint32
+ *   word 0: opcode (bits 0-3) | flags >> 8 (bits 4-8) | c (bits 9-31)
+ *   word 1: a (bits 0-15) | b (bits 16-31)
+ * where, by opcode, the op words 1-3 of the 16-byte form are
+ *   HR, DR: (a, b, c)   HW, DW: (a, b, 0)   BR_END: (c, b, 0)
+ *   LOOP_BEGIN: (a, 0, 0)   LOOP_END: (c, 0, 0)   ERR: (a, b, 0)   others: 0.
+ * The device unpacks each function range as it lands, before its region
+ * table; a batch whose fields do not fit (variables or statements beyond
+ * 65535, offsets beyond 2^23) must use dfx_replay_batch. */
+int dfx_replay_batch_packed(dfx_handle *h, const dfx_replay_in *in, dfx_replay_out *out);
+
 /* Device-resident batch (configuration C4 timing): upload once, replay many
  * times; dfx_replay_run leaves events/bits on the device and reports counts. */
 typedef struct dfx_replay dfx_replay;

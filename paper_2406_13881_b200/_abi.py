@@ -70,6 +70,9 @@ EV_ERR_DATAMAP, EV_ERR_BRACES_LOOP, EV_ERR_BRACES_ARM, EV_ERR_DECL, EV_ERR_ENGIN
 POS_BEFORE, POS_AFTER, POS_BODY_END, POS_KERNEL = 0, 1, 2, 3
 OUT_PRESENCE, OUT_TO, OUT_FROM, OUT_H, OUT_D = 1, 2, 4, 8, 16
 FN_NO_ERR_SITES = 1          # dfx_fn_desc.flags (include/dfx.h)
+# opcodes (include/dfx.h; lower.py emits them)
+(OP_END, OP_HR, OP_HW, OP_DR, OP_DW, OP_BR_BEGIN, OP_ARM_FORK, OP_ARM_CLOSE, OP_ARM_PASSIVE,
+ OP_BR_END, OP_LOOP_BEGIN, OP_LOOP_END, OP_ERR) = range(13)
 
 DFX_OK, DFX_E_ARG, DFX_E_CUDA, DFX_E_NOSPC, DFX_E_LIMIT = 0, -1, -2, -3, -4
 
@@ -129,7 +132,7 @@ def load_lib(path: str | os.PathLike | None = None) -> C.CDLL:
     lib = C.CDLL(str(p))
     lib.dfx_last_error.restype = C.c_char_p
     lib.dfx_abi_version.restype = C.c_int
-    for name in ("dfx_open", "dfx_close", "dfx_replay_batch"):
+    for name in ("dfx_open", "dfx_close", "dfx_replay_batch", "dfx_replay_batch_packed"):
         getattr(lib, name).restype = C.c_int
     if lib.dfx_abi_version() != ABI_VERSION:
         raise EngineError("libdfx ABI %d != %d" % (lib.dfx_abi_version(), ABI_VERSION))

@@ -358,7 +358,17 @@ int dfx_replay_destroy(dfx_handle* h, dfx_replay* rp) {
 // E1: dfx_replay_batch  (replaces dartomp.dataflow.analyze_function,
 // pkg/src/dartomp/dataflow.py:737-740, batched over functions)
 // ---------------------------------------------------------------------------
+static int replay_batch_impl(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out, bool packed);
+
 int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out) {
+  return replay_batch_impl(h, in, out, false);
+}
+
+int dfx_replay_batch_packed(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out) {
+  return replay_batch_impl(h, in, out, true);
+}
+
+static int replay_batch_impl(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out, bool packed) {
   if (!h || !in || !out) return fail(DFX_E_ARG, "dfx_replay_batch: null argument");
   CK(cudaSetDevice(h->device));
   const int nf = in->n_funcs;
@@ -417,6 +427,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   cudaStream_t st = h->st();
   void* d_fns = dbuf(h, "fns", sizeof(dfx_fn_desc) * (size_t)nf + 16);
   void* d_ops = dbuf(h, "ops", sizeof(int32_t) * 4 * (size_t)in->n_ops + 16);
+  void* d_pk = packed ? dbuf(h, "ops_packed", sizeof(uint32_t) * 2 * (size_t)in->n_ops + 16) : d_ops;
   void* d_vf = dbuf(h, "vf", sizeof(int32_t) * (size_t)in->n_vars + 16);
   void* d_span = dbuf(h, "span", sizeof(int32_t) * 2 * (size_t)in->n_stmts + 16);
   void* d_sites = dbuf(h, "sites", sizeof(int32_t) * (size_t)in->n_sites + 16);
@@ -446,7 +457,7 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
   // timed_out[1] (ints), then ev_off[K] ev_cap[K] (long long)
   const size_t gate_ints = (size_t)(K + 1) + 3 * (size_t)K + 4;
   auto* d_gate = (int*)dbuf(h, "gate", sizeof(int) * gate_ints + 16 + 2 * sizeof(long long) * K);
-  if (!d_fns || !d_ops || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
+  if (!d_fns || !d_ops || !d_pk || !d_vf || !d_span || !d_sites || !d_arms || !d_ifn || !d_ich || !d_ev ||
       !d_cnt || !d_vout || !d_gate || !d_iwf || !d_iwc)
     return fail(DFX_E_CUDA, "dfx_replay_batch: device allocation failed");
   int* g_cut = d_gate;
@@ -540,12 +551,19 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
       // each copy runs 128 B into the next range's data, so no L1 line a
       // range's warps read holds bytes not yet copied (the next copy writes
       // the same bytes again)
-      Rng rng[] = {{in->ops, d_ops, ops_a, ops_b, in->n_ops, 4},
+      // packed ops: exactly the range (unpacked on the device below; a range's
+      // ops start and end on 128-B lines of the 16-byte form)
+      if (packed && ops_b > ops_a)
+        CK(cudaMemcpyAsync((uint32_t*)d_pk + 2 * ops_a, (const uint32_t*)(const void*)in->ops + 2 * ops_a,
+                           sizeof(uint32_t) * 2 * (size_t)(ops_b - ops_a), cudaMemcpyHostToDevice,
+                           h->s_copy));
+      Rng rng[] = {{packed ? nullptr : in->ops, d_ops, ops_a, ops_b, in->n_ops, 4},
                    {in->var_flags, d_vf, vf_a, vf_b, in->n_vars, 1},
                    {in->stmt_span, d_span, sp_a, sp_b, in->n_stmts, 2},
                    {in->sites, d_sites, si_a, si_b, in->n_sites, 1},
                    {in->arms, d_arms, ar_a, ar_b, in->n_arms, 2}};
       for (auto& g : rng) {
+        if (!g.src) continue;
         int64_t e = g.b + 32 / g.unit;
         if (e > g.n) e = g.n;
         if (e > g.a)
@@ -558,6 +576,12 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     if (h->trace) CK(cudaEventRecord(h->tev[3 * k], h->s_copy));
     cudaStream_t s_reg = s_regs[k & 1];
     CK(cudaStreamWaitEvent(s_reg, h->pev[1 + k], 0));
+    if (packed && f0 < f1) {
+      const int64_t ops_a = K == 1 ? 0 : lo(f0, &dfx_fn_desc::op_off);
+      const int64_t ops_b = K == 1 || f1 == nf ? in->n_ops : lo(f1, &dfx_fn_desc::op_off);
+      int rcu = dfx::unpack_ops_launch((const uint32_t*)d_pk, (int32_t*)d_ops, ops_a, ops_b, s_reg);
+      if (rcu != DFX_OK) return fail(rcu, "unpack_ops launch failed");
+    }
     int rc = dfx::region_launch(r, f0, f1, s_reg);
     if (rc != DFX_OK) return fail(rc, "region_kernel launch failed");
     CK(cudaMemcpyAsync(g_ready + k, h->pin_one + k, sizeof(int), cudaMemcpyHostToDevice, s_reg));
@@ -583,7 +607,14 @@ int dfx_replay_batch(dfx_handle* h, const dfx_replay_in* in, dfx_replay_out* out
     cudaStreamSynchronize(h->s_copy);
     cudaStreamSynchronize(st);
     dfx_replay* rp = nullptr;
-    int rc = dfx_replay_create(h, in, out->event_cap > 0 ? out->event_cap : 1, &rp);
+    dfx_replay_in in16 = *in;
+    std::vector<int32_t> ops16;
+    if (packed) {      // the device-resident path takes the 16-byte form
+      ops16.resize(4 * (size_t)in->n_ops);
+      dfx::unpack_ops_host((const uint32_t*)(const void*)in->ops, ops16.data(), in->n_ops);
+      in16.ops = ops16.data();
+    }
+    int rc = dfx_replay_create(h, &in16, out->event_cap > 0 ? out->event_cap : 1, &rp);
     if (rc) return rc;
     int64_t n_ev = 0;
     float kms = 0.f;

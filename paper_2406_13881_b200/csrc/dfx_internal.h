@@ -49,6 +49,9 @@ struct GateDev {
 
 // region tables of functions [fn_lo, fn_hi) (replay.cu region_kernel)
 int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream);
+// packed ops (dfx_replay_batch_packed): device unpack of [lo, hi), host unpack of n
+int unpack_ops_launch(const uint32_t* packed, int32_t* ops, int64_t lo, int64_t hi, cudaStream_t st);
+void unpack_ops_host(const uint32_t* packed, int32_t* ops, int64_t n);
 // replay (persistent grid); with `gate`, items wait for their range's ready
 // flag and the region tables are the caller's (region_launch per range)
 // (without a gate, the wide items follow in a second launch on the stream)

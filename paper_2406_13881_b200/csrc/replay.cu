@@ -677,7 +677,7 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
   }
 }
 
-// Region table, one thread per function (runs before the replay of the same
+// Region table, one warp per function (runs before the replay of the same
 // function range, on the same stream).  For every BR_BEGIN / LOOP_BEGIN it
 // writes into the device copy of the program
 //   begin.z = chunk mask: bit (v >> 5) & 31 for every variable v accessed
@@ -694,79 +694,141 @@ replay_kernel(const dfx_fn_desc* __restrict__ fns, const int32_t* __restrict__ o
 //             identity across it)
 // Idempotent; fields the replay reads from these ops are untouched.
 constexpr int kRegionStack = Narrow::kMaxBr + Narrow::kMaxLoop;
-__global__ void __launch_bounds__(32)
+constexpr int kRegionWarps = 8;
+
+// One warp per function, 32 ops per step: a step without region ops (most
+// of them) folds its accesses into the open region with two warp OR
+// reductions and a population count; the region ops of a step are taken in
+// order, the accesses between them folded segment by segment.  The walk's
+// state is uniform across the warp (every lane computes the same values);
+// the stack of enclosing regions lives in shared memory, written by lane 0.
+// (A thread-per-function walk sat on the critical path of the pipelined
+// host-buffer call: ranges opened ~50 ms after their programs had landed.)
+__global__ void __launch_bounds__(kRegionWarps * 32)
 region_kernel(const dfx_fn_desc* __restrict__ fns, int4* __restrict__ ops, int fn_lo, int fn_hi) {
-  const int f = fn_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  struct Frame { int64_t dyn; int pc; uint32_t mask, wmask; int br; };
+  __shared__ Frame stk_all[kRegionWarps][kRegionStack + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = fn_lo + blockIdx.x * kRegionWarps + warp;
   if (f >= fn_hi) return;
+  Frame* stk = stk_all[warp];
   const dfx_fn_desc d = fns[f];
   int4* o = ops + d.op_off;
-  // the open region's accumulators live in registers; the stack (local
-  // memory) holds the enclosing regions' and is touched only at BEGIN / END
-  int32_t st_pc[kRegionStack + 1];
-  uint32_t st_mask[kRegionStack + 1], st_wmask[kRegionStack + 1];
-  int64_t st_dyn[kRegionStack + 1];
-  bool st_br[kRegionStack + 1];
   int cpc = -1;          // begin pc of the open region (-1: the function body)
   uint32_t cmask = 0u, cwmask = 0u;
   int64_t cdyn = 0;
-  bool cbr = false;
+  int cbr = 0;
   int sp = 0, deep = 0;  // sp: enclosing regions stacked; deep: beyond the stack (never skipped)
-  // (code, var) words of 8 ops per batch of independent loads: the stores
-  // below touch only words 2-3, so one memory latency per batch, not per op
-  constexpr int kBatch = 8;
-  int2 buf[kBatch];
-  for (int pc = 0; pc < d.n_ops; pc++) {
-    if ((pc & (kBatch - 1)) == 0) {
-#pragma unroll
-      for (int i = 0; i < kBatch; i++)
-        buf[i] = pc + i < d.n_ops ? __ldcg(reinterpret_cast<const int2*>(o + pc + i))
-                                  : make_int2(DFX_OP_END, 0);
-    }
-    int2 op = buf[0];
-#pragma unroll
-    for (int i = 1; i < kBatch; i++)
-      if ((pc & (kBatch - 1)) == i) op = buf[i];
+  for (int base = 0; base < d.n_ops; base += 32) {
+    const int pc = base + lane;
+    const int2 op = pc < d.n_ops ? __ldcg(reinterpret_cast<const int2*>(o + pc))
+                                 : make_int2(DFX_OP_END, 0);
     const int code = op.x & 0xFF;
-    if (code == DFX_OP_END) break;
-    if (code >= DFX_OP_HR && code <= DFX_OP_DW) {
-      cmask |= 1u << ((op.y >> 5) & 31);
-      if (code == DFX_OP_HW || code == DFX_OP_DW) cwmask |= 1u << ((op.y >> 5) & 31);
-      cdyn++;
-    } else if (code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN) {
-      o[pc].z = -1;          // until its end is seen
-      if (deep || sp == kRegionStack) { deep++; cmask = ~0u; continue; }
-      st_pc[sp] = cpc; st_mask[sp] = cmask; st_wmask[sp] = cwmask; st_dyn[sp] = cdyn; st_br[sp] = cbr;
-      sp++;
-      cpc = pc; cmask = 0u; cwmask = 0u; cdyn = 0; cbr = code == DFX_OP_BR_BEGIN;
-    } else if (code == DFX_OP_BR_END || code == DFX_OP_LOOP_END) {
-      if (deep) { deep--; continue; }
-      if (sp == 0) continue; // unbalanced
-      const int b = cpc;
-      const bool loop = code == DFX_OP_LOOP_END;
-      const int64_t dyn = loop ? 3 + 2 * cdyn : 2 + cdyn;
-      uint32_t mask = cmask;
-      if (dyn > 0x7FFFFFFF || loop == cbr) mask = ~0u;   // too long, or mismatched
-      o[b].z = (int)mask;
-      o[b].w = pc - b;
-      if (loop) o[pc].z = (int)cwmask;
-      o[pc].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (cbr ? 0x80000000u : 0u));
-      const bool br = cbr;
-      sp--;
-      cpc = st_pc[sp]; cmask = st_mask[sp] | mask; cwmask = st_wmask[sp] | cwmask;
-      cdyn = st_dyn[sp] + dyn; cbr = st_br[sp] | br;
-    } else {
-      if (code == DFX_OP_ERR) cmask = ~0u;
-      cdyn++;
+    const bool acc = code >= DFX_OP_HR && code <= DFX_OP_DW;
+    const bool wr = code == DFX_OP_HW || code == DFX_OP_DW;
+    const bool ctl = code == DFX_OP_END || code == DFX_OP_BR_BEGIN || code == DFX_OP_LOOP_BEGIN ||
+                     code == DFX_OP_BR_END || code == DFX_OP_LOOP_END;
+    const uint32_t bit = acc ? 1u << ((op.y >> 5) & 31) : 0u;
+    unsigned ctlm = __ballot_sync(0xFFFFFFFFu, ctl);
+    int s = 0;             // first lane of the current segment
+    bool done = false;
+    for (;;) {
+      // fold the segment [s, next region op) into the open region: accesses
+      // set chunk bits, an ERR op marks it never skipped, every op counts 1
+      const unsigned lo = s >= 32 ? 0u : 0xFFFFFFFFu << s;
+      const unsigned hi = ctlm ? (1u << (__ffs(ctlm) - 1)) - 1u : 0xFFFFFFFFu;
+      const unsigned seg = lo & hi;
+      const bool in = (seg >> lane) & 1u;
+      cmask |= __reduce_or_sync(0xFFFFFFFFu, in ? bit : 0u);
+      cwmask |= __reduce_or_sync(0xFFFFFFFFu, in && wr ? bit : 0u);
+      if (__any_sync(0xFFFFFFFFu, in && code == DFX_OP_ERR)) cmask = ~0u;
+      cdyn += __popc(seg);
+      if (!ctlm) break;
+      const int j = __ffs(ctlm) - 1;
+      ctlm &= ctlm - 1;
+      s = j + 1;
+      const int cj = __shfl_sync(0xFFFFFFFFu, code, j);
+      const int pcj = base + j;
+      if (cj == DFX_OP_END) { done = true; break; }
+      if (cj == DFX_OP_BR_BEGIN || cj == DFX_OP_LOOP_BEGIN) {
+        if (lane == 0) o[pcj].z = -1;          // until its end is seen
+        if (deep || sp == kRegionStack) { deep++; cmask = ~0u; continue; }
+        if (lane == 0) stk[sp] = Frame{cdyn, cpc, cmask, cwmask, cbr};
+        sp++;
+        cpc = pcj; cmask = 0u; cwmask = 0u; cdyn = 0; cbr = cj == DFX_OP_BR_BEGIN;
+      } else {                                   // BR_END / LOOP_END
+        if (deep) { deep--; continue; }
+        if (sp == 0) continue;                   // unbalanced
+        const int b = cpc;
+        const bool loop = cj == DFX_OP_LOOP_END;
+        const int64_t dyn = loop ? 3 + 2 * cdyn : 2 + cdyn;
+        uint32_t mask = cmask;
+        if (dyn > 0x7FFFFFFF || (int)loop == cbr) mask = ~0u;   // too long, or mismatched
+        if (lane == 0) {
+          o[b].z = (int)mask;
+          o[b].w = pcj - b;
+          o[pcj].w = (int)((uint32_t)(dyn > 0x7FFFFFFF ? 0x7FFFFFFF : dyn) | (cbr ? 0x80000000u : 0u));
+          if (loop) o[pcj].z = (int)cwmask;
+        }
+        const int br = cbr;
+        sp--;
+        __syncwarp();
+        const Frame fr = stk[sp];
+        cpc = fr.pc; cmask = fr.mask | mask; cwmask = fr.wmask | cwmask;
+        cdyn = fr.dyn + dyn; cbr = fr.br | br;
+      }
     }
+    if (done) break;
   }
 }
 
 int region_launch(const ReplayDev& r, int fn_lo, int fn_hi, cudaStream_t stream) {
   if (fn_hi > fn_lo)
-    region_kernel<<<(fn_hi - fn_lo + 31) / 32, 32, 0, stream>>>(
+    region_kernel<<<(fn_hi - fn_lo + kRegionWarps - 1) / kRegionWarps, kRegionWarps * 32, 0, stream>>>(
         r.fns, reinterpret_cast<int4*>(const_cast<int32_t*>(r.ops)), fn_lo, fn_hi);
   return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
 }
+
+// Packed ops (dfx_replay_batch_packed, include/dfx.h) -> the 16-byte form, for
+// the op range [lo, hi); region-table words are left 0 for region_kernel.
+__host__ __device__ __forceinline__ int4 unpack_op(uint2 p) {
+  const int code = (int)(p.x & 15u), fl = (int)((p.x >> 4) & 31u), c = (int)(p.x >> 9);
+  const int a = (int)(p.y & 0xFFFFu), b = (int)(p.y >> 16);
+  int4 o = make_int4(code | fl << 8, 0, 0, 0);
+  switch (code) {
+    case DFX_OP_HR: case DFX_OP_DR: o.y = a; o.z = b; o.w = c; break;
+    case DFX_OP_HW: case DFX_OP_DW: case DFX_OP_ERR: o.y = a; o.z = b; break;
+    case DFX_OP_BR_END: o.y = c; o.z = b; break;
+    case DFX_OP_LOOP_BEGIN: o.y = a; break;
+    case DFX_OP_LOOP_END: o.y = c; break;
+    default: break;
+  }
+  return o;
+}
+
+__global__ void unpack_ops_kernel(const uint2* __restrict__ pk, int4* __restrict__ ops, int64_t lo,
+                                  int64_t hi) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
+       i += (int64_t)gridDim.x * blockDim.x)
+    ops[i] = unpack_op(__ldg(pk + i));
+}
+
+int unpack_ops_launch(const uint32_t* packed, int32_t* ops, int64_t lo, int64_t hi, cudaStream_t st) {
+  if (hi <= lo) return DFX_OK;
+  int64_t g = (hi - lo + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  unpack_ops_kernel<<<(int)g, 256, 0, st>>>(reinterpret_cast<const uint2*>(packed),
+                                            reinterpret_cast<int4*>(ops), lo, hi);
+  return cudaGetLastError() == cudaSuccess ? DFX_OK : DFX_E_CUDA;
+}
+
+void unpack_ops_host(const uint32_t* packed, int32_t* ops, int64_t n) {
+  for (int64_t i = 0; i < n; i++) {
+    const int4 o = unpack_op(make_uint2(packed[2 * i], packed[2 * i + 1]));
+    ops[4 * i] = o.x; ops[4 * i + 1] = o.y; ops[4 * i + 2] = o.z; ops[4 * i + 3] = o.w;
+  }
+}
+
 
 namespace {
 // one persistent launch over an item list: narrow (slot bitmasks in 32-bit

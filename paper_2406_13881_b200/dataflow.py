@@ -120,6 +120,63 @@ def concat_batches(batches: list[PackedBatch]) -> PackedBatch:
                        stmt_span=cat("stmt_span"), sites=cat("sites"), arms=cat("arms"))
 
 
+def pack_ops(ops: np.ndarray) -> np.ndarray | None:
+    """16-byte replay ops [n, 4] -> the 8-byte form of `dfx_replay_batch_packed`
+    ([n, 2] uint32, include/dfx.h), or None when a field does not fit (then
+    the batch goes through `dfx_replay_batch`)."""
+    o = ops.astype(np.int64)
+    x, y, z, w = o[:, 0], o[:, 1], o[:, 2], o[:, 3]
+    code, fl = x & 0xFF, x >> 8
+    a = np.zeros_like(y)
+    b = np.zeros_like(y)
+    c = np.zeros_like(y)
+    kept = np.zeros((o.shape[0], 3), dtype=bool)         # which of y, z, w the form keeps
+    acc = (code == _abi.OP_HR) | (code == _abi.OP_DR)
+    ab = acc | (code == _abi.OP_HW) | (code == _abi.OP_DW) | (code == _abi.OP_ERR)
+    a[ab], b[ab] = y[ab], z[ab]
+    kept[ab, 0] = kept[ab, 1] = True
+    c[acc] = w[acc]
+    kept[acc, 2] = True
+    m = code == _abi.OP_BR_END
+    c[m], b[m] = y[m], z[m]
+    kept[m, 0] = kept[m, 1] = True
+    m = code == _abi.OP_LOOP_BEGIN
+    a[m] = y[m]
+    kept[m, 0] = True
+    m = code == _abi.OP_LOOP_END
+    c[m] = y[m]
+    kept[m, 0] = True
+    dropped = np.where(kept, 0, o[:, 1:])
+    if ((code > 15).any() or (fl < 0).any() or (fl > 31).any() or (dropped != 0).any()
+            or (a < 0).any() or (a > 0xFFFF).any() or (b < 0).any() or (b > 0xFFFF).any()
+            or (c < 0).any() or (c >= 1 << 23).any()):
+        return None
+    out = np.empty((o.shape[0], 2), dtype=np.uint32)
+    out[:, 0] = (code | (fl << 4) | (c << 9)).astype(np.uint32)
+    out[:, 1] = (a | (b << 16)).astype(np.uint32)
+    return out
+
+
+def unpack_ops(packed: np.ndarray) -> np.ndarray:
+    """`pack_ops` inverse (the device's unpack, restated for tests)."""
+    p = packed.astype(np.int64)
+    code, fl, c = p[:, 0] & 15, (p[:, 0] >> 4) & 31, p[:, 0] >> 9
+    a, b = p[:, 1] & 0xFFFF, p[:, 1] >> 16
+    o = np.zeros((p.shape[0], 4), dtype=np.int64)
+    o[:, 0] = code | (fl << 8)
+    acc = (code == _abi.OP_HR) | (code == _abi.OP_DR)
+    ab = acc | (code == _abi.OP_HW) | (code == _abi.OP_DW) | (code == _abi.OP_ERR)
+    o[ab, 1], o[ab, 2] = a[ab], b[ab]
+    o[acc, 3] = c[acc]
+    m = code == _abi.OP_BR_END
+    o[m, 1], o[m, 2] = c[m], b[m]
+    m = code == _abi.OP_LOOP_BEGIN
+    o[m, 1] = a[m]
+    m = code == _abi.OP_LOOP_END
+    o[m, 1] = c[m]
+    return o.astype(np.int32)
+
+
 @dataclass
 class RawResult:
     events: np.ndarray     # EVENT_DTYPE, all functions
@@ -169,7 +226,9 @@ class ReplaySession:
         self._ev = None
         self._vout = None
 
-    def run(self, batch: PackedBatch) -> RawResult:
+    def run(self, batch: PackedBatch, packed_ops: np.ndarray | None = None) -> RawResult:
+        """`packed_ops`: the batch's ops in the 8-byte form (`pack_ops`), sent
+        through `dfx_replay_batch_packed` (half the ops' host->device bytes)."""
         if self.cap <= 0:
             self.cap = max(1024, 4 * int(batch.ops.shape[0]) // 10)
         while True:
@@ -178,11 +237,16 @@ class ReplaySession:
             if self._vout is None or self._vout.shape[0] < max(1, batch.n_vars):
                 self._vout = self.alloc((max(1, batch.n_vars),), np.uint8)
             rin = batch.replay_in()
+            call = self.eng.lib.dfx_replay_batch
+            if packed_ops is not None:
+                assert packed_ops.dtype == np.uint32 and packed_ops.shape == (batch.ops.shape[0], 2)
+                rin.ops = _abi.ptr(packed_ops)
+                call = self.eng.lib.dfx_replay_batch_packed
             rout = _abi.ReplayOut()
             rout.events = _abi.ptr(self._ev)
             rout.event_cap = self._ev.shape[0]
             rout.var_out = _abi.ptr(self._vout)
-            rc = self.eng.lib.dfx_replay_batch(self.eng.h, C.byref(rin), C.byref(rout))
+            rc = call(self.eng.h, C.byref(rin), C.byref(rout))
             if rc == _abi.DFX_E_NOSPC:
                 self.cap = int(rout.n_events) + 16
                 continue

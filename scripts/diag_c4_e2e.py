@@ -30,3 +30,17 @@ for i in range(4):
     torch.cuda.synchronize()
     print("host-buffer call %.1f ms wall, device span %.1f ms, events %d" %
           ((time.perf_counter() - t) * 1e3, raw.kernel_ms, raw.events.shape[0]))
+from paper_2406_13881_b200.dataflow import pack_ops  # noqa: E402
+pk_np = pack_ops(batch.ops)
+pk = pinned(pk_np.shape, np.uint32)
+pk[:] = pk_np
+for i in range(3):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    raw = sess.run(batch, pk)
+    torch.cuda.synchronize()
+    print("packed host-buffer call %.1f ms wall, device span %.1f ms" %
+          ((time.perf_counter() - t) * 1e3, raw.kernel_ms))
+import os  # noqa: E402
+if os.environ.get("DFX_TRACE"):
+    print("(trace above)")

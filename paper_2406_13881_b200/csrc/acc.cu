@@ -202,7 +202,7 @@ expand_b8_kernel(int64_t n_lo, int64_t n_nodes, int words, const int32_t* __rest
       if (end) {
         const int v = sum - 1;
         const uint32_t k = b >> 6;
-        if (v >= nvars || k == 0u) {
+        if ((unsigned)v >= (unsigned)nvars || k == 0u) {   // (a huge run of continuations wraps)
           atomicExch(bad, 1);
         } else {
           const uint32_t bit = 1u << (v & 31);

@@ -35,6 +35,25 @@ def test_requirement_lists_split_on_firstprivate_flag():
     assert req[2, 3] == 1 << 31 and fp[2, 0] == 1
 
 
+def test_event_order_is_function_then_key():
+    """`dataflow._event_order`: the combined 64-bit sort and the lexsort
+    fallback (a key too wide to share 64 bits with the function index)."""
+    import numpy as np
+    from paper_2406_13881_b200 import _abi
+    from paper_2406_13881_b200.dataflow import _event_order
+    rng = np.random.default_rng(9)
+    for wide in (False, True):
+        n = 5000
+        ev = np.zeros(n, dtype=_abi.EVENT_DTYPE)
+        ev["fn"] = rng.integers(0, 3000, n)
+        ev["key"] = rng.permutation(n).astype(np.uint64) << np.uint64(24)
+        if wide:
+            ev["key"][0] |= np.uint64(1) << np.uint64(62)
+        o = _event_order(ev)
+        exp = np.lexsort((ev["key"], ev["fn"]))
+        assert np.array_equal(ev["fn"][o], ev["fn"][exp]) and np.array_equal(ev["key"][o], ev["key"][exp])
+
+
 def test_first_occurrences_matches_a_python_scan():
     """`dataflow._first_occurrences` (the event dedup before decode), both the
     packed-key path and the lexsort path (forced by an out-of-range node)."""
@@ -57,4 +76,5 @@ def test_first_occurrences_matches_a_python_scan():
             k = (int(e["fn"]), int(e["var"]), int(e["node"]), int(e["kind"]), int(e["pos"]))
             exp[i] = k not in seen or int(e["kind"]) >= _abi.EV_ERR_DATAMAP
             seen.add(k)
-        assert np.array_equal(_first_occurrences(ev), exp)
+        assert np.array_equal(_first_occurrences(ev["fn"], ev["var"], ev["node"], ev["kind"],
+                                                 ev["pos"]), exp)

@@ -240,9 +240,8 @@ class _Lowerer:
         self._dev_by_node: dict | None = None
         self._fiv_cache: dict = {}
         self._norm_cache: dict = {}
-        self._loops_cache: dict = {}
+        self._levels_cache: dict = {}
         self._decl_anc: dict = {}
-        self._idx_cache: dict = {}
         # structural bounds for engine resources
         self.loop_depth = 0
         self.max_loop_depth = 0
@@ -343,25 +342,34 @@ class _Lowerer:
         if subscript is None:
             self.sites.extend([0, acc_code])
         else:
-            # per statement / per subscript, not per (statement, subscript, variable)
-            k = id(access_stmt)
-            loops = self._loops_cache.get(k)
-            if loops is None:
-                loops = self._loops_cache[k] = enclosing_for_loops(access_stmt, stop_at=self.fn)
-            k = id(subscript)
-            idx_vars = self._idx_cache.get(k)
-            if idx_vars is None:
-                idx_vars = self._idx_cache[k] = subscript_index_vars(subscript)
+            # per (statement, subscript), not per variable: each enclosing
+            # for-level's start and anchor code with its qualification bit
+            k2 = (id(access_stmt), id(subscript))
+            levels = self._levels_cache.get(k2)
+            if levels is None:
+                loops = enclosing_for_loops(access_stmt, stop_at=self.fn)
+                idx_vars = subscript_index_vars(subscript)
+                levels = []
+                for f in loops:
+                    code = self.norm_code(f)
+                    v = self.find_indexing_var(f)
+                    if v is not None and v in idx_vars:
+                        code |= AC_QUAL
+                    levels.append((f.span.start, code))
+                self._levels_cache[k2] = levels
             read_pos = access_stmt.span.start
-            self.sites.extend([len(loops), acc_code])
-            for f in loops:
-                code = self.norm_code(f)
-                v = self.find_indexing_var(f)
-                if v is not None and v in idx_vars:
-                    code |= AC_QUAL
-                if not self.writes_between(var, f.span.start, read_pos):
+            sites = self.sites
+            sites.extend([len(levels), acc_code])
+            pos = self._write_pos.get(id(var))
+            for start, code in levels:
+                # `writes_between(var, loop start, read)` (bounds.py:160-165)
+                if pos:
+                    i = bisect.bisect_left(pos, start)
+                    if not (i < len(pos) and pos[i] < read_pos):
+                        code |= AC_CLEAN
+                else:
                     code |= AC_CLEAN
-                self.sites.extend([f.span.start, code])
+                sites.extend([start, code])
         self._site_cache[key] = off
         return off
 

@@ -236,16 +236,23 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
     src_off = np.zeros(nf + 1, dtype=np.int32)
     src_rows, slist, bind = [], [], []
     wave = [0] * nf
+    # the bits go through dicts keyed by (function, slot) and land in the
+    # arrays at the end: numpy item assignment per access is the slow part
+    dbits: dict = {}
+    ibits: dict = {}
     for f, srcs in enumerate(per_fn):
+        row = f * n_slots
         for k, sr in enumerate(srcs):
             if sr[0] == "static":
-                order = []
+                order, seen = [], set()
                 for t, b in sr[1]:
                     sl = slot(t)
-                    direct[f, sl] |= b
+                    key = row + sl
+                    dbits[key] = dbits.get(key, 0) | b
                     if k == 0:
-                        init_bits[f, sl] |= b
-                    if sl not in order:
+                        ibits[key] = ibits.get(key, 0) | b
+                    if sl not in seen:
+                        seen.add(sl)
                         order.append(sl)
                 if k == 0:
                     init_len[f] = len(order)
@@ -259,6 +266,10 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
                 if g < f:
                     wave[f] = max(wave[f], wave[g] + 1)
         src_off[f + 1] = len(src_rows)
+    for arr, bits in ((direct, dbits), (init_bits, ibits)):
+        if bits:
+            arr.reshape(-1)[np.fromiter(bits.keys(), np.int64, len(bits))] = \
+                np.fromiter(bits.values(), np.uint8, len(bits))
     n_waves = max(wave) + 1 if nf else 0
     buckets: list[list[int]] = [[] for _ in range(n_waves)]
     for f in range(nf):

@@ -38,6 +38,7 @@ it is reported, not approximated.
 """
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -305,16 +306,41 @@ def lower_analysis(analysis, names=None) -> CfgProgram:
                            analysis.table) for n in names])
 
 
-@dataclass
 class FnRequirements:
     """Kernel (b)'s answer for one function, per CFG node id: the variables
-    needing a device -> host transfer before a host read (`update from`),
-    a host -> device transfer before a device read (`update to` / map to),
-    and a kernel's firstprivate captures."""
-    name: str
-    update_from: dict        # cfg node id -> [VariableId]
-    update_to: dict
-    firstprivate: dict
+    needing a device -> host transfer before a host read (`update_from`),
+    a host -> device transfer before a device read (`update_to` / map to),
+    and a kernel's firstprivate captures.  Held as entry arrays (CFG node,
+    variable slot, what); the per-node dicts are built when first read."""
+
+    UPDATE_FROM, UPDATE_TO, FIRSTPRIVATE = 0, 1, 2
+
+    def __init__(self, name, vars_, cfg_node, slot, what):
+        self.name = name
+        self.vars = vars_
+        self.cfg_node = cfg_node        # int32 [entries]
+        self.slot = slot                # int32 [entries]
+        self.what = what                # uint8 [entries]
+
+    def _by_node(self, w) -> dict:
+        m = self.what == w
+        out: dict = {}
+        vs = self.vars
+        for c, sl in zip(self.cfg_node[m].tolist(), self.slot[m].tolist()):
+            out.setdefault(c, []).append(vs[sl])
+        return out
+
+    @functools.cached_property
+    def update_from(self) -> dict:
+        return self._by_node(self.UPDATE_FROM)
+
+    @functools.cached_property
+    def update_to(self) -> dict:
+        return self._by_node(self.UPDATE_TO)
+
+    @functools.cached_property
+    def firstprivate(self) -> dict:
+        return self._by_node(self.FIRSTPRIVATE)
 
 
 def solve_program(prog: CfgProgram, session: AccSession | None = None):
@@ -323,25 +349,19 @@ def solve_program(prog: CfgProgram, session: AccSession | None = None):
     sess = session or AccSession()
     rl = sess.run(prog.row_ptr, prog.col, prog.kind, prog.acc_off, prog.acc, prog.S,
                   prog.words)
-    off = rl.row_off.tolist()
-    ents = rl.vars.tolist()
-    kinds = prog.kind.tolist()
-    ncfg = prog.node_cfg.tolist()
+    counts = np.diff(rl.row_off)
+    node = np.repeat(np.arange(prog.n_nodes, dtype=np.int32), counts)   # graph node per entry
+    e = rl.vars
+    what = np.where(e & REQ_FP_FLAG, FnRequirements.FIRSTPRIVATE,
+                    prog.kind[node].astype(np.int64)).astype(np.uint8)   # host node: from, kernel: to
+    slot = (e & 0x3FFF).astype(np.int32)
+    cfg_node = prog.node_cfg[node]
     out = []
     for fg in prog.fns:
         if fg.status != "ok":
             continue
-        uf, ut, fp = {}, {}, {}
-        for g in range(fg.node0, fg.node0 + fg.n_nodes):
-            a, b = off[g], off[g + 1]
-            if a == b:
-                continue
-            c = ncfg[g]
-            for e in ents[a:b]:
-                v = fg.vars[e & 0x3FFF]
-                d = fp if e & REQ_FP_FLAG else (ut if kinds[g] else uf)
-                d.setdefault(c, []).append(v)
-        out.append(FnRequirements(fg.name, uf, ut, fp))
+        a, b = np.searchsorted(node, (fg.node0, fg.node0 + fg.n_nodes))
+        out.append(FnRequirements(fg.name, fg.vars, cfg_node[a:b], slot[a:b], what[a:b]))
     return out, sess.stats
 
 

@@ -28,3 +28,19 @@ for chunk in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "0,8,56,128
     st = p.solve(chunk)
     print("chunk", chunk, {k: v for k, v in st.as_dict().items() if k in ("rounds_h", "rounds_d", "evaluated", "kernel_ms", "solve_ms")},
           "wall %.2f ms" % ((time.perf_counter() - t) * 1e3))
+# the one-call path: dfx_mfp_acc alone vs solve_program (the Python mapping included)
+import statistics  # noqa: E402
+from paper_2406_13881_b200.cfgprog import solve_program  # noqa: E402
+from paper_2406_13881_b200.csr import AccSession  # noqa: E402
+sess = AccSession()
+for label, fn in (("dfx_mfp_acc", lambda: sess.run(prog.row_ptr, prog.col, prog.kind, prog.acc_off,
+                                                  prog.acc, prog.S, prog.words)),
+                  ("solve_program", lambda: solve_program(prog, sess))):
+    fn()
+    ts = []
+    for _ in range(5):
+        t = time.perf_counter()
+        fn()
+        ts.append((time.perf_counter() - t) * 1e3)
+    print(label, "%.2f ms" % statistics.median(ts), "solve_ms %.2f kernel_ms %.2f req_ms %.2f" % (
+        sess.stats.solve_ms, sess.stats.kernel_ms, sess.stats.req_ms))

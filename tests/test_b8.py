@@ -121,3 +121,20 @@ def test_cuda_b8_refuses_malformed_stream():
     b = np.array([0], dtype=np.uint8)                   # kind 0
     with pytest.raises(_abi.EngineError):
         Acc8Session().run(row_ptr, col, kind, boff, b, S, 4)
+
+
+@pytest.mark.gpu
+def test_cuda_b8_empty_lists_and_single_node():
+    """Nodes without accesses, a graph of one node, and a list whose every
+    node is empty: the byte-coded call agrees with the uint16 call."""
+    from paper_2406_13881_b200.csr import Acc8Session, AccSession
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 4096):
+        row_ptr, col, kind, S = _random_graph(rng, n, 4)
+        for dens in (0.0, 0.02):
+            R, W = _planes(rng, n, 4, dens, dens)
+            off, acc = planes_to_acc(R, W)
+            ref = AccSession().run(row_ptr, col, kind, off, acc, S, 4)
+            boff, b = acc_to_b8(off, acc)
+            got = Acc8Session().run(row_ptr, col, kind, boff, b, S, 4).to_lists()
+            assert np.array_equal(got.row_off, ref.row_off) and np.array_equal(got.vars, ref.vars)

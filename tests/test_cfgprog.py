@@ -283,3 +283,14 @@ def test_cuda_cfg_fixpoint_equals_reference_on_monotone_programs():
                 assert (h[s], d[s]) == (rh, rd), (seed, v.name)
         n_fn += 1
     assert n_fn >= 25
+
+
+def test_empty_and_trivial_units():
+    """A unit whose functions have no accesses, and an empty item list."""
+    from dartomp.pipeline import load
+    from paper_2406_13881_b200.cfgprog import lower_analysis, lower_program
+    prog = lower_program([])
+    assert prog.n_nodes == 0 and prog.fns == []
+    prog = lower_analysis(load(text="void f(void) { }\nint g(int x) { return 1; }\n"))
+    assert all(f.status == "ok" for f in prog.fns)
+    assert prog.acc.shape[0] == 0 and prog.n_nodes > 0

@@ -63,3 +63,17 @@ def test_cuda_packed_equals_16_byte_form():
     ev = np.sort(got.events.copy(), order=["fn", "key", "var", "node", "kind", "pos"])
     assert ev.shape == ev_ref.shape and (ev == ev_ref).all()
     assert np.array_equal(got.var_out, vo_ref)
+
+
+@pytest.mark.gpu
+def test_cuda_packed_small_batch_single_range():
+    """A batch below the range pipeline's threshold (one range) and a single
+    function: packed == 16-byte form."""
+    from paper_2406_13881_b200.dataflow import ReplaySession
+    for n in (1, 30):
+        b = _c4_batch(n, 997)
+        ref = ReplaySession().run(b)
+        got = ReplaySession().run(b, packed_ops=pack_ops(b.ops))
+        key = ["fn", "key", "var", "node", "kind", "pos"]
+        assert (np.sort(got.events.copy(), order=key) == np.sort(ref.events.copy(), order=key)).all()
+        assert np.array_equal(got.var_out, ref.var_out)

@@ -241,6 +241,8 @@ class _Lowerer:
         self._fiv_cache: dict = {}
         self._norm_cache: dict = {}
         self._levels_cache: dict = {}
+        self._loops_cache: dict = {}
+        self._idx_cache: dict = {}
         self._decl_anc: dict = {}
         # structural bounds for engine resources
         self.loop_depth = 0
@@ -347,16 +349,19 @@ class _Lowerer:
             k2 = (id(access_stmt), id(subscript))
             levels = self._levels_cache.get(k2)
             if levels is None:
-                loops = enclosing_for_loops(access_stmt, stop_at=self.fn)
-                idx_vars = subscript_index_vars(subscript)
-                levels = []
-                for f in loops:
-                    code = self.norm_code(f)
-                    v = self.find_indexing_var(f)
-                    if v is not None and v in idx_vars:
-                        code |= AC_QUAL
-                    levels.append((f.span.start, code))
-                self._levels_cache[k2] = levels
+                k = id(access_stmt)         # per statement: loop start, code, indexing var
+                loops = self._loops_cache.get(k)
+                if loops is None:
+                    loops = self._loops_cache[k] = [
+                        (f.span.start, self.norm_code(f), self.find_indexing_var(f))
+                        for f in enclosing_for_loops(access_stmt, stop_at=self.fn)]
+                k = id(subscript)
+                idx_vars = self._idx_cache.get(k)
+                if idx_vars is None:
+                    idx_vars = self._idx_cache[k] = subscript_index_vars(subscript)
+                levels = self._levels_cache[k2] = [
+                    (start, code | AC_QUAL if v is not None and v in idx_vars else code)
+                    for start, code, v in loops]
             read_pos = access_stmt.span.start
             sites = self.sites
             sites.extend([len(levels), acc_code])

@@ -491,6 +491,119 @@ def _lower_portable(i: int):
     return ("ok", (fields, stmts, kstmts, region, vars_, premapped))
 
 
+def _fork_tree_map(n: int, workers: int, timeout: float):
+    """`_lower_portable` over range(n) in `workers` forked processes, or None
+    (a worker failed or the deadline passed: the caller lowers serially).
+
+    Forking a process whose heap holds a large parse costs milliseconds per
+    fork (page tables), so the workers start as a two-level tree: the parent
+    forks ~sqrt(workers) group leaders, each leader forks the rest of its
+    group in parallel with the others.  Worker w lowers functions w,
+    w + workers, ... and sends its results through its own pipe, pickled
+    once.  A group is one process group, so a stalled one is killed whole."""
+    import math
+    import os
+    import pickle
+    import select
+    import signal
+    import time
+    fan = max(1, math.isqrt(workers))
+    groups = [list(range(g, workers, fan)) for g in range(fan)]
+    pipes = [os.pipe() for _ in range(workers)]
+
+    def in_child(body, keep_write):
+        """Run `body` in this (forked) process and exit; only the write ends
+        in `keep_write` stay open."""
+        code = 1
+        try:
+            for x, (r, wfd) in enumerate(pipes):
+                os.close(r)
+                if x not in keep_write:
+                    os.close(wfd)
+            body()
+            code = 0
+        finally:
+            os._exit(code)
+
+    def run_worker(w):
+        out = pickle.dumps([_lower_portable(i) for i in range(w, n, workers)], protocol=5)
+        view = memoryview(out)
+        while view:
+            view = view[os.write(pipes[w][1], view):]
+        os.close(pipes[w][1])
+
+    def lead(grp):
+        os.setpgid(0, 0)
+        subs = []
+        for w in grp[1:]:
+            pid = os.fork()
+            if pid == 0:                # the leader holds only its group's write ends
+                code = 1
+                try:
+                    for x in grp:
+                        if x != w:
+                            os.close(pipes[x][1])
+                    run_worker(w)
+                    code = 0
+                finally:
+                    os._exit(code)
+            subs.append(pid)
+        for w in grp[1:]:
+            os.close(pipes[w][1])
+        run_worker(grp[0])
+        if not all(os.waitpid(pid, 0)[1] == 0 for pid in subs):
+            raise RuntimeError("a lowering worker failed")
+
+    import warnings
+    leaders = []
+    with warnings.catch_warnings():     # the children run pure Python, no CUDA, no locks
+        warnings.filterwarnings("ignore", message=".*multi-threaded.*fork.*",
+                                category=DeprecationWarning)
+        for grp in groups:
+            pid = os.fork()
+            if pid == 0:
+                in_child(lambda grp=grp: lead(grp), set(grp))  # never returns
+            leaders.append(pid)
+    for _, wfd in pipes:
+        os.close(wfd)
+    bufs = {r: [] for r, _ in pipes}
+    open_fds = set(bufs)
+    deadline = time.monotonic() + timeout
+    failed = False
+    while open_fds:
+        left = deadline - time.monotonic()
+        if left <= 0:
+            failed = True
+            break
+        ready, _, _ = select.select(list(open_fds), [], [], left)
+        for fd in ready:
+            chunk = os.read(fd, 1 << 22)
+            if chunk:
+                bufs[fd].append(chunk)
+            else:
+                open_fds.discard(fd)
+    if failed:
+        for pid in leaders:
+            try:
+                os.killpg(pid, signal.SIGKILL)
+            except OSError:
+                pass
+    for pid in leaders:
+        failed |= os.waitpid(pid, 0)[1] != 0
+    for r, _ in pipes:
+        os.close(r)
+    if failed:
+        return None
+    res: list = [None] * n
+    for w, (r, _) in enumerate(pipes):
+        items = pickle.loads(b"".join(bufs[r])) if bufs[r] else []
+        if len(items) != len(range(w, n, workers)):
+            return None
+        for k, item in enumerate(items):
+            res[w + k * workers] = item
+    return res
+
+
 def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | None = None):
     """`lower_function` over a batch; forked workers for large batches
     (`workers` or $DFX_LOWER_WORKERS, default min(16, cores); serial below
@@ -503,22 +616,12 @@ def lower_functions(items, allow_stale: frozenset = frozenset(), workers: int | 
         return [lower_function(src, cfg, accs, table, allow_stale)
                 for src, cfg, accs, table in items]
     global _FORK_ITEMS, _FORK_ALLOW
-    import warnings
     _FORK_ITEMS, _FORK_ALLOW = list(items), allow_stale
-    res = None
     try:
         # the workers run pure Python on the copied parse (no CUDA, no locks
         # of the parent's other threads); a bounded wait falls back to the
         # serial lowering if a worker ever stalls
-        with warnings.catch_warnings():
-            warnings.filterwarnings("ignore", message=".*multi-threaded.*fork.*",
-                                    category=DeprecationWarning)
-            with mp.get_context("fork").Pool(workers) as pool:
-                res = pool.map_async(_lower_portable, range(len(items)),
-                                     chunksize=max(1, len(items) // (8 * workers))
-                                     ).get(timeout=60 + 0.05 * len(items))
-    except mp.TimeoutError:
-        res = None
+        res = _fork_tree_map(len(items), workers, 60 + 0.05 * len(items))
     finally:
         _FORK_ITEMS, _FORK_ALLOW = [], frozenset()
     if res is None:

@@ -39,6 +39,15 @@ struct CgBuf {
 
 // Rebuild function f's summary (bits + insertion order) into `cur`; returns
 // (warp-uniform) whether its bit set differs from `prev`.
+// Per-warp shared memory of cg_function: the seen bitmap (nsp / 32 words)
+// and, for functions with many sources, the summary row being built (nsp / 4).
+// (both parts kept at multiples of 4 words: the row is read as 16-byte quads)
+__host__ __device__ __forceinline__ int cg_seen_words(int nsp) { return (((nsp + 31) >> 5) + 3) & ~3; }
+__host__ __device__ __forceinline__ int cg_warp_words(int nsp) {
+  return cg_seen_words(nsp) + ((((nsp + 3) >> 2) + 3) & ~3);
+}
+constexpr int kCgManySources = 24;
+
 __device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, const CgBuf& cur,
                                             int f, uint32_t* seen, int lane) {
   const int sw = g.nsp >> 5;                       // seen words per warp
@@ -48,6 +57,56 @@ __device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, c
     const int s0 = __ldg(g.src_off + f), s1 = __ldg(g.src_off + f + 1);
     // ---- bits: direct | OR of transformed callee rows ----------------------
     bool ch = false;
+    if (s1 - s0 > kCgManySources) {
+      // many sources (a driver calling hundreds of functions): lanes over
+      // sources, 32 callee rows per step OR-reduced quad by quad into the
+      // row in shared memory, each lane's bound parameters ORed in with
+      // shared atomics -- instead of every lane walking all sources serially
+      uint32_t* row = seen + cg_seen_words(g.nsp);
+      for (int w = lane; w < (g.nsp >> 2); w += 32)
+        row[w] = __ldg(reinterpret_cast<const uint32_t*>(g.direct + (size_t)f * g.nsp) + w);
+      __syncwarp();
+      for (int k0 = s0; k0 < s1; k0 += 32) {
+        const int k = k0 + lane;
+        const int4 r = k < s1 ? __ldg(reinterpret_cast<const int4*>(g.src) + k) : make_int4(0, 0, 0, 0);
+        const bool call = (r.x & 0xFF) != 0;
+        const bool dev = (r.x >> 8) & 1;
+        const uint8_t* cb = call ? (r.y < f ? cur.bits : prev.bits) + (size_t)r.y * g.nsp : nullptr;
+        for (int q = 0; q < nq; q++) {
+          uint4 v = call ? __ldcg(reinterpret_cast<const uint4*>(cb) + q) : make_uint4(0u, 0u, 0u, 0u);
+          if (q * 16 < P) {
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&v);
+#pragma unroll
+            for (int t = 0; t < 16; t++)
+              if (q * 16 + t < P) vb[t] = 0;            // callee params bind below
+          }
+          if (dev) { v.x = force_dev4(v.x); v.y = force_dev4(v.y); v.z = force_dev4(v.z); v.w = force_dev4(v.w); }
+          v.x = __reduce_or_sync(FULLM, v.x);
+          v.y = __reduce_or_sync(FULLM, v.y);
+          v.z = __reduce_or_sync(FULLM, v.z);
+          v.w = __reduce_or_sync(FULLM, v.w);
+          if (lane == 0) {
+            row[4 * q] |= v.x; row[4 * q + 1] |= v.y; row[4 * q + 2] |= v.z; row[4 * q + 3] |= v.w;
+          }
+        }
+        __syncwarp();
+        if (call)
+          for (int j = r.z; j < r.z + r.w; j++) {
+            const int i = __ldg(g.bind + 2 * j), sl = __ldg(g.bind + 2 * j + 1);
+            uint32_t e = __ldcg(cb + i);
+            if (!(e & 3u)) continue;
+            if (dev) e = (e & 3u) | 8u;
+            atomicOr(&row[sl >> 2], e << (8 * (sl & 3)));
+          }
+        __syncwarp();
+      }
+      for (int q = lane; q < nq; q += 32) {
+        const uint4 acc = *reinterpret_cast<const uint4*>(row + 4 * q);
+        const uint4 old = __ldcg(reinterpret_cast<const uint4*>(prev.bits + (size_t)f * g.nsp) + q);
+        ch |= (old.x != acc.x) | (old.y != acc.y) | (old.z != acc.z) | (old.w != acc.w);
+        __stcg(reinterpret_cast<uint4*>(cur.bits + (size_t)f * g.nsp) + q, acc);
+      }
+    } else
     for (int q = lane; q < nq; q += 32) {
       uint4 acc = __ldg(reinterpret_cast<const uint4*>(g.direct + (size_t)f * g.nsp) + q);
       uint8_t* ab = reinterpret_cast<uint8_t*>(&acc);
@@ -137,7 +196,7 @@ cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int ns
                int* __restrict__ changed) {
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool any = false;
   for (int pos = lo + shard + nshards * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); pos < hi;
@@ -157,7 +216,7 @@ cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, i
   cgr::grid_group grid = cgr::this_grid();
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int pass = first_pass; pass <= max_passes; pass++) {
@@ -185,7 +244,7 @@ int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8
   if (n <= 0) return DFX_OK;
   int blocks = (n + kCgWarps - 1) / kCgWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  const size_t smem = (size_t)kCgWarps * (g.nsp / 32) * sizeof(uint32_t);
+  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
   CgBuf prev{pbits, plist, plen}, cur{cbits, clist, clen};
   cg_wave_kernel<<<blocks, kCgWarps * 32, smem, st>>>(g, prev, cur, lo, hi, shard, nshards,
                                                       d_changed);
@@ -257,7 +316,7 @@ int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
              int* d_passes, cudaStream_t st, int first_pass) {
-  const size_t smem = (size_t)kCgWarps * (g.nsp / 32) * sizeof(uint32_t);
+  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
   // occupancy per (device, smem size)
   constexpr int kDevs = 64;
   static int sms_d[kDevs] = {}, per_sm_d[kDevs] = {};
@@ -326,7 +385,7 @@ cg_wave_peer_kernel(CgDev g, PeerTables tab, int cur, int lo, int hi, int rank, 
                     int pass, int gen, unsigned int* blocks_done) {
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * (g.nsp >> 5);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int prev = cur ^ 1;
   const size_t nsp = (size_t)g.nsp;
@@ -387,7 +446,7 @@ int cg_peer_wave(const CgDev& g, const PeerTables& tab, int cur, int wave, int r
   int blocks = (n + kPeerWarps - 1) / kPeerWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;            // an empty share still signals its arrival
-  const size_t smem = (size_t)kPeerWarps * (g.nsp / 32) * sizeof(uint32_t);
+  const size_t smem = (size_t)kPeerWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
   if (cudaMemsetAsync(blocks_done, 0, sizeof(unsigned int), st) != cudaSuccess) return DFX_E_CUDA;
   cg_wave_peer_kernel<<<blocks, kPeerWarps * 32, smem, st>>>(g, tab, cur, lo, hi, rank, nranks,
                                                              pass, gen, blocks_done);

@@ -1504,6 +1504,7 @@ int dfx_cg_create(dfx_handle* h, const dfx_cg_in* in, dfx_cg** out) {
   auto* c = new dfx_cg();
   dfx::CgDev& g = c->g;
   g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = in->n_waves;
+  g.many = in->src_off && dfx::cg_many_sources(in->src_off, nf);
   auto up = [&](const void* src, size_t bytes) -> void* {
     void* p = cg_alloc(c, bytes);
     if (p && bytes && src) cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, st);
@@ -1843,6 +1844,7 @@ int cg_setup(dfx_handle* h, const dfx_cg_in* in, const int32_t* wave_off, const 
   CK(cudaMemsetAsync(R.d_flags, 0, sizeof(int) * (size_t)(maxp + 2), st));
   dfx::CgDev& g = R.g;
   g.n_funcs = nf; g.n_slots = ns; g.nsp = nsp; g.n_params = in->n_params; g.n_waves = n_waves;
+  g.many = in->src_off && dfx::cg_many_sources(in->src_off, nf);
   g.direct = d_direct; g.src_off = d_srcoff; g.src = d_src; g.slist = d_slist; g.bind = d_bind;
   g.wave_fns = d_wfns;
   g.h_wave_off = wave_off;

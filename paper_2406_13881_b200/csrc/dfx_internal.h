@@ -140,6 +140,7 @@ namespace dfx {
 
 struct CgDev {
   int32_t n_funcs, n_slots, nsp, n_params, n_waves;
+  int32_t many;              // some function has more than kCgManySources sources (summ.cu)
   const uint8_t* direct;     // [n_funcs * nsp]
   const int32_t* src_off;
   const int32_t* src;        // int32 x4 rows
@@ -149,6 +150,8 @@ struct CgDev {
   const int32_t* h_wave_off; // host copy
 };
 
+// whether a call graph needs kernel (c)'s many-sources path (and its shared memory)
+bool cg_many_sources(const int32_t* src_off_host, int n_funcs);
 int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8_t* cbits,
             int16_t* clist, int32_t* clen, int wave, int shard, int nshards, int* d_changed,
             cudaStream_t st);

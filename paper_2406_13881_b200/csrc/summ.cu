@@ -42,11 +42,19 @@ struct CgBuf {
 // Per-warp shared memory of cg_function: the seen bitmap (nsp / 32 words)
 // and, for functions with many sources, the summary row being built (nsp / 4).
 // (both parts kept at multiples of 4 words: the row is read as 16-byte quads)
+// and first-occurrence positions (nsp words) for those functions' order
 __host__ __device__ __forceinline__ int cg_seen_words(int nsp) { return (((nsp + 31) >> 5) + 3) & ~3; }
-__host__ __device__ __forceinline__ int cg_warp_words(int nsp) {
-  return cg_seen_words(nsp) + ((((nsp + 3) >> 2) + 3) & ~3);
-}
+__host__ __device__ __forceinline__ int cg_row_words(int nsp) { return (((nsp + 3) >> 2) + 3) & ~3; }
 constexpr int kCgManySources = 24;
+__host__ __device__ __forceinline__ int cg_warp_words(int nsp, bool many) {
+  return cg_seen_words(nsp) + (many ? cg_row_words(nsp) + ((nsp + 3) & ~3) : 0);
+}
+
+bool cg_many_sources(const int32_t* src_off, int n_funcs) {
+  for (int f = 0; f < n_funcs; f++)
+    if (src_off[f + 1] - src_off[f] > kCgManySources) return true;
+  return false;
+}
 
 __device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, const CgBuf& cur,
                                             int f, uint32_t* seen, int lane) {
@@ -57,7 +65,7 @@ __device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, c
     const int s0 = __ldg(g.src_off + f), s1 = __ldg(g.src_off + f + 1);
     // ---- bits: direct | OR of transformed callee rows ----------------------
     bool ch = false;
-    if (s1 - s0 > kCgManySources) {
+    if (g.many && s1 - s0 > kCgManySources) {
       // many sources (a driver calling hundreds of functions): lanes over
       // sources, 32 callee rows per step OR-reduced quad by quad into the
       // row in shared memory, each lane's bound parameters ORed in with
@@ -138,9 +146,60 @@ __device__ __forceinline__ bool cg_function(const CgDev& g, const CgBuf& prev, c
     }
     const bool any = __any_sync(FULLM, ch);
     // ---- insertion order ------------------------------------------------------
+    int16_t* out = cur.list + (size_t)f * g.nsp;
+    if (g.many && s1 - s0 > kCgManySources && s1 - s0 < (1 << 12)) {
+      // many sources: the order is the distinct candidates sorted by first
+      // occurrence, so each candidate's position in the candidate sequence --
+      // (source, part: bound parameters before globals, index in the list)
+      // -- is min-reduced per slot with shared atomics, lanes over sources;
+      // a slot's place in the list is then the number of slots seen earlier
+      uint32_t* fpos = seen + cg_seen_words(g.nsp) + cg_row_words(g.nsp);
+      for (int w = lane; w < g.nsp; w += 32) fpos[w] = 0xFFFFFFFFu;
+      __syncwarp();
+      for (int k0 = s0; k0 < s1; k0 += 32) {
+        const int k = k0 + lane;
+        if (k >= s1) continue;
+        const int4 r = __ldg(reinterpret_cast<const int4*>(g.src) + k);
+        const uint32_t kb = (uint32_t)(k - s0) << 20;
+        if ((r.x & 0xFF) == 0) {                 // static list
+          for (int j = 0; j < r.z; j++)
+            atomicMin(&fpos[__ldg(g.slist + r.y + j)], kb | (uint32_t)j);
+          continue;
+        }
+        const int callee = r.y;
+        const CgBuf& b = callee < f ? cur : prev;
+        const int glen = __ldcg(b.len + callee);
+        const int16_t* gl = b.list + (size_t)callee * g.nsp;
+        for (int j = 0; j < glen; j++) {
+          const int x = __ldcg(gl + j);
+          if (x >= P) {                          // globals, after the bound parameters
+            atomicMin(&fpos[x], kb | (1u << 19) | (uint32_t)j);
+          } else {
+            for (int t = r.z; t < r.z + r.w; t++)
+              if (__ldg(g.bind + 2 * t) == x) {
+                atomicMin(&fpos[__ldg(g.bind + 2 * t + 1)], kb | (uint32_t)j);
+                break;
+              }
+          }
+        }
+      }
+      __syncwarp();
+      int len = 0;
+      for (int s0l = 0; s0l < g.nsp; s0l += 32) {
+        const int sl = s0l + lane;
+        const uint32_t mine = sl < g.nsp ? fpos[sl] : 0xFFFFFFFFu;
+        if (mine != 0xFFFFFFFFu) {
+          int rank = 0;
+          for (int t = 0; t < g.nsp; t++) rank += fpos[t] < mine;
+          out[rank] = (int16_t)sl;
+        }
+        len += __popc(__ballot_sync(FULLM, mine != 0xFFFFFFFFu));
+      }
+      if (lane == 0) __stcg(cur.len + f, len);
+      return any;
+    }
     for (int w = lane; w < sw; w += 32) seen[w] = 0u;
     __syncwarp();
-    int16_t* out = cur.list + (size_t)f * g.nsp;
     int len = 0;
     auto append = [&](int cand) {       // one candidate slot (or -1) per lane
       bool fresh = cand >= 0 && !((seen[cand >> 5] >> (cand & 31)) & 1u);
@@ -196,7 +255,7 @@ cg_wave_kernel(CgDev g, CgBuf prev, CgBuf cur, int lo, int hi, int shard, int ns
                int* __restrict__ changed) {
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp, g.many);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool any = false;
   for (int pos = lo + shard + nshards * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); pos < hi;
@@ -216,7 +275,7 @@ cg_solve_kernel(CgDev g, CgBuf t0, CgBuf t1, const int* __restrict__ wave_off, i
   cgr::grid_group grid = cgr::this_grid();
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp, g.many);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int pass = first_pass; pass <= max_passes; pass++) {
@@ -244,7 +303,7 @@ int cg_wave(const CgDev& g, uint8_t* pbits, int16_t* plist, int32_t* plen, uint8
   if (n <= 0) return DFX_OK;
   int blocks = (n + kCgWarps - 1) / kCgWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
+  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp, g.many) * sizeof(uint32_t);
   CgBuf prev{pbits, plist, plen}, cur{cbits, clist, clen};
   cg_wave_kernel<<<blocks, kCgWarps * 32, smem, st>>>(g, prev, cur, lo, hi, shard, nshards,
                                                       d_changed);
@@ -316,7 +375,7 @@ int repitch(const void* src, size_t sp, void* dst, size_t dp, size_t width, size
 int cg_solve(const CgDev& g, uint8_t* b0, int16_t* l0, int32_t* n0, uint8_t* b1, int16_t* l1,
              int32_t* n1, const int32_t* d_wave_off, int max_passes, int* d_changed,
              int* d_passes, cudaStream_t st, int first_pass) {
-  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
+  const size_t smem = (size_t)kCgWarps * cg_warp_words(g.nsp, g.many) * sizeof(uint32_t);
   // occupancy per (device, smem size)
   constexpr int kDevs = 64;
   static int sms_d[kDevs] = {}, per_sm_d[kDevs] = {};
@@ -385,7 +444,7 @@ cg_wave_peer_kernel(CgDev g, PeerTables tab, int cur, int lo, int hi, int rank, 
                     int pass, int gen, unsigned int* blocks_done) {
   extern __shared__ uint32_t seen_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp);
+  uint32_t* seen = seen_all + warp * cg_warp_words(g.nsp, g.many);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int prev = cur ^ 1;
   const size_t nsp = (size_t)g.nsp;
@@ -446,7 +505,7 @@ int cg_peer_wave(const CgDev& g, const PeerTables& tab, int cur, int wave, int r
   int blocks = (n + kPeerWarps - 1) / kPeerWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;            // an empty share still signals its arrival
-  const size_t smem = (size_t)kPeerWarps * cg_warp_words(g.nsp) * sizeof(uint32_t);
+  const size_t smem = (size_t)kPeerWarps * cg_warp_words(g.nsp, g.many) * sizeof(uint32_t);
   if (cudaMemsetAsync(blocks_done, 0, sizeof(unsigned int), st) != cudaSuccess) return DFX_E_CUDA;
   cg_wave_peer_kernel<<<blocks, kPeerWarps * 32, smem, st>>>(g, tab, cur, lo, hi, rank, nranks,
                                                              pass, gen, blocks_done);

@@ -55,6 +55,9 @@ _KIND_BITS = {AccessKind.READ: BIT_R, AccessKind.WRITE: BIT_W,
               AccessKind.UNKNOWN: BIT_R | BIT_W}   # `_norm`: unknown -> readwrite
 
 
+_KIND_BITS_ID = {id(k): v for k, v in _KIND_BITS.items()}
+
+
 def _eff_bits(kind, spaces) -> int:
     b = _KIND_BITS[kind]
     for sp in spaces:
@@ -162,15 +165,19 @@ def lower_call_graph(src, tu, cfgs, accesses, table) -> CallGraph:
         fn = defined[name]
         pidx = {p: i for i, p in enumerate(params[name])}
         items = []
+        unknown, host, glob = AccessKind.UNKNOWN, Space.HOST, Storage.GLOBAL
         for acc in accesses[name]:                 # `_direct_effects` (:75-87)
-            if acc.kind is AccessKind.UNKNOWN:
+            kind = acc.kind
+            if kind is unknown:
                 continue
-            b = _eff_bits(acc.kind, (acc.space,))
-            d = acc.var.decl
+            # `_eff_bits(kind, (space,))` (Enum.__hash__ is Python-level: id-keyed)
+            b = _KIND_BITS_ID[id(kind)] | (BIT_H if acc.space is host else BIT_D)
+            var = acc.var
+            d = var.decl
             if d is not None and d in pidx and d.type_info.is_pointerish:
                 items.append((("p", pidx[d]), b))
-            elif acc.var.storage is Storage.GLOBAL:
-                items.append((("g", acc.var.name), b))
+            elif var.storage is glob:
+                items.append((("g", var.name), b))
         srcs = [("static", items)]
         for cs in cfgs[name].call_sites:
             args = cs.call.children

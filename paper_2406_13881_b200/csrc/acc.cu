@@ -254,6 +254,7 @@ __device__ __forceinline__ int b8_node(int64_t n, int words, const uint32_t* __r
           if (slot >= 0) m = __ldg(reinterpret_cast<const uint4*>(FPQ) + (size_t)n * n_fp_slots + slot);
         }
       }
+      if (!__any_sync(FULL, (m.x | m.y | m.z | m.w) != 0u)) continue;   // no entries here (most FP rows)
       const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
       int last = -1;
 #pragma unroll

@@ -574,6 +574,7 @@ __device__ __forceinline__ int b8_bytes(const uint4 (&m)[VPL], int lane) {
 #pragma unroll
   for (int v = 0; v < VPL; v++) {
     const int q = lane + 32 * v;
+    if (!__any_sync(FULL, (m[v].x | m[v].y | m[v].z | m[v].w) != 0u)) continue;   // no entries here
     const uint32_t mw[4] = {m[v].x, m[v].y, m[v].z, m[v].w};
     int last = -1;
 #pragma unroll

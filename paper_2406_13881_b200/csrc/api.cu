@@ -596,7 +596,19 @@ static int replay_batch_impl(dfx_handle* h, const dfx_replay_in* in, dfx_replay_
       return fail(rc, "replay launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
   }
+  // once the last range is open, its region stream backfills the slots the
+  // gated launch left to the region kernels (same item queue)
+  cudaEvent_t ev_bf = nullptr;
+  if (K > 1 && !getenv("DFX_NO_BACKFILL")) {
+    cudaStream_t s_last = s_regs[(K - 1) & 1];
+    if (dfx::replay_launch_backfill(r, s_last, &gate) == DFX_OK &&
+        cudaEventCreateWithFlags(&ev_bf, cudaEventDisableTiming) == cudaSuccess) {
+      CK(cudaEventRecord(ev_bf, s_last));
+      CK(cudaStreamWaitEvent(st, ev_bf, 0));
+    }
+  }
   CK(cudaEventRecord(h->ev1, st));
+  if (ev_bf) cudaEventDestroy(ev_bf);   // released once recorded and waited on
   // a range's region kernel never got an SM slot beside the gated launch
   // (e.g. another process holds the GPU), so its items gave up waiting:
   // replay the batch again, ungated, through the device-resident path

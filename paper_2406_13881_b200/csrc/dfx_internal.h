@@ -58,6 +58,10 @@ void unpack_ops_host(const uint32_t* packed, int32_t* ops, int64_t n);
 int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate = nullptr);
 // the wide items only (no region pass): after a gated launch
 int replay_launch_wide(const ReplayDev& r, cudaStream_t stream);
+// gated only: a second launch into the block slots the gated launch leaves to
+// the region kernels, on a stream where every range is already open; it
+// shares the item queue (`next` is not reset)
+int replay_launch_backfill(const ReplayDev& r, cudaStream_t stream, const GateDev* gate);
 
 // replay class of a function: 0 narrow, 1 wide, 2 beyond the wide limits
 int fn_class(const dfx_fn_desc& d);

@@ -836,14 +836,17 @@ namespace {
 // slots -- all of C4 -- else 64-bit) or wide (Mask256, Wide traits)
 int launch_items(const ReplayDev& r, const int32_t* item_fn, const int32_t* item_chunk,
                  int n_items, int slots, unsigned* next, bool wide, cudaStream_t stream,
-                 const GateDev* gate) {
+                 const GateDev* gate, bool backfill = false) {
   if (slots < 2) slots = 2;
   if (slots > (wide ? Wide::kMaxSlots : Narrow::kMaxSlots)) return DFX_E_LIMIT;
   const int wpb = wide ? Wide::kWarps : Narrow::kWarps;
   const size_t smem = (size_t)wpb * slots * 32 * (wide ? sizeof(Wide::Prov) : sizeof(Narrow::Prov));
   const int need = (n_items + wpb - 1) / wpb;
   if (need == 0) return DFX_OK;
-  if (cudaMemsetAsync(next, 0, sizeof(unsigned), stream) != cudaSuccess) return DFX_E_CUDA;
+  // a gated launch's counter is zeroed with the gate block the caller uploads
+  // before any range opens, so a backfill launch on another stream can never
+  // see it reset
+  if (!gate && cudaMemsetAsync(next, 0, sizeof(unsigned), stream) != cudaSuccess) return DFX_E_CUDA;
   // a persistent grid (resident blocks x SMs) over the item queue
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -860,7 +863,9 @@ int launch_items(const ReplayDev& r, const int32_t* item_fn, const int32_t* item
       // ranges, 16 free slots starved the region kernels: 328 ms)
       int free_blocks = sms / 2;
       if (const char* e = getenv("DFX_GATE_FREE")) free_blocks = atoi(e);
-      blocks -= free_blocks;
+      // the backfill launch takes exactly those slots once every range is
+      // open, pulling from the same item queue
+      blocks = backfill ? free_blocks : blocks - free_blocks;
     }
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
@@ -892,6 +897,11 @@ int replay_launch(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) 
                         stream, gate);
   if (rc != DFX_OK || gate) return rc;
   return replay_launch_wide(r, stream);
+}
+
+int replay_launch_backfill(const ReplayDev& r, cudaStream_t stream, const GateDev* gate) {
+  return launch_items(r, r.item_fn, r.item_chunk, r.n_items, r.max_slots, r.next, false, stream,
+                      gate, true);
 }
 
 int replay_launch_wide(const ReplayDev& r, cudaStream_t stream) {

@@ -72,7 +72,8 @@ def _random_graph(rng, n, words):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,words,dens", [(5000, 4, 0.05), (20000, 16, 1 / 32), (3000, 128, 0.01)])
+@pytest.mark.parametrize("n,words,dens", [(5000, 4, 0.05), (20000, 16, 1 / 32), (3000, 128, 0.01),
+                                          (1500, 512, 0.004)])
 def test_cuda_b8_equals_uint16_lists(n, words, dens):
     from paper_2406_13881_b200.csr import Acc8Session, AccSession
     rng = np.random.default_rng(n + words)

@@ -1162,8 +1162,39 @@ def c5_reference_compare(n_funcs=10_000):
 _JSON_OUT = None
 
 
+def host_cpu() -> dict:
+    """The host the CPU baselines ran on: os.cpu_count(),
+    the affinity set the process may use, the /proc/cpuinfo model name."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "cpu_model": model}
+
+
+def _tag_cpu_baselines(rec, host) -> None:
+    if isinstance(rec, dict):
+        for k, v in rec.items():
+            if k == "cpu_baseline" and isinstance(v, dict) and "unavailable" not in v:
+                for hk, hv in host.items():
+                    v.setdefault(hk, hv)
+            else:
+                _tag_cpu_baselines(v, host)
+    elif isinstance(rec, list):
+        for v in rec:
+            _tag_cpu_baselines(v, host)
+
+
 def emit_line(rec) -> None:
-    """The run's one JSON line, on the process's real stdout (see main)."""
+    """The run's one JSON line, on the process's real stdout (see main).
+    Every cpu_baseline record carries the host description."""
+    _tag_cpu_baselines(rec, host_cpu())
     out = _JSON_OUT or sys.stdout
     out.write(json.dumps(rec) + "\n")
     out.flush()

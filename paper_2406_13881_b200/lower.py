@@ -38,6 +38,7 @@ ERR  kind node             statically-known error at this visit
 from __future__ import annotations
 
 import bisect
+import operator
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -45,7 +46,7 @@ import numpy as np
 from ._host import import_dartomp
 
 import_dartomp()
-from dartomp.access import AccessKind, Space, Storage, reads, writes  # noqa: E402
+from dartomp.access import AccessKind, Space, Storage  # noqa: E402
 from dartomp.bounds import (enclosing_for_loops, find_indexing_var,  # noqa: E402
                             subscript_index_vars)
 from dartomp.dataflow import compute_region_extent  # noqa: E402
@@ -127,7 +128,10 @@ def _clause_names(info, clause: str) -> set[str]:
 
 
 _JUMPS = (NodeKind.RETURN_STMT, NodeKind.BREAK_STMT, NodeKind.CONTINUE_STMT)
+_ARRAY_SUBSCRIPT = NodeKind.ARRAY_SUBSCRIPT
 # `access.reads` / `access.writes` (`access.py:44-49`) as tuples (identity tests)
+_UNKNOWN = AccessKind.UNKNOWN
+_by_name = operator.attrgetter("name")
 _READ_KINDS = (AccessKind.READ, AccessKind.READWRITE, AccessKind.UNKNOWN)
 _WRITE_KINDS = (AccessKind.WRITE, AccessKind.READWRITE, AccessKind.UNKNOWN)
 
@@ -167,14 +171,16 @@ _STMT_KINDS = frozenset({
     NodeKind.WHILE_STMT, NodeKind.DO_STMT, NodeKind.OMP_DIRECTIVE,
     NodeKind.BREAK_STMT, NodeKind.CONTINUE_STMT,
 })
+_STMT_KIND_IDS = frozenset(id(k) for k in _STMT_KINDS)   # Enum.__hash__ is Python-level
 
 
 def _enclosing_statement(ast):
     """`access.enclosing_statement` (`access.py:147-160`) with its statement-
     kind set built once instead of per call."""
     node = ast
+    kinds = _STMT_KIND_IDS
     while node is not None:
-        if node.kind in _STMT_KINDS:
+        if id(node.kind) in kinds:
             return node
         node = node.parent
     return ast
@@ -224,7 +230,7 @@ class _Lowerer:
         # (`bounds.py:160-165`) queries of Algorithm-1 finalisation
         self._write_pos: dict[int, list[int]] = {}
         for acc in accesses:
-            if writes(acc.kind):
+            if acc.kind in _WRITE_KINDS:
                 self._write_pos.setdefault(id(acc.var), []).append(acc.ast.span.start)
         for v in self._write_pos.values():
             v.sort()
@@ -344,9 +350,16 @@ class _Lowerer:
         if subscript is None:
             self.sites.extend([0, acc_code])
         else:
-            # per (statement, subscript), not per variable: each enclosing
-            # for-level's start and anchor code with its qualification bit
-            k2 = (id(access_stmt), id(subscript))
+            # per (statement, index text), not per variable: each enclosing
+            # for-level's start and anchor code with its qualification bit.
+            # The index variables depend only on the subscript's index
+            # expressions, so subscripts with the same index text (`x[i]`,
+            # `y[i]`) share one entry.
+            base = subscript
+            while base.kind is _ARRAY_SUBSCRIPT:
+                base = base.children[0]
+            itext = self.src.text[base.span.end:subscript.span.end]
+            k2 = (id(access_stmt), itext)
             levels = self._levels_cache.get(k2)
             if levels is None:
                 k = id(access_stmt)         # per statement: loop start, code, indexing var
@@ -355,10 +368,9 @@ class _Lowerer:
                     loops = self._loops_cache[k] = [
                         (f.span.start, self.norm_code(f), self.find_indexing_var(f))
                         for f in enclosing_for_loops(access_stmt, stop_at=self.fn)]
-                k = id(subscript)
-                idx_vars = self._idx_cache.get(k)
+                idx_vars = self._idx_cache.get(itext)
                 if idx_vars is None:
-                    idx_vars = self._idx_cache[k] = subscript_index_vars(subscript)
+                    idx_vars = self._idx_cache[itext] = subscript_index_vars(subscript)
                 levels = self._levels_cache[k2] = [
                     (start, code | AC_QUAL if v is not None and v in idx_vars else code)
                     for start, code, v in loops]
@@ -439,12 +451,16 @@ class _Lowerer:
             return None
         idx = self._dev_read_sub
         if idx is None:
-            idx = self._dev_read_sub = {}
-            for acc in self.accesses:
-                if (acc.space is Space.DEVICE and reads(acc.kind)
-                        and acc.subscript is not None):
-                    idx.setdefault((acc.cfg_node, id(acc.var)), acc.subscript)
+            idx = self._dev_read_subscripts()
         return idx.get((node.id, id(var)))
+
+    def _dev_read_subscripts(self) -> dict:
+        idx = self._dev_read_sub = {}
+        for acc in self.accesses:
+            if (acc.space is Space.DEVICE and acc.kind in _READ_KINDS
+                    and acc.subscript is not None):
+                idx.setdefault((acc.cfg_node, id(acc.var)), acc.subscript)
+        return idx
 
     # ---- access ops ------------------------------------------------------
     def op_hr(self, var, stmt, subscript, override):
@@ -497,20 +513,18 @@ class _Lowerer:
     def process_accesses(self, stmt, accs, override=None) -> None:
         inside = self.in_region(stmt)
         for acc in accs:
-            if acc.kind is AccessKind.UNKNOWN:
+            kind = acc.kind
+            if kind is _UNKNOWN:
                 continue
-            space = acc.space
-            if space is Space.DEVICE and not inside:
-                space = Space.HOST
-            if space is Space.HOST:
-                if reads(acc.kind):
+            if acc.space is Space.HOST or not inside:
+                if kind in _READ_KINDS:
                     self.op_hr(acc.var, stmt, acc.subscript, override)
-                if writes(acc.kind):
+                if kind in _WRITE_KINDS:
                     self.op_hw(acc.var, stmt)
             else:
-                if reads(acc.kind):
+                if kind in _READ_KINDS:
                     self.op_dr(acc.var, stmt, frozenset(), override)
-                if writes(acc.kind):
+                if kind in _WRITE_KINDS:
                     self.op_dw(acc.var, stmt)
 
     def exec_stmt(self, stmt) -> None:
@@ -550,17 +564,28 @@ class _Lowerer:
             v = self.find_indexing_var(f)
             if v is not None:
                 private.add(v)
-        for var in sorted(entry_reads, key=lambda v: v.name):
-            if var.name in private:
+        # `op_dr` / `op_dw` inline: the subscript of each variable's first
+        # device read at this kernel node (`_device_read_subscript`)
+        sub = self._dev_read_sub
+        if sub is None:
+            sub = self._dev_read_subscripts()
+        nid = node.id
+        s_stmt = self.sid(stmt)
+        ops, vid, site = self.ops, self.vid, self.site
+        for var in sorted(entry_reads, key=_by_name):
+            name = var.name
+            if name in private:
                 continue
-            if var.name in captured:
+            if name in captured:
                 self.op_hr(var, stmt, None, None)
                 continue
-            self.op_dr(var, stmt, kw, None)
-        for var in sorted(kernel_writes, key=lambda v: v.name):
-            if var.name in private or var.name in captured:
+            flags = OP_DR | F_FP if (var.is_scalar and var not in kw) else OP_DR
+            ops.append((flags, vid(var), s_stmt, site(stmt, sub.get((nid, id(var))), var)))
+        for var in sorted(kernel_writes, key=_by_name):
+            name = var.name
+            if name in private or name in captured:
                 continue
-            self.op_dw(var, stmt)
+            ops.append((OP_DW, vid(var), s_stmt, 0))
         extra = list(self.group(stmt))
         if extra:
             self.process_accesses(stmt, extra)

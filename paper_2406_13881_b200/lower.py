@@ -416,6 +416,7 @@ class _Lowerer:
         inside: dict = {}
         anc = self._decl_anc
         kid = id(kernel_ast)
+        ks, ke = kernel_ast.span.start, kernel_ast.span.end
         for acc in by.get(node_id, ()):
             var = acc.var
             k = id(var)
@@ -424,6 +425,8 @@ class _Lowerer:
                 d = var.decl
                 if d is None:
                     ins = False
+                elif d.span.start < ks or d.span.end > ke:
+                    ins = False     # a descendant's span nests in its ancestors'
                 else:
                     a = anc.get(id(d))
                     if a is None:      # the declaration and its ancestors' ids, once per function

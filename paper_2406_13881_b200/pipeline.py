@@ -1,10 +1,11 @@
 """Drop-in driver: the reference's `load` / `plan_transform` / `transform`
 (`dartomp/pipeline.py:38-105`) with the hot path swapped for the engine.
 
-The front end (lexer, parser, AST-CFG, access classification) and the
-emitter (`rewriter.apply_plans`, `report.plan_lines`) are the host package's
-own; `summarize_all` runs on kernel (c) and every function's data-flow
-analysis runs in ONE batched launch of the E1 replay kernel.
+The lexer, AST-CFG and access classification are the host package's own; the
+parser is `frontend.py`'s (the reference's tree, checked node for node in
+`tests/test_frontend.py`); `summarize_all` runs
+on kernel (c), every function's data-flow analysis runs in ONE batched launch
+of the E1 replay kernel, and the emitter is native (`emit.py`).
 
 `install()` patches a live `dartomp` in place (its `pipeline` and `cli`
 modules pick the engine up), which is how an existing user -- including
@@ -19,7 +20,6 @@ from dartomp.access import VariableTable, classify_accesses  # noqa: E402
 from dartomp.astcfg import build_astcfg  # noqa: E402
 from dartomp.lexer import expand_defines  # noqa: E402
 from dartomp.nodes import defined_functions  # noqa: E402
-from dartomp.parser import parse  # noqa: E402
 from dartomp.diagnostics import PreconditionError  # noqa: E402
 from dartomp.omp import DATA_MAPPING_KINDS  # noqa: E402
 from dartomp.pipeline import Analysis, check_transform_preconditions  # noqa: E402
@@ -27,6 +27,7 @@ from dartomp.source import SourceFile  # noqa: E402
 
 from .dataflow import analyze_function, analyze_functions  # noqa: E402
 from .emit import apply_plans, plan_lines  # noqa: E402
+from .frontend import parse, paused_gc  # noqa: E402
 from .lower import premapped_directive  # noqa: E402
 from .interproc import apply_call_effects, summarize_all  # noqa: E402
 
@@ -34,27 +35,30 @@ from .interproc import apply_call_effects, summarize_all  # noqa: E402
 def load(path: str | None = None, text: str | None = None,
          sizes: dict[str, int] | None = None, pointer_default: int = 1024,
          summary_runner=None) -> Analysis:
-    """`dartomp.pipeline.load` (`pipeline.py:38-62`) with kernel (c)."""
-    if text is not None:
-        src = SourceFile.from_text(text, path=path or "<string>")
-    else:
-        src = SourceFile.from_path(path)
-    pre = expand_defines(src)
-    tu, pwarnings = parse(src, pre)
-    table = VariableTable(src, tu, sizes=sizes, pointer_default=pointer_default)
-    warnings = list(pre.warnings) + list(pwarnings)
-    cfgs, raw = {}, {}
-    for name, fn in defined_functions(tu).items():
-        cfg = build_astcfg(src, fn)
-        cfgs[name] = cfg
-        warnings.extend(cfg.warnings)
-        raw[name] = classify_accesses(src, cfg, table)
-    summaries = summarize_all(src, tu, cfgs, raw, table, runner=summary_runner)
-    expanded = {name: apply_call_effects(src, cfgs[name], raw[name], summaries, table)
-                for name in cfgs}
-    return Analysis(src=src, tu=tu, table=table, cfgs=cfgs, raw_accesses=raw,
-                    accesses=expanded, summaries=summaries,
-                    defines=dict(pre.defines), warnings=warnings)
+    """`dartomp.pipeline.load` (`pipeline.py:38-62`) with kernel (c), the
+    drop-in parser (`frontend.py`: the reference's tree by precedence
+    climbing) and the cyclic collector paused for the call."""
+    with paused_gc():
+        if text is not None:
+            src = SourceFile.from_text(text, path=path or "<string>")
+        else:
+            src = SourceFile.from_path(path)
+        pre = expand_defines(src)
+        tu, pwarnings = parse(src, pre)
+        table = VariableTable(src, tu, sizes=sizes, pointer_default=pointer_default)
+        warnings = list(pre.warnings) + list(pwarnings)
+        cfgs, raw = {}, {}
+        for name, fn in defined_functions(tu).items():
+            cfg = build_astcfg(src, fn)
+            cfgs[name] = cfg
+            warnings.extend(cfg.warnings)
+            raw[name] = classify_accesses(src, cfg, table)
+        summaries = summarize_all(src, tu, cfgs, raw, table, runner=summary_runner)
+        expanded = {name: apply_call_effects(src, cfgs[name], raw[name], summaries, table)
+                    for name in cfgs}
+        return Analysis(src=src, tu=tu, table=table, cfgs=cfgs, raw_accesses=raw,
+                        accesses=expanded, summaries=summaries,
+                        defines=dict(pre.defines), warnings=warnings)
 
 
 def _precheck(analysis: Analysis, names: list):

@@ -686,7 +686,18 @@ def run_api_record(args):
     # C4-style functions from C source at the reference API
     n = args.api_funcs
     text = generate(7, GenConfig(n_funcs=n, n_globals=24, n_stmts=40, p_kernel=0.3))
+    # the front end at scale: the reference `load` against the
+    # drop-in's (its parser and the paused collector), one run each
+    t0 = time.perf_counter()
     a = ref.load(text=text)
+    t_load_ref = 1e3 * (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    a_eng = eng.load(text=text)
+    t_load_eng = 1e3 * (time.perf_counter() - t0)
+    same_units = (list(a_eng.cfgs) == list(a.cfgs)
+                  and sum(len(v) for v in a_eng.accesses.values())
+                  == sum(len(v) for v in a.accesses.values()))
+    del a_eng
     eng.plan_transform(a)                                      # warm
     t_ref, p_ref = med(lambda: ref.plan_transform(a), 2)
     t_eng, p_eng = med(lambda: eng.plan_transform(a), 3)
@@ -699,6 +710,9 @@ def run_api_record(args):
                                     "%d lines" % (len(a.cfgs), len(text.splitlines())),
                         "reference_plan_transform_ms": t_ref, "dropin_plan_transform_ms": t_eng,
                         "speedup": t_ref / t_eng, "identical_plans": key(p_ref) == key(p_eng),
+                        "load": {"reference_ms": t_load_ref, "dropin_ms": t_load_eng,
+                                 "speedup": t_load_ref / t_load_eng,
+                                 "same_functions_and_accesses": same_units},
                         "lowering_workers": int(os.environ.get("DFX_LOWER_WORKERS", "0"))
                         or min(16, os.cpu_count() or 1)}
     rec.update(host_info())

@@ -27,6 +27,7 @@ import gc
 from ._host import import_dartomp
 
 import_dartomp()
+from dartomp.diagnostics import Diagnostic  # noqa: E402
 from dartomp.lexer import Preprocessed, TokenKind, expand_defines  # noqa: E402
 from dartomp.nodes import AstNode, NodeKind  # noqa: E402
 from dartomp.parser import Parser  # noqa: E402
@@ -43,6 +44,39 @@ class ClimbingParser(Parser):
     """`Parser` with `parse_logical_or` (the entry of the binary levels,
     called only from `parse_assignment`, `parser.py:455`) by precedence
     climbing."""
+
+    def parse_translation_unit(self) -> AstNode:
+        """`Parser.parse_translation_unit` (`parser.py:92-113`) with the
+        parent links set by an explicit pre-order walk: `link_parents`
+        (`nodes.py:193-196`) walks the whole unit through nested generators
+        (`AstNode.walk`, `nodes.py:108-111`), one generator frame per level
+        per node."""
+        start = self.peek().span.start if not self.at_end() else 0
+        children: list = []
+        while not self.at_end():
+            t = self.peek()
+            if t.kind is TokenKind.PRAGMA:
+                self.warnings.append(Diagnostic(
+                    self.src.path, t.line, 1, "warning",
+                    "pragma outside any function ignored"))
+                self.advance()
+                continue
+            if t.lexeme == "struct" and self.peek(2) is not None and self.check("{", 2):
+                children.append(self.parse_struct_decl())
+                continue
+            children.append(self.parse_external_decl())
+        end = self.toks[-1].span.end if self.toks else start
+        tu = AstNode(NodeKind.TRANSLATION_UNIT, Span(0, max(end, len(self.src.text))), children)
+        stack = [tu]                # the pre-order of `walk`, so a shared child ends the same
+        pop, extend = stack.pop, stack.extend
+        while stack:
+            node = pop()
+            ch = node.children
+            if ch:
+                for c in ch:
+                    c.parent = node
+                extend(reversed(ch))
+        return tu
 
     def parse_logical_or(self) -> AstNode:
         return self._climb(1)

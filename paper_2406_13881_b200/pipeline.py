@@ -3,9 +3,9 @@
 
 The lexer, AST-CFG and access classification are the host package's own; the
 parser is `frontend.py`'s (the reference's tree, checked node for node in
-`tests/test_frontend.py`); `summarize_all` runs
-on kernel (c), every function's data-flow analysis runs in ONE batched launch
-of the E1 replay kernel, and the emitter is native (`emit.py`).
+`tests/test_frontend.py`); `summarize_all` runs on kernel (c), every
+function's data-flow analysis runs in ONE batched launch of the E1 replay
+kernel, and the emitter is native (`emit.py`).
 
 `install()` patches a live `dartomp` in place (its `pipeline` and `cli`
 modules pick the engine up), which is how an existing user -- including
@@ -122,9 +122,10 @@ def transform(analysis: Analysis, allow_stale: frozenset[str] = frozenset(),
 
 def install() -> None:
     """Route an imported `dartomp` through the engine (plugin drop-in): the
-    analysis (E1), the summaries (kernel c), the emitter (native), and the
-    CLI's `compare` (the CUDA transfer simulator; its comparison lines are the
-    reference's byte for byte).  `simulate_analysis` (the CLI's `simulate`
+    analysis (E1), the summaries (kernel c), `load` (its parser and paused
+    collector, `frontend.py`), the emitter (native), and the CLI's `compare`
+    (the CUDA transfer simulator; its comparison lines are the reference's
+    byte for byte).  `simulate_analysis` (the CLI's `simulate`
     mode, whose verbose log lists the reference's per-round records) stays the
     reference's."""
     import dartomp.cli as cli
@@ -139,11 +140,13 @@ def install() -> None:
     pl.analyze_function = analyze_function
     pl.summarize_all = summarize_all
     pl.plan_transform = plan_transform
+    pl.load = load
     pl.transform = transform
     pl.apply_plans = apply_plans
     pl.compare = compare
     rw.apply_plans = apply_plans
     rp.plan_lines = plan_lines
+    cli.load = load
     cli.transform = transform
     cli.plan_lines = plan_lines
     cli.compare = compare

@@ -228,6 +228,7 @@ replay_one(int item, WarpCtl<M, P>& c, typename P::Prov* prov, int lane, const d
   L.presence = L.to_comp = L.from_comp = 0;
   L.halted = !active;
   int cur = c.cur;
+  __syncwarp();         // as after every read of the warp's shared control block
   int record = 1;
   // visit counter (`_Analyzer` op order, the event key) of the op at pc is
   // sbase + pc + 1: it advances with pc, and sbase absorbs the jumps (loop
@@ -463,6 +464,7 @@ replay_one(int item, WarpCtl<M, P>& c, typename P::Prov* prov, int lane, const d
         }
         __syncwarp();
         cur = c.cur;
+        __syncwarp();   // every lane has read c.cur before lane 0 writes it again (racecheck)
         break;
       }
       case DFX_OP_LOOP_BEGIN: {  // _loop_rounds: entry = state.copy(); dry round

@@ -1847,6 +1847,11 @@ int cg_setup(dfx_handle* h, const dfx_cg_in* in, const int32_t* wave_off, const 
     if (rc0) return fail(DFX_E_CUDA, "dfx_summaries: repitch failed");
   }
   if (nf) CK(cudaMemcpyAsync(R.tn[0], in->init_len, sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+  // the solve writes a row's list only up to its length; the download reads
+  // whole rows (the host keeps the first len entries), so the second table
+  // starts defined (a few MB; compute-sanitizer initcheck)
+  CK(cudaMemsetAsync(R.tb[1], 0, rows * nsp, st));
+  CK(cudaMemsetAsync(R.tl[1], 0, sizeof(int16_t) * rows * nsp, st));
   CK(cudaMemcpyAsync(d_srcoff, in->src_off, sizeof(int32_t) * (size_t)(nf + 1), cudaMemcpyHostToDevice, st));
   if (in->n_src) CK(cudaMemcpyAsync(d_src, in->src, sizeof(int32_t) * 4 * (size_t)in->n_src, cudaMemcpyHostToDevice, st));
   if (in->n_slist) CK(cudaMemcpyAsync(d_slist, in->slist, sizeof(int16_t) * (size_t)in->n_slist, cudaMemcpyHostToDevice, st));

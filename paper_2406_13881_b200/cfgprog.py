@@ -45,6 +45,7 @@ import numpy as np
 
 from ._host import import_dartomp
 from .csr import ACC_READ, ACC_WRITE, REQ_FP_FLAG, AccSession, CsrProblem
+from .frontend import paused_gc
 from .lower import (_clause_names, _enclosing_statement, _for_stmts, _Lowerer,
                     _READ_KINDS, _WRITE_KINDS)
 
@@ -195,7 +196,13 @@ def lower_program(items) -> CfgProgram:
     a chain of graph nodes when its statement mixes host and device ops
     (a call whose callee offloads, a firstprivate capture at a kernel): the
     chain's first node takes the CFG node's predecessors, its last node
-    feeds the CFG node's successors."""
+    feeds the CFG node's successors.  The cyclic collector is paused for the
+    call (`frontend.paused_gc`)."""
+    with paused_gc():
+        return _lower_program(items)
+
+
+def _lower_program(items) -> CfgProgram:
     parts = []
     for name, src, cfg, accesses, table in items:
         fg = FnGraph(name=name, cfg=cfg)
